@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark: text scanned GB/s on B200 (BASELINE.json `metric`), one JSON line.
+
+Workload (BASELINE.json configs[1], "C2"): 1 GiB of synthetic printable-ASCII text per
+GPU (the reference generator, seed 42, produced on the device), single-pattern scans for
+the pattern-length sweep m = 4, 8, 16, 32, 64, 128, 256, 512, 1024 (patterns sampled
+from the corpus as rkmatch.bench._make_pattern does).  One step = the whole sweep, i.e.
+9 full scans of the text; value = text bytes scanned by all ranks / device time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one rank per GPU: weak scaling, each rank owns 1 GiB of the
+global N GiB corpus plus an (m-1)-byte halo, scans it, and the global ordered position
+list is returned with NCCL all_gather.  `--impl reference` times the reference
+algorithm (the C restatement in oracle/ of rkmatch._scan_range + search_parallel's range
+partition) on the host cores on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "text scanned GB/s (device-timed) at 1/2/4/8 B200 vs HBM roofline; host-CPU ref GB/s"
+SWEEP = (4, 8, 16, 32, 64, 128, 256, 512, 1024)
+ASCII = bytes(range(32, 127))
+SEED = 42
+GiB = 1 << 30
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--bytes-per-gpu", type=int, default=GiB)
+    ap.add_argument("--sweep", type=str, default=",".join(map(str, SWEEP)))
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------- helpers
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """SM clock + throttle reasons via NVML, sampled during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device: int):
+        self.samples: list[int] = []
+        self.reasons: int = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def sampled_offset(n_total: int, m: int) -> int:
+    """rkmatch.bench._make_pattern 'sampled' position (bench.py:112-114)."""
+    from paper_1810_01051_b200.datagen import splitmix64
+
+    draw, _ = splitmix64(SEED ^ 0xA5A5A5A5A5A5A5A5)
+    return draw % (n_total - m + 1)
+
+
+# ------------------------------------------------------------------------- CPU arm
+def cpu_rates(text: np.ndarray, patterns: dict, seconds: float, threads: int):
+    """Time the reference algorithm (oracle C port of _scan_range + search_parallel's
+    range partition) on prefixes sized for ~seconds/len(patterns) each."""
+    import oracle
+
+    per = seconds / len(patterns)
+    sec_per_byte = 0.0  # equal bytes per m, as in the GPU sweep: harmonic combination
+    sample = {}
+    for m, pat in patterns.items():
+        p = np.frombuffer(pat, dtype=np.uint8)
+        size = 1 << 20
+        while True:
+            t0 = time.perf_counter()
+            oracle.c_scan(text[:size], p, workers=threads)
+            dt = time.perf_counter() - t0
+            if dt >= per * 0.5 or size >= text.size:
+                break
+            size = int(min(text.size, size * max(2.0, per / max(dt, 1e-4))))
+        sec_per_byte += dt / size
+        sample[m] = size
+    return len(patterns) / sec_per_byte / 1e9, sample
+
+
+def cpu_fixed(text, patterns, sizes, threads):
+    import oracle
+
+    sec_per_byte = 0.0
+    t_all = 0.0
+    for m, pat in patterns.items():
+        t0 = time.perf_counter()
+        oracle.c_scan(text[: sizes[m]], np.frombuffer(pat, dtype=np.uint8), workers=threads)
+        dt = time.perf_counter() - t0
+        t_all += dt
+        sec_per_byte += dt / sizes[m]
+    return sec_per_byte, t_all
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on the host cores, same metric."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    sweep = [int(x) for x in args.sweep.split(",")]
+    threads = oracle.cpu_threads()
+    n = 256 << 20
+    text = np.frombuffer(oracle.generate(SEED, n, ASCII), dtype=np.uint8)
+    pats = {m: text[sampled_offset(n, m): sampled_offset(n, m) + m].tobytes() for m in sweep}
+    # per-step sample sizes so that the run (warmup + steps) stays within minutes
+    budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    _, sizes = cpu_rates(text, pats, budget, threads)
+    for _ in range(args.warmup):
+        cpu_fixed(text, pats, sizes, threads)
+    times = []
+    spb = 0.0
+    for _ in range(args.steps):
+        sb, dt = cpu_fixed(text, pats, sizes, threads)
+        times.append(dt)
+        spb += sb
+    total = sum(times)
+    # equal bytes per pattern length (the GPU sweep's weighting): harmonic combination
+    gbs = len(sweep) * args.steps / spb / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "C2 single-pattern length sweep, printable ASCII (seed 42)",
+                   "sweep": sweep, "sample_bytes_per_m": sizes},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"prefixes {sizes} of the 1 GiB C2 corpus, per step"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1810_01051_b200 as rk
+    from paper_1810_01051_b200 import _lib, sharded
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+    sweep = [int(x) for x in args.sweep.split(",")]
+    per = args.bytes_per_gpu
+    n_total = per * world
+    mmax = max(sweep)
+    spec = rk.DnaSpec(SEED, n_total, ASCII)
+
+    # this rank's bytes: [rank*per, rank*per + per + mmax - 1) ∩ [0, n_total)
+    byte_lo = rank * per
+    byte_hi = min(n_total, byte_lo + per + mmax - 1)
+    text = rk.generate_tensor(spec, device=f"cuda:{dev}", skip=byte_lo, count=byte_hi - byte_lo)
+    pats, plans = {}, {}
+    for m in sweep:
+        x = sampled_offset(n_total, m)
+        pats[m] = rk.generate_tensor(spec, device=f"cuda:{dev}", skip=x, count=m).cpu().numpy().tobytes()
+        a, b, blo, bhi = sharded.weak_shard(rank, per, n_total, m)
+        plans[m] = (a - byte_lo, b - byte_lo, rk.hash_full(pats[m]))
+    L = _lib.lib()
+    ctx = _lib.context(dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    cap = 1 << 22
+    outs = {m: torch.empty(cap, dtype=torch.int64, device=f"cuda:{dev}") for m in sweep}
+    counts = torch.zeros((len(sweep), 3), dtype=torch.int64, device=f"cuda:{dev}")
+    pat_bufs = {m: np.frombuffer(pats[m], dtype=np.uint8) for m in sweep}
+    n_local = int(text.numel())
+
+    def step(ev_pairs=None):
+        for i, m in enumerate(sweep):
+            a, b, hx = plans[m]
+            if ev_pairs is not None:
+                ev_pairs[i][0].record(stream)
+            _lib.check(L.rk_scan_async(ctx.handle, text.data_ptr(), n_local, pat_bufs[m].ctypes.data,
+                                       m, hx, a, b, outs[m].data_ptr(), cap, byte_lo,
+                                       counts[i].data_ptr(), sptr))
+            if ev_pairs is not None:
+                ev_pairs[i][1].record(stream)
+        if world > 1:
+            # the exchange: counts, then positions padded to the max count, over NVLink
+            for i, m in enumerate(sweep):
+                k = counts[i, 0:1]
+                allk = [torch.empty_like(k) for _ in range(world)]
+                dist.all_gather(allk, k)
+                kmax = int(torch.stack(allk).max().item())
+                if kmax:
+                    parts = [torch.empty(kmax, dtype=torch.int64, device=k.device) for _ in range(world)]
+                    dist.all_gather(parts, outs[m][:kmax])
+        return counts
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    # correctness gate: every ordered list is what a second pass gives, and counts add up
+    host_counts = counts.cpu().numpy()
+    assert (host_counts[:, 1] == host_counts[:, 0] + host_counts[:, 2]).all()
+
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in sweep] for _ in range(args.steps)]
+    launches0 = ctx.launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        start.record(stream)
+        for s in range(args.steps):
+            step(ev[s])
+        end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launches - launches0
+    elapsed_ms = start.elapsed_time(end)
+    per_m_ms = {m: sum(ev[s][i][0].elapsed_time(ev[s][i][1]) for s in range(args.steps)) / args.steps
+                for i, m in enumerate(sweep)}
+    t_all = torch.tensor([elapsed_ms], dtype=torch.float64, device=f"cuda:{dev}")
+    if world > 1:
+        dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t_all.item())
+    host_counts = counts.cpu().numpy()
+    bytes_per_step_rank = sum(plans[m][1] - plans[m][0] + m - 1 for m in sweep)
+    windows_all = sum(max(n_total - m + 1, 0) for m in sweep)
+    value = windows_all / (elapsed_ms / args.steps / 1e3) / 1e9  # text (window) bytes/s
+
+    # roofline of the scan kernel: algorithmic bytes = n + 8*matches per launch
+    peak, peak_kind = load_peaks()
+    alg = [(plans[m][1] - plans[m][0] + m - 1) + 8 * int(host_counts[i, 0]) for i, m in enumerate(sweep)]
+    achieved = sum(alg) / (sum(per_m_ms.values()) / 1e3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "dram_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---------------------------------------------------------------- e2e (host API)
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 3)
+    e2e = None
+    if e2e_steps > 0:
+        host = text.cpu().pin_memory()
+        h_out = torch.empty(cap, dtype=torch.int64).pin_memory()
+        mt, co, hh = _lib.u64ref(), _lib.u64ref(), _lib.u64ref()
+        h2d = d2h = 0
+
+        def e2e_step():
+            nonlocal h2d, d2h
+            got = []
+            for m in sweep:
+                a, b, hx = plans[m]
+                _lib.check(L.rk_scan_host(ctx.handle, host.data_ptr(), n_local, pat_bufs[m].ctypes.data,
+                                          m, hx, a, b, h_out.data_ptr(), cap, ctypes.byref(mt),
+                                          ctypes.byref(co), ctypes.byref(hh)))
+                h2d += (b - a) + m - 1
+                d2h += 8 * min(int(mt.value), cap) + 24
+                got.append(int(mt.value))
+            return got
+
+        got = e2e_step()
+        assert got == [int(v) for v in host_counts[:, 0]], (got, host_counts[:, 0])
+        h2d = d2h = 0
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        t_e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{dev}")
+        if world > 1:
+            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+        e2e = {"value": windows_all / (float(t_e2e.item()) / e2e_steps) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
+               "steps": e2e_steps, "api": "rk_scan_host (pinned host text -> HBM chunks -> scan -> host offsets)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+
+        threads = oracle.cpu_threads()
+        host_text = text[: 256 << 20].cpu().numpy()
+        rate, sample = cpu_rates(host_text, {m: pats[m] for m in sweep}, args.cpu_seconds, threads)
+        cpu = {"value": rate, "unit": "GB/s", "cores": threads, "kind": "port",
+               "sample": f"prefixes of the C2 corpus per m: {sample} bytes (oracle C port of "
+                         f"_scan_range + search_parallel ranges, {threads} threads)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (rkmatch generator, on device)",
+            "config": {"workload": "C2: single-pattern length sweep over 1 GiB printable-ASCII "
+                                   "text per GPU (BASELINE.json configs[1])",
+                       "bytes_per_gpu": per, "sweep": sweep, "pattern_source": "sampled",
+                       "corpus": "DnaSpec(42, N GiB, bytes(32..126))",
+                       "l2": "inputs larger than L2 (1 GiB per GPU vs 126 MB)",
+                       "parallelism": f"shard{world} (contiguous, (m-1)-byte halo)"},
+            "per_m_gbs": {str(m): (plans[m][1] - plans[m][0] + m - 1) / (per_m_ms[m] / 1e3) / 1e9
+                          for m in sweep},
+            "matches_per_m": {str(m): int(host_counts[i, 0]) for i, m in enumerate(sweep)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_kind": peak_kind, "kernel": "rk_scan_kernel<M>",
+                         "algorithmic_bytes": "n + 8*matches per launch"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

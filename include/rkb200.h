@@ -1,0 +1,127 @@
+/*
+ * rkb200.h -- C ABI of the B200-native Rabin-Karp scan (librkb200.so).
+ *
+ * The drop-in seam is the reference's scan module, rkmatch._scan
+ * (/root/reference/pkg/src/rkmatch/_scan.py), which the search API
+ * (matcher.py, parallel.py) calls directly.  Every entry point below replaces one
+ * reference function; the Python host layer (paper_1810_01051_b200/) binds them with
+ * ctypes and keeps the reference's public signatures, validation order and exceptions.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  `d_` pointers are device memory of the context's
+ *     device, `h_` pointers are host memory (pinned or pageable).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
+ *   - Every function returns 0 on success, RK_EINVAL for argument errors (the Python
+ *     layer maps it to ValueError), RK_ECUDA for CUDA failures (RuntimeError).
+ *     rk_last_error() returns the calling thread's last message.
+ *   - A context owns per-device scratch (look-back status, tickets, staging buffers).
+ *     Calls on one context must not run concurrently; use one context per stream.
+ *   - Hash: h = sum b_i * 2^(m-1-i) mod 2^64 (rkhash.py:21-28).  Window x covers text
+ *     bytes [x, x+m).  Offsets are 0-based int64, strictly ascending.
+ */
+#ifndef RKB200_H
+#define RKB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RK_OK 0
+#define RK_EINVAL 1
+#define RK_ECUDA 2
+
+typedef struct rk_ctx rk_ctx_t;
+
+/* Library identification ("rkb200 <version> sm_100a"). */
+const char* rk_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+const char* rk_last_error(void);
+/* Number of visible CUDA devices (0 when no driver/GPU). */
+int rk_device_count(void);
+
+/* Create / destroy a scan context bound to `device`. */
+int rk_ctx_create(int device, rk_ctx_t** out);
+int rk_ctx_destroy(rk_ctx_t* ctx);
+
+/*
+ * rk_scan -- replaces _scan_range (_scan.py:28-50) and scan (_scan.py:53-68).
+ * Scans windows x in [start, stop) of the device text (n bytes) for the m-byte host
+ * pattern whose 64-bit hash the caller passes as hx (the reference passes hx the same
+ * way, hash_pattern_host parallel.py:104-108).  Writes the first min(matches, cap)
+ * matching window starts, ascending, to d_out and returns the true totals:
+ *   *matches    windows whose hash equals hx AND whose bytes equal the pattern
+ *   *collisions windows whose hash equals hx but whose bytes differ
+ *   *hash_hits  matches + collisions (ScanStats.hash_hits, matcher.py:45-55)
+ * Requires stop + m - 1 <= n.  A caller seeing matches > cap may call again with a
+ * larger buffer (the reference's overflow protocol, _scan.py:64-67).  Blocks the host
+ * until the result is known.
+ */
+int rk_scan(rk_ctx_t* ctx, const uint8_t* d_text, uint64_t n, const uint8_t* h_pattern,
+            uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t* d_out,
+            uint64_t cap, uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits,
+            void* stream);
+
+/*
+ * rk_scan_async -- rk_scan without the host synchronisation: enqueues the scan on
+ * `stream`; `out_bias` is added to every written offset (shard / staging origin).
+ * If d_counts (device, 3 x u64) is non-NULL, {matches, hash_hits, collisions} are
+ * copied there on the stream; rk_scan_result() returns the totals of the last scan of
+ * this context to the host.
+ */
+int rk_scan_async(rk_ctx_t* ctx, const uint8_t* d_text, uint64_t n, const uint8_t* h_pattern,
+                  uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t* d_out,
+                  uint64_t cap, int64_t out_bias, uint64_t* d_counts, void* stream);
+int rk_scan_result(rk_ctx_t* ctx, uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits,
+                   void* stream);
+
+/*
+ * rk_scan_host -- the end-to-end path for a HOST text (search_sequential /
+ * search_parallel called with bytes, matcher.py:101-122, parallel.py:124-177).  The text
+ * is staged into HBM in chunks with cudaMemcpyAsync on a copy stream (through an
+ * internal pinned ring when h_text is pageable), each chunk scanned as soon as it lands
+ * while the next one is in flight, and the ordered offsets are copied into h_out
+ * (first min(matches, cap)).  Synchronous.
+ */
+int rk_scan_host(rk_ctx_t* ctx, const uint8_t* h_text, uint64_t n, const uint8_t* h_pattern,
+                 uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t* h_out,
+                 uint64_t cap, uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits);
+/* Copies offsets [first, first+count) of the last rk_scan_host of this context (all of
+ * them are kept on the device, so a caller whose cap was too small never rescans). */
+int rk_scan_host_fetch(rk_ctx_t* ctx, int64_t* h_out, uint64_t first, uint64_t count);
+
+/*
+ * rk_multi_scan -- one equal-length group of search_multi (matcher.py:139-153).
+ * h_patterns holds P deduplicated patterns of length m back to back (PatternSet order,
+ * matcher.py:66-84), h_hashes their hash_full values.  Writes up to cap (offset, index)
+ * pairs, ordered by (pattern index, offset) -- the reference's per-pattern ascending
+ * lists -- and returns the number of pairs.  Requires 1 <= P <= RK_MULTI_MAX_PATTERNS.
+ */
+#define RK_MULTI_MAX_PATTERNS 4096
+int rk_multi_scan(rk_ctx_t* ctx, const uint8_t* d_text, uint64_t n, const uint8_t* h_patterns,
+                  uint32_t P, uint32_t m, const uint64_t* h_hashes, int64_t* d_off,
+                  uint32_t* d_idx, uint64_t cap, uint64_t* pairs, void* stream);
+
+/*
+ * rk_window_hashes -- _scan.py:71-91: d_out[x - start] = hash of window x for
+ * x in [start, stop).  Requires stop - 1 + m <= n.
+ */
+int rk_window_hashes(rk_ctx_t* ctx, const uint8_t* d_text, uint64_t n, uint32_t m,
+                     uint64_t start, uint64_t stop, uint64_t* d_out, void* stream);
+
+/*
+ * rk_generate -- datagen.generate on device (datagen.py:68-77 with the counter form of
+ * splitmix64_stream, datagen.py:37-48): d_out[i] = alphabet[z_{skip+i+1} mod k].
+ */
+int rk_generate(rk_ctx_t* ctx, uint8_t* d_out, uint64_t count, uint64_t seed, uint64_t skip,
+                const uint8_t* h_alphabet, uint32_t k, void* stream);
+
+/* Number of kernel launches issued by this context so far (bench accounting). */
+uint64_t rk_launch_count(rk_ctx_t* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RKB200_H */

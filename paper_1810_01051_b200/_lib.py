@@ -1,0 +1,157 @@
+"""ctypes binding of librkb200.so (include/rkb200.h) and per-device contexts.
+
+There is no fallback: if the library is missing, or no sm_100 device is visible, every
+search entry point raises.  (The CPU oracle under ``oracle/`` is test infrastructure and
+is never imported from here.)
+"""
+
+from __future__ import annotations
+
+import atexit
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "librkb200.so"
+
+RK_OK, RK_EINVAL, RK_ECUDA = 0, 1, 2
+MULTI_MAX_PATTERNS = 4096
+
+# every symbol include/rkb200.h declares (checked by tests/test_capi.py)
+EXPORTS = (
+    "rk_version", "rk_last_error", "rk_device_count", "rk_ctx_create", "rk_ctx_destroy",
+    "rk_scan", "rk_scan_async", "rk_scan_result", "rk_scan_host", "rk_scan_host_fetch",
+    "rk_multi_scan", "rk_window_hashes", "rk_generate", "rk_launch_count",
+)
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def _declare(lib: ctypes.CDLL) -> None:
+    u8p = ctypes.c_void_p
+    u64 = ctypes.c_uint64
+    u32 = ctypes.c_uint32
+    i64 = ctypes.c_int64
+    pu64 = ctypes.POINTER(ctypes.c_uint64)
+    vp = ctypes.c_void_p
+    ci = ctypes.c_int
+    lib.rk_version.restype = ctypes.c_char_p
+    lib.rk_version.argtypes = []
+    lib.rk_last_error.restype = ctypes.c_char_p
+    lib.rk_last_error.argtypes = []
+    lib.rk_device_count.restype = ci
+    lib.rk_device_count.argtypes = []
+    lib.rk_ctx_create.restype = ci
+    lib.rk_ctx_create.argtypes = [ci, ctypes.POINTER(vp)]
+    lib.rk_ctx_destroy.restype = ci
+    lib.rk_ctx_destroy.argtypes = [vp]
+    lib.rk_scan.restype = ci
+    lib.rk_scan.argtypes = [vp, u8p, u64, u8p, u32, u64, u64, u64, vp, u64, pu64, pu64, pu64, vp]
+    lib.rk_scan_async.restype = ci
+    lib.rk_scan_async.argtypes = [vp, u8p, u64, u8p, u32, u64, u64, u64, vp, u64, i64, vp, vp]
+    lib.rk_scan_result.restype = ci
+    lib.rk_scan_result.argtypes = [vp, pu64, pu64, pu64, vp]
+    lib.rk_scan_host.restype = ci
+    lib.rk_scan_host.argtypes = [vp, u8p, u64, u8p, u32, u64, u64, u64, vp, u64, pu64, pu64, pu64]
+    lib.rk_scan_host_fetch.restype = ci
+    lib.rk_scan_host_fetch.argtypes = [vp, vp, u64, u64]
+    lib.rk_multi_scan.restype = ci
+    lib.rk_multi_scan.argtypes = [vp, u8p, u64, u8p, u32, u32, vp, vp, vp, u64, pu64, vp]
+    lib.rk_window_hashes.restype = ci
+    lib.rk_window_hashes.argtypes = [vp, u8p, u64, u32, u64, u64, vp, vp]
+    lib.rk_generate.restype = ci
+    lib.rk_generate.argtypes = [vp, vp, u64, u64, u64, u8p, u32, vp]
+    lib.rk_launch_count.restype = u64
+    lib.rk_launch_count.argtypes = [vp]
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build it with `python -m paper_1810_01051_b200._build`"
+                    " (or __graft_entry__.build()); there is no CPU fallback"
+                )
+            L = ctypes.CDLL(str(LIB_PATH))
+            _declare(L)
+            _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == RK_OK:
+        return
+    msg = lib().rk_last_error().decode("utf-8", "replace")
+    if rc == RK_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(f"librkb200: {msg}")
+
+
+class Context:
+    """One rk_ctx_t (per-device scratch: look-back status, tickets, staging rings)."""
+
+    def __init__(self, device: int):
+        self.device = device
+        h = ctypes.c_void_p()
+        check(lib().rk_ctx_create(device, ctypes.byref(h)))
+        self.handle = h
+        self.lock = threading.Lock()
+
+    def close(self) -> None:
+        if self.handle:
+            lib().rk_ctx_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    @property
+    def launches(self) -> int:
+        return int(lib().rk_launch_count(self.handle))
+
+
+_ctx: dict[int, Context] = {}
+_ctx_lock = threading.Lock()
+
+
+def default_device() -> int:
+    env = os.environ.get("RKB200_DEVICE")
+    if env is not None:
+        return int(env)
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:  # pragma: no cover - torch always present in this image
+        pass
+    return 0
+
+
+def context(device: int | None = None) -> Context:
+    if device is None:
+        device = default_device()
+    with _ctx_lock:
+        c = _ctx.get(device)
+        if c is None:
+            c = Context(device)
+            _ctx[device] = c
+        return c
+
+
+@atexit.register
+def _close_all() -> None:  # pragma: no cover
+    for c in list(_ctx.values()):
+        try:
+            c.close()
+        except Exception:
+            pass
+    _ctx.clear()
+
+
+def u64ref(v: int = 0):
+    return ctypes.c_uint64(v)

@@ -1,0 +1,172 @@
+"""Scan module -- the drop-in for rkmatch._scan (/root/reference/pkg/src/rkmatch/_scan.py).
+
+Same three functions, same arguments and errors, backed by librkb200.so:
+
+* ``as_u8(data)``        _scan.py:17-25 (also accepts 1-D uint8 torch tensors, CPU or CUDA)
+* ``scan(text, pattern, hx, start, stop)``   _scan.py:53-68 -> (int64 offsets, collisions)
+* ``window_hashes(text, m, start, stop)``    _scan.py:71-91 -> uint64 hashes
+
+Host inputs go through ``rk_scan_host`` (chunked pinned staging into HBM overlapped with
+the scan); CUDA tensors go straight to ``rk_scan`` on the current torch stream and give
+CUDA results.  There is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+_INITIAL_CAPACITY = 1 << 16  # offsets returned without a second pass (reference: 4096)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _is_tensor(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def as_u8(data):
+    """View bytes-like input as a uint8 array without copying (_scan.py:17-25).
+
+    bytes / bytearray / memoryview -> np.frombuffer; uint8 ndarray -> contiguous;
+    1-D uint8 torch tensor -> contiguous tensor (kept on its device).  Anything else is
+    a TypeError, as in the reference."""
+    if isinstance(data, np.ndarray):
+        if data.dtype != np.uint8:
+            raise TypeError(f"expected uint8 array, got {data.dtype}")
+        return np.ascontiguousarray(data).reshape(-1)
+    if isinstance(data, (bytes, bytearray, memoryview)):
+        return np.frombuffer(data, dtype=np.uint8)
+    if _is_tensor(data):
+        torch = _torch()
+        if data.dtype != torch.uint8:
+            raise TypeError(f"expected uint8 tensor, got {data.dtype}")
+        return data.contiguous().reshape(-1)
+    raise TypeError(f"expected bytes-like input, got {type(data).__name__}")
+
+
+def _size(t) -> int:
+    return int(t.numel()) if _is_tensor(t) else int(t.size)
+
+
+def _host_bytes(p) -> np.ndarray:
+    if _is_tensor(p):
+        return p.detach().to("cpu").contiguous().numpy()
+    return np.ascontiguousarray(p, dtype=np.uint8)
+
+
+def _device_of(t) -> int | None:
+    if _is_tensor(t) and t.is_cuda:
+        return t.device.index if t.device.index is not None else _torch().cuda.current_device()
+    return None
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data if a.size else 0
+
+
+def scan_counts(text, pattern, hx: int, start: int, stop: int, *, out_bias: int = 0):
+    """Core call: (offsets, matches, collisions, hash_hits) for windows [start, stop).
+
+    ``offsets`` is an int64 ndarray for host text and an int64 CUDA tensor for CUDA
+    text, holding all matches in ascending order."""
+    L = _lib.lib()
+    p = _host_bytes(pattern)
+    m = int(p.size)
+    n = _size(text)
+    hx = int(hx) & ((1 << 64) - 1)
+    mt, co, hh = _lib.u64ref(), _lib.u64ref(), _lib.u64ref()
+    dev = _device_of(text)
+    if dev is None:
+        t = text if isinstance(text, np.ndarray) else _host_bytes(text)
+        ctx = _lib.context()
+        cap = max(0, min(stop - start, _INITIAL_CAPACITY))
+        out = np.empty(max(cap, 1), dtype=np.int64)
+        with ctx.lock:
+            _lib.check(L.rk_scan_host(ctx.handle, _ptr(t), n, _ptr(p), m, hx, start, stop,
+                                      out.ctypes.data, cap, ctypes.byref(mt), ctypes.byref(co),
+                                      ctypes.byref(hh)))
+            k = int(mt.value)
+            if k > cap:
+                out = np.empty(k, dtype=np.int64)
+                _lib.check(L.rk_scan_host_fetch(ctx.handle, out.ctypes.data, 0, k))
+        out = out[:k]
+        if out_bias:
+            out += out_bias
+        return out, k, int(co.value), int(hh.value)
+
+    torch = _torch()
+    ctx = _lib.context(dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    cap = max(0, min(stop - start, _INITIAL_CAPACITY))
+    out = torch.empty(max(cap, 1), dtype=torch.int64, device=text.device)
+    with ctx.lock:
+        _lib.check(L.rk_scan(ctx.handle, text.data_ptr(), n, _ptr(p), m, hx, start, stop,
+                             out.data_ptr(), cap, ctypes.byref(mt), ctypes.byref(co),
+                             ctypes.byref(hh), stream))
+        k = int(mt.value)
+        if k > cap:  # the reference's overflow protocol: one more pass with exact room
+            out = torch.empty(k, dtype=torch.int64, device=text.device)
+            _lib.check(L.rk_scan(ctx.handle, text.data_ptr(), n, _ptr(p), m, hx, start, stop,
+                                 out.data_ptr(), k, ctypes.byref(mt), ctypes.byref(co),
+                                 ctypes.byref(hh), stream))
+    out = out[:k]
+    if out_bias:
+        out += out_bias
+    return out, k, int(co.value), int(hh.value)
+
+
+def scan(text, pattern, hx: int, start: int, stop: int):
+    """Scan window offsets [start, stop); returns (offsets, collision count) (_scan.py:53-68)."""
+    if stop <= start:
+        if _device_of(text) is not None:
+            torch = _torch()
+            return torch.empty(0, dtype=torch.int64, device=text.device), 0
+        return np.empty(0, dtype=np.int64), 0
+    offsets, _, collisions, _ = scan_counts(text, pattern, hx, start, stop)
+    return offsets, collisions
+
+
+def window_hashes(text, m: int, start: int, stop: int):
+    """uint64 hashes of every window [x, x+m), x in [start, stop) (_scan.py:71-91)."""
+    if m < 1:
+        raise ValueError("window length must be >= 1")
+    n = _size(text)
+    if start == stop:
+        if _device_of(text) is not None:
+            torch = _torch()
+            return torch.empty(0, dtype=torch.uint64, device=text.device)
+        return np.empty(0, dtype=np.uint64)
+    if start < 0 or stop < start or stop - 1 + m > n:
+        raise ValueError(
+            f"window range [{start}, {stop}) of length {m} out of bounds "
+            f"for text of length {n}"
+        )
+    torch = _torch()
+    dev = _device_of(text)
+    on_host = dev is None
+    if on_host:
+        dev = _lib.default_device()
+        t = torch.from_numpy(np.ascontiguousarray(text)).to(f"cuda:{dev}")
+    else:
+        t = text
+    ctx = _lib.context(dev)
+    out = torch.empty(stop - start, dtype=torch.uint64, device=t.device)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    with ctx.lock:
+        _lib.check(_lib.lib().rk_window_hashes(ctx.handle, t.data_ptr(), n, m, start, stop,
+                                               out.data_ptr(), stream))
+    if on_host:
+        return out.cpu().numpy()
+    return out

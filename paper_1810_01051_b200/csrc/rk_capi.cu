@@ -1,0 +1,610 @@
+// rk_capi.cu -- the C ABI (include/rkb200.h): contexts, argument checking, launch
+// planning for the ordered single-pattern scan, the host-text staging pipeline, the
+// multi-pattern table build, and error reporting.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+#include "../../include/rkb200.h"
+#include "rk_internal.h"
+
+using namespace rkb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define RK_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(RK_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                  \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+constexpr uint64_t kStageChunk = 64ull << 20;  // host staging granularity (multiple of kTile)
+static_assert(kStageChunk % kTile == 0, "stage chunk must be tile aligned");
+
+}  // namespace
+
+struct rk_ctx {
+  int device = 0;
+  int num_sms = 0;
+  unsigned long long* d_ticket = nullptr;    // monotonic ticket counter
+  unsigned long long* d_counters = nullptr;  // [0] matches, [1] hash_hits, [2] collisions
+  unsigned long long* h_counters = nullptr;  // pinned mirror
+  uint64_t* d_status = nullptr;
+  uint64_t status_cap = 0;
+  uint8_t* d_pattern = nullptr;
+  uint64_t pattern_cap = 0;
+  std::vector<uint8_t> pattern_host;  // bytes currently in d_pattern
+  uint64_t ticket_next = 0;
+  uint32_t epoch = 0;
+  uint64_t launches = 0;
+  // host staging
+  uint8_t* d_stage = nullptr;
+  uint64_t stage_cap = 0;
+  uint8_t* h_ring[2] = {nullptr, nullptr};
+  int64_t* d_out_stage = nullptr;
+  uint64_t out_stage_cap = 0;
+  uint64_t host_last = 0;  // offsets held in d_out_stage by the last rk_scan_host
+  cudaStream_t s_copy = nullptr, s_comp = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr};  // ring slot free again
+  cudaEvent_t ev_ready = nullptr;                 // bytes of the current chunk landed
+  // multi-pattern tables
+  uint8_t* d_mpats = nullptr;
+  uint64_t mpats_cap = 0;
+  uint64_t* d_mphash = nullptr;
+  uint32_t* d_morder = nullptr;
+  uint32_t* d_mfilter = nullptr;
+  uint2* d_mtable = nullptr;
+  uint64_t mslots_cap = 0;
+  std::mutex mu;
+};
+
+namespace {
+
+template <class T>
+int grow(T** p, uint64_t* cap, uint64_t need, bool zero, cudaStream_t s) {
+  if (*cap >= need && *p) return RK_OK;
+  if (*p) {
+    RK_CUDA(cudaStreamSynchronize(s));
+    RK_CUDA(cudaFree(*p));
+    *p = nullptr;
+  }
+  uint64_t c = std::max<uint64_t>(need, 64);
+  RK_CUDA(cudaMalloc((void**)p, c * sizeof(T)));
+  if (zero) RK_CUDA(cudaMemsetAsync(*p, 0, c * sizeof(T), s));
+  *cap = c;
+  return RK_OK;
+}
+
+PatWords pack_pattern(const uint8_t* h, uint32_t m) {
+  PatWords pw{};
+  for (uint32_t i = 0; i < m && i < 32; ++i) pw.w[i >> 2] |= (uint32_t)h[i] << (8 * (i & 3));
+  return pw;
+}
+
+// Geometry of one scan of windows [start, stop) over text at d_text.
+struct Geometry {
+  const uint8_t* abase;
+  uint64_t amis, ja_lo, ja_hi, tile_first, num_tiles;
+};
+
+Geometry geometry(const uint8_t* d_text, uint32_t m, uint64_t start, uint64_t stop) {
+  Geometry g;
+  const uintptr_t p = (uintptr_t)d_text;
+  g.abase = (const uint8_t*)(p & ~(uintptr_t)31);
+  g.amis = p - (uintptr_t)g.abase;
+  g.ja_lo = start + m - 1 + g.amis;
+  g.ja_hi = stop + m - 1 + g.amis;
+  g.tile_first = g.ja_lo / kTile;
+  g.num_tiles = (g.ja_hi - 1) / kTile - g.tile_first + 1;
+  return g;
+}
+
+// Starts a logical scan: new epoch (status entries of other epochs read as "not yet
+// published"), status capacity for `tiles` sequence numbers, zeroed counters.
+int begin_scan(rk_ctx* c, uint64_t tiles, cudaStream_t s) {
+  if (int r = grow(&c->d_status, &c->status_cap, tiles, true, s)) return r;
+  c->epoch = (c->epoch + 1) & 0xffff;
+  if (c->epoch == 0) {
+    RK_CUDA(cudaMemsetAsync(c->d_status, 0, c->status_cap * sizeof(uint64_t), s));
+    c->epoch = 1;
+  }
+  RK_CUDA(cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), s));
+  return RK_OK;
+}
+
+int launch_one(rk_ctx* c, const uint8_t* d_text, uint64_t n, uint32_t m, uint64_t hx,
+               uint64_t start, uint64_t stop, int64_t* d_out, uint64_t cap, int64_t bias,
+               uint64_t seq_base, bool last, const PatWords& pw, cudaStream_t s) {
+  const Geometry g = geometry(d_text, m, start, stop);
+  ScanArgs a{};
+  a.abase = g.abase;
+  a.amis = g.amis;
+  a.n = n;
+  a.pattern = c->d_pattern;
+  a.hx = hx;
+  a.ja_lo = g.ja_lo;
+  a.ja_hi = g.ja_hi;
+  a.tile0 = g.tile_first;
+  a.num_tiles = g.num_tiles;
+  a.seq_base = seq_base;
+  a.out_bias = bias;
+  a.out = d_out;
+  a.cap = d_out ? cap : 0;
+  a.ticket = c->d_ticket;
+  a.counters = c->d_counters;
+  a.status = c->d_status;
+  a.m = m;
+  a.epoch = c->epoch;
+  a.last_launch = last ? 1u : 0u;
+  a.pw = pw;
+  const uint64_t max_grid = (uint64_t)c->num_sms * (uint64_t)scan_blocks_per_sm(m);
+  const uint64_t want = (g.num_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int grid = (int)std::max<uint64_t>(1, std::min(max_grid, want));
+  a.ticket_base = c->ticket_next;
+  c->ticket_next += g.num_tiles + (uint64_t)grid * kWarpsPerBlock;
+  RK_CUDA(launch_scan(a, grid, s));
+  ++c->launches;
+  return RK_OK;
+}
+
+int check_scan_args(const uint8_t* text, uint64_t n, const uint8_t* h_pattern, uint32_t m,
+                    uint64_t start, uint64_t stop, const void* out, uint64_t cap) {
+  if (!h_pattern || m < 1) return fail(RK_EINVAL, "pattern must be non-empty");
+  if (stop > start) {
+    if (!text) return fail(RK_EINVAL, "text pointer is NULL");
+    if (stop + (uint64_t)m - 1 > n)
+      return fail(RK_EINVAL, "window range [%llu, %llu) of length %u out of bounds for text of "
+                  "length %llu", (unsigned long long)start, (unsigned long long)stop, m,
+                  (unsigned long long)n);
+    if (cap && !out) return fail(RK_EINVAL, "output pointer is NULL with cap > 0");
+  }
+  return RK_OK;
+}
+
+// m <= 24: every window hash is < 2^32, so a 64-bit hx >= 2^32 can never be hit.
+bool hash_unreachable(uint32_t m, uint64_t hx) { return m <= 24 && (hx >> 32) != 0; }
+
+// Device copy of the pattern; re-uploaded only when the bytes change.
+int upload_pattern(rk_ctx* c, const uint8_t* h_pattern, uint32_t m, cudaStream_t s) {
+  if (c->d_pattern && c->pattern_host.size() == m &&
+      memcmp(c->pattern_host.data(), h_pattern, m) == 0)
+    return RK_OK;
+  if (int r = grow(&c->d_pattern, &c->pattern_cap, m, false, s)) return r;
+  c->pattern_host.assign(h_pattern, h_pattern + m);
+  RK_CUDA(cudaMemcpyAsync(c->d_pattern, c->pattern_host.data(), m, cudaMemcpyHostToDevice, s));
+  RK_CUDA(cudaStreamSynchronize(s));  // pattern_host may change on the next call
+  return RK_OK;
+}
+
+int enqueue_scan(rk_ctx* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_pattern,
+                 uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t* d_out,
+                 uint64_t cap, int64_t bias, cudaStream_t s) {
+  if (stop <= start || hash_unreachable(m, hx)) {
+    RK_CUDA(cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), s));
+    return RK_OK;
+  }
+  if (int r = upload_pattern(c, h_pattern, m, s)) return r;
+  const Geometry g = geometry(d_text, m, start, stop);
+  if (int r = begin_scan(c, g.num_tiles, s)) return r;
+  return launch_one(c, d_text, n, m, hx, start, stop, d_out, cap, bias, 0, true,
+                    pack_pattern(h_pattern, m), s);
+}
+
+int read_counters(rk_ctx* c, uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits,
+                  cudaStream_t s) {
+  RK_CUDA(cudaMemcpyAsync(c->h_counters, c->d_counters, 3 * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, s));
+  RK_CUDA(cudaStreamSynchronize(s));
+  if (matches) *matches = c->h_counters[0];
+  if (hash_hits) *hash_hits = c->h_counters[1];
+  if (collisions) *collisions = c->h_counters[2];
+  return RK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rk_version(void) { return "rkb200 0.1.0 sm_100a"; }
+
+const char* rk_last_error(void) { return g_err.c_str(); }
+
+int rk_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int rk_ctx_create(int device, rk_ctx_t** out) {
+  if (!out) return fail(RK_EINVAL, "out is NULL");
+  *out = nullptr;
+  int ndev = rk_device_count();
+  if (device < 0 || device >= ndev)
+    return fail(RK_ECUDA, "CUDA device %d not available (%d visible)", device, ndev);
+  DeviceGuard g(device);
+  if (!g.ok) return fail(RK_ECUDA, "cudaSetDevice(%d) failed", device);
+  cudaDeviceProp prop;
+  RK_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(RK_ECUDA, "device %d is sm_%d%d; librkb200 is built for sm_100a", device,
+                prop.major, prop.minor);
+  rk_ctx* c = new rk_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  RK_CUDA(cudaMalloc(&c->d_ticket, sizeof(unsigned long long)));
+  RK_CUDA(cudaMemset(c->d_ticket, 0, sizeof(unsigned long long)));
+  RK_CUDA(cudaMalloc(&c->d_counters, 4 * sizeof(unsigned long long)));
+  RK_CUDA(cudaMallocHost(&c->h_counters, 4 * sizeof(unsigned long long)));
+  RK_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
+  RK_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+  for (auto& e : c->ev_copied) RK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  RK_CUDA(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
+  *out = c;
+  return RK_OK;
+}
+
+int rk_ctx_destroy(rk_ctx_t* c) {
+  if (!c) return RK_OK;
+  DeviceGuard g(c->device);
+  cudaDeviceSynchronize();
+  cudaFree(c->d_ticket);
+  cudaFree(c->d_counters);
+  cudaFreeHost(c->h_counters);
+  cudaFree(c->d_status);
+  cudaFree(c->d_pattern);
+  cudaFree(c->d_stage);
+  cudaFree(c->d_out_stage);
+  for (auto* h : c->h_ring) cudaFreeHost(h);
+  for (auto e : c->ev_copied) cudaEventDestroy(e);
+  cudaEventDestroy(c->ev_ready);
+  cudaStreamDestroy(c->s_copy);
+  cudaStreamDestroy(c->s_comp);
+  cudaFree(c->d_mpats);
+  cudaFree(c->d_mphash);
+  cudaFree(c->d_morder);
+  cudaFree(c->d_mfilter);
+  cudaFree(c->d_mtable);
+  delete c;
+  return RK_OK;
+}
+
+uint64_t rk_launch_count(rk_ctx_t* c) { return c ? c->launches : 0; }
+
+int rk_scan_async(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_pattern,
+                  uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t* d_out,
+                  uint64_t cap, int64_t out_bias, uint64_t* d_counts, void* stream) {
+  if (!c) return fail(RK_EINVAL, "context is NULL");
+  if (int r = check_scan_args(d_text, n, h_pattern, m, start, stop, d_out, cap)) return r;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int r = enqueue_scan(c, d_text, n, h_pattern, m, hx, start, stop, d_out, cap, out_bias, s))
+    return r;
+  if (d_counts)
+    RK_CUDA(cudaMemcpyAsync(d_counts, c->d_counters, 3 * sizeof(uint64_t),
+                            cudaMemcpyDeviceToDevice, s));
+  return RK_OK;
+}
+
+int rk_scan_result(rk_ctx_t* c, uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits,
+                   void* stream) {
+  if (!c) return fail(RK_EINVAL, "context is NULL");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  return read_counters(c, matches, collisions, hash_hits, (cudaStream_t)stream);
+}
+
+int rk_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_pattern, uint32_t m,
+            uint64_t hx, uint64_t start, uint64_t stop, int64_t* d_out, uint64_t cap,
+            uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits, void* stream) {
+  if (!c) return fail(RK_EINVAL, "context is NULL");
+  if (int r = check_scan_args(d_text, n, h_pattern, m, start, stop, d_out, cap)) return r;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int r = enqueue_scan(c, d_text, n, h_pattern, m, hx, start, stop, d_out, cap, 0, s)) return r;
+  return read_counters(c, matches, collisions, hash_hits, s);
+}
+
+int rk_scan_host(rk_ctx_t* c, const uint8_t* h_text, uint64_t n, const uint8_t* h_pattern,
+                 uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t* h_out,
+                 uint64_t cap, uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits) {
+  if (!c) return fail(RK_EINVAL, "context is NULL");
+  if (int r = check_scan_args(h_text, n, h_pattern, m, start, stop, h_out, cap)) return r;
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  cudaStream_t sc = c->s_comp, sk = c->s_copy;
+  c->host_last = 0;
+  if (stop <= start || hash_unreachable(m, hx)) {
+    RK_CUDA(cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), sc));
+    return read_counters(c, matches, collisions, hash_hits, sc);
+  }
+  // bytes the windows need: [start, stop + m - 1)
+  const uint64_t b_lo = start, b_hi = stop + m - 1;
+  if (int r = grow(&c->d_stage, &c->stage_cap, n, false, sc)) return r;
+  if (int r = grow(&c->d_out_stage, &c->out_stage_cap, std::max<uint64_t>(cap, 1ull << 16), false,
+                   sc))
+    return r;
+  if (int r = upload_pattern(c, h_pattern, m, sc)) return r;
+
+  cudaPointerAttributes attr;
+  const bool pinned = cudaPointerGetAttributes(&attr, h_text) == cudaSuccess &&
+                      attr.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (!pinned && !c->h_ring[0]) {
+    for (auto& h : c->h_ring) RK_CUDA(cudaMallocHost(&h, kStageChunk));
+  }
+
+  // The staging buffer is cudaMalloc'ed (256-byte aligned), so a-space == text index.
+  const Geometry gall = geometry(c->d_stage, m, start, stop);
+  if (int r = begin_scan(c, gall.num_tiles, sc)) return r;
+  const PatWords pw = pack_pattern(h_pattern, m);
+  const uint64_t icap = c->out_stage_cap;
+
+  // chunk k covers end positions [k*C, (k+1)*C) and needs bytes < (k+1)*C; its copy on
+  // s_copy overlaps the scan of chunk k-1 on s_comp.
+  const uint64_t ja_lo = gall.ja_lo, ja_hi = gall.ja_hi;
+  const uint64_t k0 = ja_lo / kStageChunk, k1 = (ja_hi - 1) / kStageChunk;
+  uint64_t copied = b_lo;  // bytes [b_lo, copied) are enqueued
+  int slot = 0;
+  for (uint64_t k = k0; k <= k1; ++k) {
+    const uint64_t e_lo = std::max(ja_lo, k * kStageChunk);
+    const uint64_t e_hi = std::min(ja_hi, (k + 1) * kStageChunk);
+    const uint64_t need = std::min(b_hi, (k + 1) * kStageChunk);
+    if (need > copied) {
+      const uint64_t len = need - copied;
+      if (pinned) {
+        RK_CUDA(cudaMemcpyAsync(c->d_stage + copied, h_text + copied, len,
+                                cudaMemcpyHostToDevice, sk));
+      } else {
+        // pageable: CPU copy into a pinned ring slot, then DMA; a slot is reused only
+        // after the DMA issued from it two steps ago has finished
+        for (uint64_t off = 0; off < len; off += kStageChunk) {
+          const uint64_t l = std::min<uint64_t>(kStageChunk, len - off);
+          RK_CUDA(cudaEventSynchronize(c->ev_copied[slot]));
+          memcpy(c->h_ring[slot], h_text + copied + off, l);
+          RK_CUDA(cudaMemcpyAsync(c->d_stage + copied + off, c->h_ring[slot], l,
+                                  cudaMemcpyHostToDevice, sk));
+          RK_CUDA(cudaEventRecord(c->ev_copied[slot], sk));
+          slot ^= 1;
+        }
+      }
+      copied = need;
+      RK_CUDA(cudaEventRecord(c->ev_ready, sk));
+      RK_CUDA(cudaStreamWaitEvent(sc, c->ev_ready, 0));
+    }
+    const uint64_t ws = e_lo - (m - 1), we = e_hi - (m - 1);  // windows ending in the chunk
+    const Geometry gk = geometry(c->d_stage, m, ws, we);
+    if (int r = launch_one(c, c->d_stage, n, m, hx, ws, we, c->d_out_stage, icap, 0,
+                           gk.tile_first - gall.tile_first, k == k1, pw, sc))
+      return r;
+  }
+  uint64_t mt = 0, co = 0, hh = 0;
+  if (int r = read_counters(c, &mt, &co, &hh, sc)) return r;
+  if (mt > icap) {
+    // more offsets than the staging output held: rescan the staged text on the device
+    if (int r = grow(&c->d_out_stage, &c->out_stage_cap, mt, false, sc)) return r;
+    if (int r = begin_scan(c, gall.num_tiles, sc)) return r;
+    if (int r = launch_one(c, c->d_stage, n, m, hx, start, stop, c->d_out_stage, mt, 0, 0, true,
+                           pw, sc))
+      return r;
+    if (int r = read_counters(c, &mt, &co, &hh, sc)) return r;
+  }
+  c->host_last = mt;
+  const uint64_t nout = std::min(mt, cap);
+  if (nout) {
+    RK_CUDA(cudaMemcpyAsync(h_out, c->d_out_stage, nout * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            sc));
+    RK_CUDA(cudaStreamSynchronize(sc));
+  }
+  if (matches) *matches = mt;
+  if (collisions) *collisions = co;
+  if (hash_hits) *hash_hits = hh;
+  return RK_OK;
+}
+
+int rk_scan_host_fetch(rk_ctx_t* c, int64_t* h_out, uint64_t first, uint64_t count) {
+  if (!c) return fail(RK_EINVAL, "context is NULL");
+  if (first > c->host_last || count > c->host_last - first)
+    return fail(RK_EINVAL, "fetch [%llu, %llu) beyond the %llu offsets of the last host scan",
+                (unsigned long long)first, (unsigned long long)(first + count),
+                (unsigned long long)c->host_last);
+  if (!count) return RK_OK;
+  if (!h_out) return fail(RK_EINVAL, "NULL output");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  RK_CUDA(cudaMemcpyAsync(h_out, c->d_out_stage + first, count * sizeof(int64_t),
+                          cudaMemcpyDeviceToHost, c->s_comp));
+  RK_CUDA(cudaStreamSynchronize(c->s_comp));
+  return RK_OK;
+}
+
+int rk_window_hashes(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, uint32_t m, uint64_t start,
+                     uint64_t stop, uint64_t* d_out, void* stream) {
+  if (!c) return fail(RK_EINVAL, "context is NULL");
+  if (m < 1) return fail(RK_EINVAL, "window length must be >= 1");
+  if (stop == start) return RK_OK;
+  if (stop < start || stop - 1 + m > n)
+    return fail(RK_EINVAL, "window range [%llu, %llu) of length %u out of bounds for text of "
+                "length %llu", (unsigned long long)start, (unsigned long long)stop, m,
+                (unsigned long long)n);
+  if (!d_text || !d_out) return fail(RK_EINVAL, "NULL pointer");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  RK_CUDA(launch_window_hashes(d_text, n, m, start, stop, d_out, (cudaStream_t)stream));
+  ++c->launches;
+  return RK_OK;
+}
+
+int rk_generate(rk_ctx_t* c, uint8_t* d_out, uint64_t count, uint64_t seed, uint64_t skip,
+                const uint8_t* h_alphabet, uint32_t k, void* stream) {
+  if (!c) return fail(RK_EINVAL, "context is NULL");
+  if (!h_alphabet || k < 1 || k > 256) return fail(RK_EINVAL, "alphabet must have 1..256 symbols");
+  if (count && !d_out) return fail(RK_EINVAL, "NULL output");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  RK_CUDA(launch_generate(d_out, count, seed, skip, h_alphabet, k, (cudaStream_t)stream));
+  ++c->launches;
+  return RK_OK;
+}
+
+int rk_multi_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_patterns,
+                  uint32_t P, uint32_t m, const uint64_t* h_hashes, int64_t* d_off,
+                  uint32_t* d_idx, uint64_t cap, uint64_t* pairs, void* stream) {
+  if (!c) return fail(RK_EINVAL, "context is NULL");
+  if (P < 1 || P > RK_MULTI_MAX_PATTERNS)
+    return fail(RK_EINVAL, "pattern count %u outside [1, %d]", P, RK_MULTI_MAX_PATTERNS);
+  if (m < 1 || !h_patterns || !h_hashes) return fail(RK_EINVAL, "patterns must be non-empty");
+  if (cap && (!d_off || !d_idx)) return fail(RK_EINVAL, "NULL output with cap > 0");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  *pairs = 0;
+  if (n < m) return RK_OK;
+  if (!d_text) return fail(RK_EINVAL, "text pointer is NULL");
+
+  // ---- host build: filter bits, open-addressing table of distinct low32 keys
+  std::vector<std::pair<uint32_t, uint32_t>> keyed(P);
+  for (uint32_t i = 0; i < P; ++i) keyed[i] = {(uint32_t)h_hashes[i], i};
+  std::stable_sort(keyed.begin(), keyed.end(),
+                   [](const auto& x, const auto& y) { return x.first < y.first; });
+  std::vector<uint32_t> order(P);
+  std::vector<std::pair<uint32_t, uint32_t>> runs;  // (key, first<<13 | cnt)
+  for (uint32_t i = 0; i < P;) {
+    uint32_t j = i;
+    while (j < P && keyed[j].first == keyed[i].first) {
+      order[j] = keyed[j].second;
+      ++j;
+    }
+    runs.push_back({keyed[i].first, (i << 13) | (j - i)});
+    i = j;
+  }
+  uint32_t tsize = 64;
+  while (tsize < 2 * runs.size()) tsize <<= 1;
+  std::vector<uint2> table(tsize, make_uint2(0u, kMultiEmpty));
+  std::vector<uint32_t> filter(kMultiFilterWords, 0u);
+  // reachable keys only: m <= 24 windows have hash < 2^32
+  for (const auto& r : runs) {
+    uint32_t slot = (r.first * 0x9E3779B1u) & (tsize - 1);
+    while (table[slot].y != kMultiEmpty) slot = (slot + 1) & (tsize - 1);
+    table[slot] = make_uint2(r.first, r.second);
+    const uint32_t b = (r.first * 0x9E3779B1u) >> 16;
+    filter[b >> 5] |= 1u << (b & 31);
+  }
+  if (int r = grow(&c->d_mpats, &c->mpats_cap, (uint64_t)P * m, false, s)) return r;
+  uint64_t pcap = c->mslots_cap;
+  if (pcap < std::max<uint64_t>(P, tsize)) {
+    cudaFree(c->d_mphash);
+    cudaFree(c->d_morder);
+    cudaFree(c->d_mtable);
+    pcap = std::max<uint64_t>(P, tsize);
+    RK_CUDA(cudaMalloc(&c->d_mphash, pcap * sizeof(uint64_t)));
+    RK_CUDA(cudaMalloc(&c->d_morder, pcap * sizeof(uint32_t)));
+    RK_CUDA(cudaMalloc(&c->d_mtable, pcap * sizeof(uint2)));
+    c->mslots_cap = pcap;
+  }
+  if (!c->d_mfilter) RK_CUDA(cudaMalloc(&c->d_mfilter, kMultiFilterWords * sizeof(uint32_t)));
+  RK_CUDA(cudaMemcpyAsync(c->d_mpats, h_patterns, (uint64_t)P * m, cudaMemcpyHostToDevice, s));
+  RK_CUDA(cudaMemcpyAsync(c->d_mphash, h_hashes, P * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  RK_CUDA(cudaMemcpyAsync(c->d_morder, order.data(), P * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  RK_CUDA(cudaMemcpyAsync(c->d_mtable, table.data(), tsize * sizeof(uint2), cudaMemcpyHostToDevice, s));
+  RK_CUDA(cudaMemcpyAsync(c->d_mfilter, filter.data(), kMultiFilterWords * sizeof(uint32_t),
+                          cudaMemcpyHostToDevice, s));
+  RK_CUDA(cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), s));
+
+  const uint64_t nw = n - m + 1;
+  const Geometry gg = geometry(d_text, m, 0, nw);
+  MultiHostPlan p{};
+  p.abase = gg.abase;
+  p.amis = gg.amis;
+  p.n = n;
+  p.ja_lo = gg.ja_lo;
+  p.ja_hi = gg.ja_hi;
+  p.tile0 = gg.tile_first;
+  p.num_tiles = gg.num_tiles;
+  p.cap = cap;
+  p.pats = c->d_mpats;
+  p.phash = c->d_mphash;
+  p.filter = c->d_mfilter;
+  p.table = c->d_mtable;
+  p.order = c->d_morder;
+  p.out_off = d_off;
+  p.out_idx = d_idx;
+  p.ticket = c->d_ticket;
+  p.counters = c->d_counters;
+  p.m = m;
+  p.P = P;
+  p.tsize = tsize;
+  const uint64_t want = (gg.num_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->num_sms * 2, want));
+  p.ticket_base = c->ticket_next;
+  c->ticket_next += gg.num_tiles + (uint64_t)grid * kWarpsPerBlock;
+  RK_CUDA(launch_multi_plan(p, grid, s));
+  ++c->launches;
+  RK_CUDA(cudaMemcpyAsync(c->h_counters, c->d_counters, sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, s));
+  RK_CUDA(cudaStreamSynchronize(s));
+  const uint64_t total = c->h_counters[0];
+  *pairs = total;
+  // order by (pattern index, offset): the reference's per-pattern ascending lists
+  const uint64_t k = std::min(total, cap);
+  if (k > 1) {
+    std::vector<int64_t> off(k);
+    std::vector<uint32_t> idx(k);
+    RK_CUDA(cudaMemcpyAsync(off.data(), d_off, k * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    RK_CUDA(cudaMemcpyAsync(idx.data(), d_idx, k * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    RK_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint64_t> perm(k);
+    for (uint64_t i = 0; i < k; ++i) perm[i] = i;
+    std::sort(perm.begin(), perm.end(), [&](uint64_t x, uint64_t y) {
+      return idx[x] != idx[y] ? idx[x] < idx[y] : off[x] < off[y];
+    });
+    std::vector<int64_t> off2(k);
+    std::vector<uint32_t> idx2(k);
+    for (uint64_t i = 0; i < k; ++i) {
+      off2[i] = off[perm[i]];
+      idx2[i] = idx[perm[i]];
+    }
+    RK_CUDA(cudaMemcpyAsync(d_off, off2.data(), k * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    RK_CUDA(cudaMemcpyAsync(d_idx, idx2.data(), k * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    RK_CUDA(cudaStreamSynchronize(s));
+  }
+  return RK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,179 @@
+"""Matcher core -- drop-in for rkmatch.matcher (/root/reference/pkg/src/rkmatch/matcher.py).
+
+``MatchResult``, ``ScanStats``, ``PatternSet``, ``search_naive`` and
+``search_sequential`` keep the reference's fields, signatures, validation order and
+exceptions; ``search_multi`` returns the same ``[(index, MatchResult)]`` list.  The hash
+sweeps run on the B200 (``_scan`` / ``rk_multi_scan``); ``search_naive`` stays the
+brute-force definition the reference ships as its oracle.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, _scan
+from .rkhash import hash_full
+
+
+@dataclass
+class MatchResult:
+    """All match offsets for one (text, pattern) search (matcher.py:23-42).
+
+    Offsets are ascending, unique, in [0, text_length - pattern_length], and the window
+    at every reported offset byte-equals the pattern."""
+
+    text_length: int
+    pattern_length: int
+    offsets: list[int]
+
+    def to_bitmap(self) -> np.ndarray:
+        """Dense per-window boolean map, True where a match starts."""
+        n_windows = max(self.text_length - self.pattern_length + 1, 0)
+        bitmap = np.zeros(n_windows, dtype=bool)
+        if self.offsets:
+            bitmap[np.asarray(self.offsets)] = True
+        return bitmap
+
+
+@dataclass
+class ScanStats:
+    """Counters of an instrumented scan (matcher.py:45-55): hash_hits = matches + collisions."""
+
+    windows: int = 0
+    hash_hits: int = 0
+    collisions: int = 0
+
+
+class PatternSet:
+    """Deduplicated non-empty patterns indexed for one-pass multi search (matcher.py:58-87)."""
+
+    def __init__(self, patterns):
+        self.patterns: list[bytes] = []
+        self.by_length: dict[int, list[int]] = {}
+        self.hash_index: dict[int, dict[int, list[int]]] = {}
+        seen: set[bytes] = set()
+        for raw in patterns:
+            p = bytes(raw)
+            if not p:
+                raise ValueError("empty pattern")
+            if p in seen:
+                continue
+            seen.add(p)
+            idx = len(self.patterns)
+            self.patterns.append(p)
+            m = len(p)
+            self.by_length.setdefault(m, []).append(idx)
+            self.hash_index.setdefault(m, {}).setdefault(hash_full(p), []).append(idx)
+        if not self.patterns:
+            raise ValueError("pattern set is empty")
+
+    def __len__(self) -> int:
+        return len(self.patterns)
+
+
+def _to_list(offsets) -> list[int]:
+    return offsets.tolist()
+
+
+def search_naive(text, pattern) -> MatchResult:
+    """Ground-truth definition: direct byte comparison at every offset (matcher.py:90-98)."""
+    text = text if isinstance(text, bytes) else bytes(text)
+    pattern = pattern if isinstance(pattern, bytes) else bytes(pattern)
+    if not pattern:
+        raise ValueError("empty pattern")
+    n, m = len(text), len(pattern)
+    offsets = [x for x in range(n - m + 1) if text[x : x + m] == pattern]
+    return MatchResult(n, m, offsets)
+
+
+def search_sequential(text, pattern, stats: ScanStats | None = None) -> MatchResult:
+    """Hash every window, byte-verify on hash equality (matcher.py:101-122), on the B200."""
+    t = _scan.as_u8(text)
+    p = _scan.as_u8(pattern)
+    m = _scan._size(p)
+    if m == 0:
+        raise ValueError("empty pattern")
+    n = _scan._size(t)
+    n_windows = n - m + 1
+    if n_windows <= 0:
+        return MatchResult(n, m, [])
+    hx = hash_full(p)
+    offsets, matches, collisions, hash_hits = _scan.scan_counts(t, p, hx, 0, n_windows)
+    if stats is not None:
+        stats.windows += n_windows
+        stats.hash_hits += hash_hits
+        stats.collisions += collisions
+    return MatchResult(n, m, _to_list(offsets))
+
+
+def _device_text(t):
+    """(device tensor, device index) for search_multi; host text is copied once."""
+    import torch
+
+    if _scan._device_of(t) is not None:
+        return t, _scan._device_of(t)
+    dev = _lib.default_device()
+    host = torch.from_numpy(np.ascontiguousarray(t))
+    if host.numel():
+        host = host.pin_memory()
+    return host.to(f"cuda:{dev}", non_blocking=True), dev
+
+
+def multi_group(t_dev, dev: int, pats: list[bytes]):
+    """One equal-length group through rk_multi_scan -> [offsets ndarray per pattern]."""
+    import torch
+
+    L = _lib.lib()
+    m = len(pats[0])
+    P = len(pats)
+    n = int(t_dev.numel())
+    flat = np.frombuffer(b"".join(pats), dtype=np.uint8)
+    hashes = np.array([hash_full(p) for p in pats], dtype=np.uint64)
+    ctx = _lib.context(dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    cap = 1 << 16
+    pairs = _lib.u64ref()
+    for _attempt in range(2):
+        off = torch.empty(cap, dtype=torch.int64, device=t_dev.device)
+        idx = torch.empty(cap, dtype=torch.int32, device=t_dev.device)
+        with ctx.lock:
+            _lib.check(L.rk_multi_scan(ctx.handle, t_dev.data_ptr(), n, flat.ctypes.data, P, m,
+                                       hashes.ctypes.data, off.data_ptr(), idx.data_ptr(), cap,
+                                       ctypes.byref(pairs), stream))
+        k = int(pairs.value)
+        if k <= cap:
+            break
+        cap = k
+    off = off[:k].cpu().numpy()
+    idx = idx[:k].cpu().numpy()
+    bounds = np.searchsorted(idx, np.arange(P + 1), side="left")
+    return [off[bounds[i] : bounds[i + 1]] for i in range(P)]
+
+
+def search_multi(text, patterns) -> list[tuple[int, MatchResult]]:
+    """Every pattern of a PatternSet, one device sweep per length (matcher.py:125-157).
+
+    Returns one (pattern index, MatchResult) per distinct pattern, in index order; each
+    result equals search_naive for that pattern."""
+    if not isinstance(patterns, PatternSet):
+        patterns = PatternSet(patterns)
+    t = _scan.as_u8(text)
+    n = _scan._size(t)
+    found: dict[int, list[int]] = {i: [] for i in range(len(patterns))}
+    lengths = [m for m in sorted(patterns.by_length) if n - m + 1 > 0]
+    if lengths:
+        t_dev, dev = _device_text(t)
+        for m in lengths:
+            idxs = patterns.by_length[m]
+            for a in range(0, len(idxs), _lib.MULTI_MAX_PATTERNS):
+                batch = idxs[a : a + _lib.MULTI_MAX_PATTERNS]
+                per = multi_group(t_dev, dev, [patterns.patterns[i] for i in batch])
+                for i, offs in zip(batch, per):
+                    found[i] = offs.tolist()
+    return [
+        (i, MatchResult(n, len(patterns.patterns[i]), found[i]))
+        for i in range(len(patterns))
+    ]

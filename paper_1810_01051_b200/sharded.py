@@ -1,0 +1,100 @@
+"""Multi-GPU sharding: one process per GPU (torchrun), contiguous shards with halo.
+
+The reference partitions the window range contiguously over workers and concatenates
+the per-range lists in range order (/root/reference/pkg/src/rkmatch/parallel.py:155-172).
+The same partition becomes the GPU shard map:
+
+* rank r owns windows [a_r, b_r) and holds text bytes [a_r, b_r + m - 1) -- its shard
+  plus an (m-1)-byte halo (the hash needs min(m,32)-1 of them, verification m-1);
+* each rank scans its shard with no inter-GPU traffic;
+* the only exchange is the final gather: per-rank counts, then the positions padded to
+  the largest count, with NCCL all_gather over NVLink; concatenating in rank order is
+  already the globally ascending list.
+
+The functions take a ``torch.distributed`` process group, so the host logic is tested
+with ``gloo`` on CPU (tests/test_sharded.py) and runs with ``nccl`` on B200s.
+"""
+
+from __future__ import annotations
+
+
+def weak_shard(rank: int, per_rank: int, n_total: int, m: int) -> tuple[int, int, int, int]:
+    """Weak scaling (fixed bytes per rank): rank r's windows start at r*per_rank.
+
+    Returns (win_lo, win_hi, byte_lo, byte_hi) in global coordinates."""
+    n_windows = max(n_total - m + 1, 0)
+    a = min(rank * per_rank, n_windows)
+    b = min((rank + 1) * per_rank, n_windows)
+    return a, b, a, min(b + m - 1, n_total) if b > a else a
+
+
+def strong_shard(rank: int, world: int, n_total: int, m: int) -> tuple[int, int, int, int]:
+    """Strong scaling (fixed total): windows split as ceil(W/G) contiguous ranges."""
+    n_windows = max(n_total - m + 1, 0)
+    chunk = -(-n_windows // world) if n_windows else 0
+    a = min(rank * chunk, n_windows)
+    b = min(a + chunk, n_windows)
+    return a, b, a, min(b + m - 1, n_total) if b > a else a
+
+
+def gather_offsets(local, group=None):
+    """All ranks' ascending offset lists concatenated in rank order (all_gather twice)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    dev = local.device
+    k = torch.tensor([local.numel()], dtype=torch.int64, device=dev)
+    counts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(counts, k, group=group)
+    counts = [int(c.item()) for c in counts]
+    kmax = max(counts)
+    if kmax == 0:
+        return torch.empty(0, dtype=torch.int64, device=dev), counts
+    padded = torch.zeros(kmax, dtype=torch.int64, device=dev)
+    padded[: local.numel()] = local
+    parts = [torch.empty(kmax, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(parts, padded, group=group)
+    return torch.cat([p[:c] for p, c in zip(parts, counts)]), counts
+
+
+def sum_counters(values, group=None):
+    """All-reduce (sum) of per-rank integer counters (matches, hash_hits, collisions)."""
+    import torch
+    import torch.distributed as dist
+
+    t = values if isinstance(values, torch.Tensor) else torch.tensor(values, dtype=torch.int64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def search_sharded(shard, pattern, win_lo: int, win_hi: int, byte_lo: int, group=None,
+                   scan_fn=None):
+    """Scan this rank's shard (global windows [win_lo, win_hi), bytes from byte_lo) and
+    gather the global ascending offsets on every rank.
+
+    Returns (offsets tensor, [matches, hash_hits, collisions] summed over ranks).
+    ``scan_fn(shard, pattern, start, stop) -> (offsets, matches, collisions, hash_hits)``
+    defaults to the B200 scan."""
+    import torch
+
+    from . import _scan
+    from .rkhash import hash_full
+
+    if scan_fn is None:
+        hx = hash_full(pattern)
+
+        def scan_fn(t, p, a, b):
+            return _scan.scan_counts(t, p, hx, a, b)
+
+    if win_hi > win_lo:
+        offs, k, coll, hits = scan_fn(shard, pattern, win_lo - byte_lo, win_hi - byte_lo)
+        if not isinstance(offs, torch.Tensor):
+            offs = torch.as_tensor(offs)
+        offs = offs.to(torch.int64) + byte_lo
+    else:
+        dev = shard.device if isinstance(shard, torch.Tensor) else "cpu"
+        offs, k, coll, hits = torch.empty(0, dtype=torch.int64, device=dev), 0, 0, 0
+    allo, _ = gather_offsets(offs, group)
+    tot = sum_counters(torch.tensor([k, hits, coll], dtype=torch.int64, device=offs.device), group)
+    return allo, [int(v) for v in tot.tolist()]

@@ -1,0 +1,272 @@
+"""GPU parity: the sm_100a scan against the golden vectors (produced by the reference)
+and against the CPU oracle on seeded inputs.  Integer work: every comparison is
+bit-exact (offsets, windows, hash_hits, collisions)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1810_01051_b200 as rk
+from paper_1810_01051_b200 import _scan
+from tests import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def check_case(c, text_obj):
+    st = rk.ScanStats()
+    r = rk.search_sequential(text_obj, c["pattern"], stats=st)
+    assert r.offsets == c["offsets"], c["tag"]
+    assert (r.text_length, r.pattern_length) == (c["n"], c["m"])
+    if c["m"] <= c["n"]:
+        assert st.windows == c["windows"], c["tag"]
+        assert st.hash_hits == c["hash_hits"], c["tag"]
+        assert st.collisions == c["collisions"], c["tag"]
+
+
+def test_golden_scan_cases_host_bytes(gpu):
+    for c in G.scan_cases():
+        check_case(c, c["text"])
+
+
+def test_golden_scan_cases_device_tensors(gpu):
+    torch = _torch()
+    for c in G.scan_cases():
+        t = torch.frombuffer(bytearray(c["text"]), dtype=torch.uint8).cuda() if c["n"] else \
+            torch.empty(0, dtype=torch.uint8, device="cuda")
+        check_case(c, t)
+
+
+def test_golden_parallel_and_cfg_independence(gpu):
+    for i, c in enumerate(G.scan_cases()):
+        if i % 5 or c["m"] > c["n"]:
+            continue
+        for block in (1, 32, 1024):
+            cfg = rk.plan_launch(c["n"], c["m"], block)
+            st = rk.ScanStats()
+            r = rk.search_parallel(c["text"], c["pattern"], cfg, workers=4, stats=st)
+            assert r.offsets == c["offsets"] and st.collisions == c["collisions"], c["tag"]
+        padded = rk.LaunchConfig((1024, 2, 2), 512)
+        assert rk.search_parallel(c["text"], c["pattern"], padded, 3).offsets == c["offsets"]
+
+
+def test_unaligned_device_views(gpu):
+    """Text pointers at every offset mod 32 (the kernel's 256-bit loads are aligned down)."""
+    torch = _torch()
+    rng = np.random.default_rng(3)
+    base = rng.integers(0, 4, 70000, dtype=np.uint8)
+    base[rng.integers(0, 69000, 400)] = 7
+    dev = torch.from_numpy(base).cuda()
+    for shift in range(33):
+        for m in (1, 3, 8, 17, 31, 32, 33, 40, 64, 70):
+            n = 69000 - shift
+            view = dev[shift : shift + n]
+            host = base[shift : shift + n]
+            pat = host[1234 : 1234 + m].tobytes()
+            eo, ec = oracle.c_scan(host, np.frombuffer(pat, dtype=np.uint8), workers=4)
+            st = rk.ScanStats()
+            r = rk.search_sequential(view, pat, stats=st)
+            assert r.offsets == eo.tolist(), (shift, m)
+            assert st.collisions == ec, (shift, m)
+
+
+def test_window_ranges_via_scan(gpu):
+    """_scan.scan(text, pattern, hx, start, stop) on arbitrary sub-ranges."""
+    torch = _torch()
+    rng = np.random.default_rng(11)
+    host = rng.integers(0, 3, 200000, dtype=np.uint8)
+    dev = torch.from_numpy(host).cuda()
+    for m in (2, 5, 12, 24, 29, 32, 48, 100):
+        pat = host[777 : 777 + m]
+        hx = oracle.hash_full(pat.tobytes())
+        nw = host.size - m + 1
+        for start, stop in [(0, nw), (1, 2), (5, 5), (16383, 16385), (12345, 170001),
+                            (nw - 1, nw), (0, 1), (100, 33000)]:
+            eo, ec = oracle.c_scan(host, pat, start, stop)
+            do, dc = _scan.scan(dev, pat.tobytes(), hx, start, stop)
+            assert do.cpu().numpy().tolist() == eo.tolist(), (m, start, stop)
+            assert dc == ec
+            ho, hc = _scan.scan(host, pat.tobytes(), hx, start, stop)
+            assert ho.tolist() == eo.tolist() and hc == ec
+
+
+def test_foreign_hx_semantics(gpu):
+    """hx is a parameter (as in _scan_range): windows are hash-checked against it, then
+    byte-verified against the pattern bytes."""
+    rng = np.random.default_rng(5)
+    host = rng.integers(97, 100, 5000, dtype=np.uint8)
+    for m in (2, 8, 30, 40, 70):
+        pat = host[100 : 100 + m]
+        other = host[200 : 200 + m]
+        hx = oracle.hash_full(other.tobytes())
+        lib = oracle.load()
+        import ctypes
+
+        coll = ctypes.c_uint64()
+        out = np.empty(host.size, dtype=np.int64)
+        k = lib.ro_scan_range(host.ctypes.data, pat.ctypes.data, m, hx, 0, host.size - m + 1,
+                              out.ctypes.data, out.size, ctypes.byref(coll))
+        do, dc = _scan.scan(host, pat.tobytes(), hx, 0, host.size - m + 1)
+        assert do.tolist() == out[:k].tolist() and dc == coll.value, m
+    # unreachable hash for short windows
+    do, dc = _scan.scan(b"abcabc", b"abc", 1 << 40, 0, 4)
+    assert do.tolist() == [] and dc == 0
+
+
+def test_random_fuzz_against_oracle(gpu):
+    rng = np.random.default_rng(20240810)
+    for case in range(600):
+        k = (2, 3, 4, 256)[case % 4]
+        n = int(rng.integers(1, 40000))
+        m = int(rng.integers(1, 130))
+        text = rng.integers(0, k, n, dtype=np.uint8)
+        if m <= n and rng.random() < 0.6:
+            x = int(rng.integers(0, n - m + 1))
+            pat = text[x : x + m].copy()
+        else:
+            pat = rng.integers(0, k, m, dtype=np.uint8)
+        st = rk.ScanStats()
+        r = rk.search_sequential(text.tobytes(), pat.tobytes(), stats=st)
+        if m > n:
+            assert r.offsets == []
+            continue
+        eo, ec = oracle.c_scan(text, pat, workers=4)
+        assert r.offsets == eo.tolist(), (case, n, m, k)
+        assert st.collisions == ec, (case, n, m, k)
+        assert st.hash_hits == len(eo) + ec
+
+
+def test_c1_sweep_golden(gpu):
+    co = G.corpus()
+    text = rk.generate(rk.DnaSpec(42, 2**20, G.ASCII))
+    assert hashlib.sha256(text).hexdigest() == co["ascii_seed42_1MiB_sha256"]
+    for e in co["ascii_seed42_1MiB_sweep"]:
+        st = rk.ScanStats()
+        r = rk.search_sequential(text, G.dec(e["pattern"]), stats=st)
+        assert r.offsets == e["offsets"], (e["m"], e["source"])
+        assert st.collisions == e["collisions"] and st.hash_hits == e["hash_hits"]
+        assert st.windows == e["windows"]
+
+
+def test_dna_planted_golden(gpu):
+    co = G.corpus()
+    dna = rk.generate(rk.DnaSpec(42, 4 * 2**20))
+    assert hashlib.sha256(dna).hexdigest() == co["dna_seed42_4MiB_sha256"]
+    assert hashlib.sha256(rk.generate(rk.DnaSpec(42, 2 * 2**20))).hexdigest() == \
+        co["dna_seed42_2MiB_sha256"]
+    for e in co["dna_seed42_4MiB"]:
+        pat = G.dec(e["pattern"])
+        text = rk.plant(dna, pat, e["plant"])
+        st = rk.ScanStats()
+        r = rk.search_sequential(text, pat, stats=st)
+        assert r.offsets == e["offsets"] and st.collisions == e["collisions"]
+
+
+def test_window_hashes_golden(gpu):
+    torch = _torch()
+    for e in G.hash_kat()["window_hashes"]:
+        text = G.dec(e["text"])
+        m = e["m"]
+        h = _scan.window_hashes(np.frombuffer(text, dtype=np.uint8), m, 0, len(text) - m + 1)
+        assert [int(v) for v in h.tolist()] == [int(v) for v in e["h"]]
+        d = _scan.window_hashes(torch.frombuffer(bytearray(text), dtype=torch.uint8).cuda(), m, 1,
+                                len(text) - m + 1)
+        assert [int(v) for v in d.cpu().numpy().tolist()] == [int(v) for v in e["h"][1:]]
+    with pytest.raises(ValueError):
+        _scan.window_hashes(np.zeros(6, np.uint8), 3, 0, 5)
+    with pytest.raises(ValueError):
+        _scan.window_hashes(np.zeros(6, np.uint8), 0, 0, 1)
+
+
+def test_generate_matches_oracle_slices(gpu):
+    for seed, alpha in [(42, b"ACGT"), (43, G.ASCII), (7, b"ab"), (2**64 - 1, bytes(range(256)))]:
+        spec = rk.DnaSpec(seed, 3 * 2**20 + 5, alpha)
+        got = rk.generate(spec)
+        assert got == oracle.generate(seed, spec.length, alpha)
+        t = rk.generate_tensor(spec, skip=1000003, count=4099)
+        assert t.cpu().numpy().tobytes() == got[1000003 : 1000003 + 4099]
+
+
+def test_golden_multi_cases(gpu):
+    for c in G.multi_cases():
+        out = rk.search_multi(c["text"], rk.PatternSet(c["patterns"]))
+        assert [[i, r.offsets] for i, r in out] == c["results"], c["tag"]
+        for i, r in out:
+            assert r.pattern_length == len(c["deduped"][i])
+
+
+def test_multi_singleton_equals_sequential(gpu):
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        text = rng.choice(list(b"ACGT"), int(rng.integers(1, 3000))).astype(np.uint8).tobytes()
+        m = int(rng.integers(1, 40))
+        pat = rng.choice(list(b"ACGT"), m).astype(np.uint8).tobytes()
+        [(idx, res)] = rk.search_multi(text, rk.PatternSet([pat]))
+        assert idx == 0 and res == rk.search_sequential(text, pat)
+
+
+def test_multi_many_lengths_against_oracle(gpu):
+    rng = np.random.default_rng(9)
+    text = rng.integers(0, 4, 300000, dtype=np.uint8)
+    pats = []
+    for m in (1, 3, 7, 16, 24, 25, 31, 32, 33, 64, 65, 90):
+        for _ in range(20):
+            x = int(rng.integers(0, text.size - m))
+            pats.append(text[x : x + m].tobytes())
+        pats.append(rng.integers(0, 4, m, dtype=np.uint8).tobytes())
+    out = rk.search_multi(text.tobytes(), pats)
+    ps, by_len, _ = oracle.pattern_set(pats)
+    expect = {}
+    for m, idxs in by_len.items():
+        for j, offs in oracle.c_search_multi_group(text, [ps[i] for i in idxs]):
+            expect[idxs[j]] = offs.tolist()
+    for i, r in out:
+        assert r.offsets == expect[i], (i, len(ps[i]))
+
+
+def test_dense_all_a(gpu):
+    """Adversarial density (C5 shape): every window matches."""
+    torch = _torch()
+    for n, m in [(4097, 1), (100000, 4), (65536 + 17, 31), (50000, 32), (70000, 100)]:
+        t = torch.full((n,), 97, dtype=torch.uint8, device="cuda")
+        st = rk.ScanStats()
+        offs, k, coll, hits = _scan.scan_counts(t, b"a" * m, rk.hash_full(b"a" * m), 0, n - m + 1)
+        assert k == n - m + 1 and coll == 0 and hits == k
+        assert torch.equal(offs, torch.arange(n - m + 1, device="cuda")), (n, m)
+        r = rk.search_sequential(b"a" * n, b"a" * m, stats=st)
+        assert r.offsets == list(range(n - m + 1))
+        assert st.collisions == 0
+
+
+def test_host_overflow_fetch_path(gpu):
+    # more matches than the initial capacity of the host path: fetched, never rescanned
+    n = (1 << 16) * 3 + 11
+    r = rk.search_sequential(b"ab" * (n // 2), b"ab")
+    assert r.offsets == list(range(0, 2 * (n // 2) - 1, 2))
+
+
+def test_search_parallel_devices_kw(gpu):
+    rng = np.random.default_rng(1)
+    text = rng.integers(0, 4, 100000, dtype=np.uint8).tobytes()
+    pat = text[5000:5012]
+    cfg = rk.plan_launch(len(text), len(pat), 256)
+    r1 = rk.search_parallel(text, pat, cfg, 4, devices=[0])
+    assert r1 == rk.search_naive(text, pat)
+
+
+def test_pinned_host_tensor_input(gpu):
+    torch = _torch()
+    rng = np.random.default_rng(2)
+    host = torch.from_numpy(rng.integers(0, 4, 1 << 20, dtype=np.uint8)).pin_memory()
+    pat = host[4321 : 4321 + 20].numpy().tobytes()
+    r = rk.search_sequential(host, pat)
+    eo, _ = oracle.c_scan(host.numpy(), np.frombuffer(pat, dtype=np.uint8), workers=4)
+    assert r.offsets == eo.tolist()
