@@ -21,8 +21,9 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "rkb200"
 LIB = PKG / "librkb200.so"
-SOURCES = ["rk_scan.cu", "rk_multi.cu", "rk_aux.cu", "rk_capi.cu"]
-HEADERS = ["rk_device.cuh", "rk_internal.h"]
+SOURCES = ["rk_scan.cu", *[f"rk_scan_g{g}.cu" for g in range(4)], "rk_multi.cu",
+           *[f"rk_multi_g{g}.cu" for g in range(4)], "rk_emit.cu", "rk_aux.cu", "rk_capi.cu"]
+HEADERS = ["rk_device.cuh", "rk_internal.h", "rk_scan_impl.cuh", "rk_multi_impl.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--use_fast_math",
@@ -61,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             print(r.stdout, r.stderr, file=sys.stderr)
         return obj
 
-    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs),

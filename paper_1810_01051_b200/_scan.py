@@ -57,13 +57,23 @@ def as_u8(data):
 
 
 def _size(t) -> int:
-    return int(t.numel()) if _is_tensor(t) else int(t.size)
+    if _is_tensor(t):
+        return int(t.numel())
+    if isinstance(t, np.ndarray):
+        return int(t.size)
+    return len(t)
 
 
 def _host_bytes(p) -> np.ndarray:
     if _is_tensor(p):
         return p.detach().to("cpu").contiguous().numpy()
-    return np.ascontiguousarray(p, dtype=np.uint8)
+    if isinstance(p, (bytes, bytearray, memoryview)):
+        return np.frombuffer(p, dtype=np.uint8)
+    if isinstance(p, np.ndarray):
+        if p.dtype != np.uint8:
+            raise TypeError(f"expected uint8 array, got {p.dtype}")
+        return np.ascontiguousarray(p).reshape(-1)
+    return np.frombuffer(bytes(p), dtype=np.uint8)
 
 
 def _device_of(t) -> int | None:
@@ -89,7 +99,7 @@ def scan_counts(text, pattern, hx: int, start: int, stop: int, *, out_bias: int 
     mt, co, hh = _lib.u64ref(), _lib.u64ref(), _lib.u64ref()
     dev = _device_of(text)
     if dev is None:
-        t = text if isinstance(text, np.ndarray) else _host_bytes(text)
+        t = _host_bytes(text)
         ctx = _lib.context()
         cap = max(0, min(stop - start, _INITIAL_CAPACITY))
         out = np.empty(max(cap, 1), dtype=np.int64)

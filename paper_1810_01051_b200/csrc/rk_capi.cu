@@ -58,16 +58,23 @@ static_assert(kStageChunk % kTile == 0, "stage chunk must be tile aligned");
 struct rk_ctx {
   int device = 0;
   int num_sms = 0;
-  unsigned long long* d_ticket = nullptr;    // monotonic ticket counter
   unsigned long long* d_counters = nullptr;  // [0] matches, [1] hash_hits, [2] collisions
   unsigned long long* h_counters = nullptr;  // pinned mirror
-  uint64_t* d_status = nullptr;
-  uint64_t status_cap = 0;
-  uint8_t* d_pattern = nullptr;
-  uint64_t pattern_cap = 0;
-  std::vector<uint8_t> pattern_host;  // bytes currently in d_pattern
-  uint64_t ticket_next = 0;
-  uint32_t epoch = 0;
+  uint32_t* d_tile_info = nullptr;  // per tile: matches | chunk bitmap << 16
+  uint64_t tile_info_cap = 0;
+  uint32_t* d_masks = nullptr;      // per tile: kTileChunks x 32 lane hit masks
+  uint64_t masks_cap = 0;
+  unsigned long long* d_block_sums = nullptr;
+  uint64_t block_sums_cap = 0;
+  uint8_t* d_pattern = nullptr;  // pattern of the current scan (points into a cache slot)
+  struct PatSlot {
+    std::vector<uint8_t> bytes;
+    uint8_t* d = nullptr;
+    uint64_t cap = 0;
+    uint64_t last_use = 0;
+  };
+  std::vector<PatSlot> pat_cache = std::vector<PatSlot>(64);
+  uint64_t pat_clock = 0;
   uint64_t launches = 0;
   // host staging
   uint8_t* d_stage = nullptr;
@@ -113,6 +120,15 @@ PatWords pack_pattern(const uint8_t* h, uint32_t m) {
   return pw;
 }
 
+RollConsts roll_consts(uint32_t m) {
+  RollConsts K;
+  K.k2 = 2;
+  K.k8 = 8;
+  K.k16 = 16;
+  K.negpow = m < 32 ? (uint32_t)(0u - (1u << m)) : 0u;
+  return K;
+}
+
 // Geometry of one scan of windows [start, stop) over text at d_text.
 struct Geometry {
   const uint8_t* abase;
@@ -131,50 +147,73 @@ Geometry geometry(const uint8_t* d_text, uint32_t m, uint64_t start, uint64_t st
   return g;
 }
 
-// Starts a logical scan: new epoch (status entries of other epochs read as "not yet
-// published"), status capacity for `tiles` sequence numbers, zeroed counters.
+// Starts a logical scan of `tiles` tiles: per-tile buffers sized, counters and the
+// per-256-tile match sums zeroed.
 int begin_scan(rk_ctx* c, uint64_t tiles, cudaStream_t s) {
-  if (int r = grow(&c->d_status, &c->status_cap, tiles, true, s)) return r;
-  c->epoch = (c->epoch + 1) & 0xffff;
-  if (c->epoch == 0) {
-    RK_CUDA(cudaMemsetAsync(c->d_status, 0, c->status_cap * sizeof(uint64_t), s));
-    c->epoch = 1;
-  }
+  if (int r = grow(&c->d_tile_info, &c->tile_info_cap, tiles, false, s)) return r;
+  if (int r = grow(&c->d_masks, &c->masks_cap, tiles * (uint64_t)(kTileChunks * 32), false, s))
+    return r;
+  const uint64_t nb = (tiles + kEmitTiles - 1) / kEmitTiles;
+  if (int r = grow(&c->d_block_sums, &c->block_sums_cap, nb, false, s)) return r;
   RK_CUDA(cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), s));
+  RK_CUDA(cudaMemsetAsync(c->d_block_sums, 0, nb * sizeof(unsigned long long), s));
   return RK_OK;
 }
 
+// Orders the offsets of a logical scan whose tiles are sequence numbers [0, tiles)
+// starting at a-space tile `tile0`.
+int emit(rk_ctx* c, uint64_t tiles, uint64_t tile0, int64_t start_bias, int64_t* d_out,
+         uint64_t cap, cudaStream_t s) {
+  EmitArgs e;
+  e.tile_info = c->d_tile_info;
+  e.masks = c->d_masks;
+  e.block_sums = c->d_block_sums;
+  e.num_tiles = tiles;
+  e.tile0 = tile0;
+  e.start_bias = start_bias;
+  e.out = d_out;
+  e.cap = d_out ? cap : 0;
+  e.counters = c->d_counters;
+  RK_CUDA(launch_emit(e, s));
+  ++c->launches;
+  return RK_OK;
+}
+
+TextGeom text_geom(const Geometry& g, uint64_t n, uint32_t m, uint64_t seq_base) {
+  TextGeom t;
+  t.abase = g.abase;
+  t.amis = g.amis;
+  t.n = n;
+  t.ja_lo = g.ja_lo;
+  t.ja_hi = g.ja_hi;
+  t.tile0 = g.tile_first;
+  t.num_tiles = g.num_tiles;
+  t.seq_base = seq_base;
+  t.m = m;
+  t.K = roll_consts(m);
+  return t;
+}
+
+// Persistent grid: every SM full, never more warps than tiles.
+int grid_for(uint64_t tiles, int num_sms, int blocks_per_sm) {
+  const uint64_t max_grid = (uint64_t)num_sms * (uint64_t)blocks_per_sm;
+  const uint64_t want = (tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  return (int)std::max<uint64_t>(1, std::min(max_grid, want));
+}
+
 int launch_one(rk_ctx* c, const uint8_t* d_text, uint64_t n, uint32_t m, uint64_t hx,
-               uint64_t start, uint64_t stop, int64_t* d_out, uint64_t cap, int64_t bias,
-               uint64_t seq_base, bool last, const PatWords& pw, cudaStream_t s) {
+               uint64_t start, uint64_t stop, uint64_t seq_base, const PatWords& pw, cudaStream_t s) {
   const Geometry g = geometry(d_text, m, start, stop);
   ScanArgs a{};
-  a.abase = g.abase;
-  a.amis = g.amis;
-  a.n = n;
+  a.g = text_geom(g, n, m, seq_base);
   a.pattern = c->d_pattern;
   a.hx = hx;
-  a.ja_lo = g.ja_lo;
-  a.ja_hi = g.ja_hi;
-  a.tile0 = g.tile_first;
-  a.num_tiles = g.num_tiles;
-  a.seq_base = seq_base;
-  a.out_bias = bias;
-  a.out = d_out;
-  a.cap = d_out ? cap : 0;
-  a.ticket = c->d_ticket;
   a.counters = c->d_counters;
-  a.status = c->d_status;
-  a.m = m;
-  a.epoch = c->epoch;
-  a.last_launch = last ? 1u : 0u;
+  a.block_sums = c->d_block_sums;
+  a.tile_info = c->d_tile_info;
+  a.masks = c->d_masks;
   a.pw = pw;
-  const uint64_t max_grid = (uint64_t)c->num_sms * (uint64_t)scan_blocks_per_sm(m);
-  const uint64_t want = (g.num_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  const int grid = (int)std::max<uint64_t>(1, std::min(max_grid, want));
-  a.ticket_base = c->ticket_next;
-  c->ticket_next += g.num_tiles + (uint64_t)grid * kWarpsPerBlock;
-  RK_CUDA(launch_scan(a, grid, s));
+  RK_CUDA(launch_scan(a, grid_for(g.num_tiles, c->num_sms, scan_blocks_per_sm(m)), s));
   ++c->launches;
   return RK_OK;
 }
@@ -196,15 +235,27 @@ int check_scan_args(const uint8_t* text, uint64_t n, const uint8_t* h_pattern, u
 // m <= 24: every window hash is < 2^32, so a 64-bit hx >= 2^32 can never be hit.
 bool hash_unreachable(uint32_t m, uint64_t hx) { return m <= 24 && (hx >> 32) != 0; }
 
-// Device copy of the pattern; re-uploaded only when the bytes change.
+// Device copy of the pattern from a small per-context cache (64 slots, LRU), so
+// repeated scans with the same patterns -- a length sweep, a service loop -- issue no
+// host-to-device copy and no synchronisation.  A slot is only overwritten after the
+// stream has drained, because an earlier kernel may still be reading it.
 int upload_pattern(rk_ctx* c, const uint8_t* h_pattern, uint32_t m, cudaStream_t s) {
-  if (c->d_pattern && c->pattern_host.size() == m &&
-      memcmp(c->pattern_host.data(), h_pattern, m) == 0)
-    return RK_OK;
-  if (int r = grow(&c->d_pattern, &c->pattern_cap, m, false, s)) return r;
-  c->pattern_host.assign(h_pattern, h_pattern + m);
-  RK_CUDA(cudaMemcpyAsync(c->d_pattern, c->pattern_host.data(), m, cudaMemcpyHostToDevice, s));
-  RK_CUDA(cudaStreamSynchronize(s));  // pattern_host may change on the next call
+  ++c->pat_clock;
+  rk_ctx::PatSlot* victim = &c->pat_cache[0];
+  for (auto& sl : c->pat_cache) {
+    if (sl.d && sl.bytes.size() == m && memcmp(sl.bytes.data(), h_pattern, m) == 0) {
+      sl.last_use = c->pat_clock;
+      c->d_pattern = sl.d;
+      return RK_OK;
+    }
+    if (sl.last_use < victim->last_use) victim = &sl;
+  }
+  RK_CUDA(cudaStreamSynchronize(s));
+  if (int r = grow(&victim->d, &victim->cap, m, false, s)) return r;
+  victim->bytes.assign(h_pattern, h_pattern + m);
+  victim->last_use = c->pat_clock;
+  RK_CUDA(cudaMemcpy(victim->d, victim->bytes.data(), m, cudaMemcpyHostToDevice));
+  c->d_pattern = victim->d;
   return RK_OK;
 }
 
@@ -218,8 +269,10 @@ int enqueue_scan(rk_ctx* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_
   if (int r = upload_pattern(c, h_pattern, m, s)) return r;
   const Geometry g = geometry(d_text, m, start, stop);
   if (int r = begin_scan(c, g.num_tiles, s)) return r;
-  return launch_one(c, d_text, n, m, hx, start, stop, d_out, cap, bias, 0, true,
-                    pack_pattern(h_pattern, m), s);
+  if (int r = launch_one(c, d_text, n, m, hx, start, stop, 0, pack_pattern(h_pattern, m), s))
+    return r;
+  return emit(c, g.num_tiles, g.tile_first, bias - (int64_t)g.amis - (int64_t)m + 1, d_out, cap,
+              s);
 }
 
 int read_counters(rk_ctx* c, uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits,
@@ -266,8 +319,6 @@ int rk_ctx_create(int device, rk_ctx_t** out) {
   rk_ctx* c = new rk_ctx();
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
-  RK_CUDA(cudaMalloc(&c->d_ticket, sizeof(unsigned long long)));
-  RK_CUDA(cudaMemset(c->d_ticket, 0, sizeof(unsigned long long)));
   RK_CUDA(cudaMalloc(&c->d_counters, 4 * sizeof(unsigned long long)));
   RK_CUDA(cudaMallocHost(&c->h_counters, 4 * sizeof(unsigned long long)));
   RK_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
@@ -282,11 +333,12 @@ int rk_ctx_destroy(rk_ctx_t* c) {
   if (!c) return RK_OK;
   DeviceGuard g(c->device);
   cudaDeviceSynchronize();
-  cudaFree(c->d_ticket);
   cudaFree(c->d_counters);
   cudaFreeHost(c->h_counters);
-  cudaFree(c->d_status);
-  cudaFree(c->d_pattern);
+  cudaFree(c->d_tile_info);
+  cudaFree(c->d_masks);
+  cudaFree(c->d_block_sums);
+  for (auto& sl : c->pat_cache) cudaFree(sl.d);
   cudaFree(c->d_stage);
   cudaFree(c->d_out_stage);
   for (auto* h : c->h_ring) cudaFreeHost(h);
@@ -410,20 +462,22 @@ int rk_scan_host(rk_ctx_t* c, const uint8_t* h_text, uint64_t n, const uint8_t* 
     }
     const uint64_t ws = e_lo - (m - 1), we = e_hi - (m - 1);  // windows ending in the chunk
     const Geometry gk = geometry(c->d_stage, m, ws, we);
-    if (int r = launch_one(c, c->d_stage, n, m, hx, ws, we, c->d_out_stage, icap, 0,
-                           gk.tile_first - gall.tile_first, k == k1, pw, sc))
+    if (int r = launch_one(c, c->d_stage, n, m, hx, ws, we, gk.tile_first - gall.tile_first, pw,
+                           sc))
       return r;
   }
+  const int64_t start_bias = -(int64_t)m + 1;  // staging buffer: a-space == text index
+  if (int r = emit(c, gall.num_tiles, gall.tile_first, start_bias, c->d_out_stage, icap, sc))
+    return r;
   uint64_t mt = 0, co = 0, hh = 0;
   if (int r = read_counters(c, &mt, &co, &hh, sc)) return r;
   if (mt > icap) {
     // more offsets than the staging output held: rescan the staged text on the device
+    // more offsets than the staging output held: re-emit from the kept masks (no rescan)
     if (int r = grow(&c->d_out_stage, &c->out_stage_cap, mt, false, sc)) return r;
-    if (int r = begin_scan(c, gall.num_tiles, sc)) return r;
-    if (int r = launch_one(c, c->d_stage, n, m, hx, start, stop, c->d_out_stage, mt, 0, 0, true,
-                           pw, sc))
+    if (int r = emit(c, gall.num_tiles, gall.tile_first, start_bias, c->d_out_stage, mt, sc))
       return r;
-    if (int r = read_counters(c, &mt, &co, &hh, sc)) return r;
+    if (int r = read_counters(c, &mt, nullptr, nullptr, sc)) return r;
   }
   c->host_last = mt;
   const uint64_t nout = std::min(mt, cap);
@@ -549,15 +603,8 @@ int rk_multi_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
 
   const uint64_t nw = n - m + 1;
   const Geometry gg = geometry(d_text, m, 0, nw);
-  MultiHostPlan p{};
-  p.abase = gg.abase;
-  p.amis = gg.amis;
-  p.n = n;
-  p.ja_lo = gg.ja_lo;
-  p.ja_hi = gg.ja_hi;
-  p.tile0 = gg.tile_first;
-  p.num_tiles = gg.num_tiles;
-  p.cap = cap;
+  MultiArgs p{};
+  p.g = text_geom(gg, n, m, 0);
   p.pats = c->d_mpats;
   p.phash = c->d_mphash;
   p.filter = c->d_mfilter;
@@ -565,16 +612,11 @@ int rk_multi_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
   p.order = c->d_morder;
   p.out_off = d_off;
   p.out_idx = d_idx;
-  p.ticket = c->d_ticket;
+  p.cap = cap;
   p.counters = c->d_counters;
-  p.m = m;
   p.P = P;
   p.tsize = tsize;
-  const uint64_t want = (gg.num_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->num_sms * 2, want));
-  p.ticket_base = c->ticket_next;
-  c->ticket_next += gg.num_tiles + (uint64_t)grid * kWarpsPerBlock;
-  RK_CUDA(launch_multi_plan(p, grid, s));
+  RK_CUDA(launch_multi(p, grid_for(gg.num_tiles, c->num_sms, multi_blocks_per_sm(m, tsize)), s));
   ++c->launches;
   RK_CUDA(cudaMemcpyAsync(c->h_counters, c->d_counters, sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, s));

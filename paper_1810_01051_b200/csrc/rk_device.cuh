@@ -11,6 +11,13 @@
 // A window is a hash hit iff all 64 bits agree; a hit is a match iff its bytes equal the
 // pattern, otherwise it is a collision (_scan.py:38-49).  The kernels filter on the exact
 // low-32 value and confirm the high half and the bytes only for the rare survivors.
+//
+// Work decomposition.  Positions are window END positions in "a-space" (offsets from
+// the 32-byte-aligned address at or below the text).  A chunk is 1 KiB of end positions
+// (32 per lane); a tile is kTileChunks chunks and is the unit of ordered emission.  Warp
+// w of W owns tiles w, w+W, w+2W, ... and streams them through a per-warp ring of
+// shared-memory stages filled by TMA bulk copies (cp.async.bulk + mbarrier), so the bytes
+// in flight live in shared memory, not registers.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -20,19 +27,20 @@ namespace rkb {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kR = 32;                       // end positions per lane per chunk
 constexpr int kChunk = 32 * kR;              // 1 KiB of end positions per warp step
-constexpr int kTileChunks = 16;              // chunks per ordered tile
-constexpr int kTile = kChunk * kTileChunks;  // 16 KiB per tile (unit of ordered compaction)
-constexpr int kPrefetch = 4;                 // chunks in flight per warp (4 x 1 KiB)
+constexpr int kTileChunks = 8;               // chunks per tile
+constexpr int kTile = kChunk * kTileChunks;  // 8 KiB per tile (unit of ordered emission)
 constexpr int kWarpsPerBlock = 8;
 constexpr int kBlock = 32 * kWarpsPerBlock;
 constexpr uint32_t kFoldW = 0x01020408u;     // dp4a weights: 8*b0 + 4*b1 + 2*b2 + b3
+constexpr int kEmitTiles = 256;              // tiles per block of the ordered emission
 
-// Look-back tile status word: [epoch:16 | flag:2 | value:46].
-constexpr uint64_t kFlagAgg = 1, kFlagIncl = 2;
-__host__ __device__ __forceinline__ uint64_t pack_status(uint32_t epoch, uint64_t flag,
-                                                         uint64_t v) {
-  return (uint64_t(epoch & 0xffff) << 48) | (flag << 46) | (v & ((1ull << 46) - 1));
-}
+// TMA ring: kStages stages of kStageChunks chunks, each stage preceded by the 32 bytes
+// before its first chunk (the lookback the first lane needs).
+constexpr int kStageChunks = 2;
+constexpr int kStages = 4;
+constexpr int kStageBytes = kStageChunks * kChunk + 32;  // 2080 (multiple of 16)
+constexpr int kStagesPerTile = kTileChunks / kStageChunks;
+static_assert(kTileChunks % kStageChunks == 0, "stage/tile");
 
 struct Vec32 {
   uint32_t w[8];
@@ -42,32 +50,39 @@ struct PatWords {
   uint32_t w[8];  // pattern bytes (m < 32), little-endian packed
 };
 
-// Arguments of one single-pattern scan launch.  Positions are in "a-space": offsets
-// from `abase`, the 32-byte-aligned address at or below the text pointer; text byte i
-// sits at a-position i + amis.
-struct ScanArgs {
-  const uint8_t* abase;
-  uint64_t amis;        // text - abase, in [0, 32)
-  uint64_t n;           // text length in bytes
-  const uint8_t* pattern;  // device copy of the pattern (m bytes)
-  uint64_t hx;          // 64-bit pattern hash
-  uint64_t ja_lo, ja_hi;   // valid window END positions, a-space, [lo, hi)
-  uint64_t tile0;       // a-space tile index of the first tile of this launch
-  uint64_t num_tiles;   // tiles in this launch
-  uint64_t seq_base;    // look-back sequence number of this launch's first tile
-  uint64_t ticket_base; // value of *ticket before this launch
-  int64_t out_bias;     // added to every reported window start (shards / staging)
-  int64_t* out;         // ordered window starts, first `cap` written
-  uint64_t cap;
-  unsigned long long* ticket;
-  unsigned long long* counters;  // [0]=matches total, [1]=hash_hits, [2]=collisions
-  uint64_t* status;     // look-back status per sequence number
-  uint32_t m;
-  uint32_t epoch;
-  uint32_t last_launch; // 1 if this launch's last tile ends the logical scan
-  PatWords pw;
+// Runtime copies of small constants.  The roll is written as x * k + y with k in a
+// register so ptxas emits IMAD (FMA pipe) instead of LEA/IADD3 (ALU pipe): the per-byte
+// work is then split between the two integer pipes ("instruction budget").
+struct RollConsts {
+  uint32_t k2, k8, k16;  // 2, 8, 16
+  uint32_t negpow;       // -(2^m) mod 2^32 (m < 32)
 };
 
+// Text geometry shared by every streaming kernel.
+struct TextGeom {
+  const uint8_t* abase;  // 32-byte-aligned address at or below the text
+  uint64_t amis;         // text - abase, in [0, 32)
+  uint64_t n;            // text length in bytes
+  uint64_t ja_lo, ja_hi; // valid window END positions, a-space, [lo, hi)
+  uint64_t tile0;        // a-space tile index of the launch's first tile
+  uint64_t num_tiles;    // tiles in this launch
+  uint64_t seq_base;     // sequence number of this launch's first tile (staged scans)
+  uint32_t m;
+  RollConsts K;
+
+  __device__ __forceinline__ int64_t tile_a(uint64_t t) const {
+    return (int64_t)((tile0 + t) * (uint64_t)kTile);
+  }
+  // every byte a tile's fast pass touches, [ta - 32, ta + kTile), lies in the text
+  __device__ __forceinline__ bool interior(int64_t ta) const {
+    return ta - 32 >= (int64_t)amis && ta + kTile <= (int64_t)(amis + n);
+  }
+  __device__ __forceinline__ bool valid_end(int64_t ja) const {
+    return ja >= (int64_t)ja_lo && ja < (int64_t)ja_hi;
+  }
+};
+
+// ------------------------------------------------------------------------- loads
 __device__ __forceinline__ Vec32 ldg256(const uint8_t* p) {
   Vec32 v;
   asm volatile(
@@ -78,36 +93,48 @@ __device__ __forceinline__ Vec32 ldg256(const uint8_t* p) {
   return v;
 }
 
+// 4 text bytes at a-position p, zero outside the text (cold path, kept out of line).
+static __device__ __noinline__ uint32_t edge_word(const uint8_t* abase, int64_t lo, int64_t hi,
+                                                  int64_t p) {
+  uint32_t w = 0;
+  for (int b = 0; b < 4; ++b) {
+    const int64_t q = p + b;
+    const uint32_t byte = (q >= lo && q < hi) ? (uint32_t)abase[q] : 0u;
+    w |= byte << (8 * b);
+  }
+  return w;
+}
+
 // 32 bytes at a-position p (32-aligned, may be negative).  Bytes outside the text read
 // as 0; positions whose windows would touch them are masked by the validity check.
-__device__ __forceinline__ Vec32 load_edge(const ScanArgs& a, int64_t p) {
-  const int64_t lo = (int64_t)a.amis, hi = (int64_t)(a.amis + a.n);
-  if (p >= lo && p + 32 <= hi) return ldg256(a.abase + p);
+__device__ __forceinline__ Vec32 load_edge(const TextGeom& g, int64_t p) {
+  const int64_t lo = (int64_t)g.amis, hi = (int64_t)(g.amis + g.n);
+  if (p >= lo && p + 32 <= hi) return ldg256(g.abase + p);
   Vec32 v;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    uint32_t w = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int64_t q = p + 4 * i + b;
-      const uint32_t byte = (q >= lo && q < hi) ? (uint32_t)a.abase[q] : 0u;
-      w |= byte << (8 * b);
-    }
-    v.w[i] = w;
-  }
+#pragma unroll 1
+  for (int i = 0; i < 8; ++i) v.w[i] = edge_word(g.abase, lo, hi, p + 4 * i);
   return v;
 }
 
-__device__ __forceinline__ uint32_t bsel(uint32_t w, int k) {
-  return __byte_perm(w, 0u, 0x4440u | (uint32_t)k);
+// 32 bytes of shared memory at p (16-byte aligned).
+__device__ __forceinline__ Vec32 lds32(const uint8_t* p) {
+  const uint4 x = *reinterpret_cast<const uint4*>(p);
+  const uint4 y = *reinterpret_cast<const uint4*>(p + 16);
+  Vec32 v;
+  v.w[0] = x.x;
+  v.w[1] = x.y;
+  v.w[2] = x.z;
+  v.w[3] = x.w;
+  v.w[4] = y.x;
+  v.w[5] = y.y;
+  v.w[6] = y.z;
+  v.w[7] = y.w;
+  return v;
 }
 
-// Byte i of the 64-byte window [J-32, J+32) held as lb[0..7] ++ w[0..7].
-template <int I>
-__device__ __forceinline__ uint32_t byte64(const uint32_t (&lb)[8], const uint32_t (&w)[8]) {
-  static_assert(I >= 0 && I < 64, "byte index");
-  if constexpr (I < 32) return bsel(lb[I >> 2], I & 3);
-  else return bsel(w[(I - 32) >> 2], I & 3);
+// ------------------------------------------------------------------------- bytes
+__device__ __forceinline__ uint32_t bsel(uint32_t w, int k) {
+  return __byte_perm(w, 0u, 0x4440u | (uint32_t)k);
 }
 
 // fold of 32 bytes, mod 2^32 (= S at the last byte): 8 dp4a + 7 shifts.
@@ -124,7 +151,6 @@ __device__ __forceinline__ uint32_t fold_tail(const uint32_t (&lb)[8]) {
   static_assert(M >= 1 && M < 32, "tail");
   constexpr int first = 32 - M;
   uint32_t s = 0;
-  // leading partial word byte by byte, then whole words by dp4a
 #pragma unroll
   for (int i = first; i < ((first + 3) & ~3); ++i) s = 2u * s + bsel(lb[i >> 2], i & 3);
 #pragma unroll
@@ -132,12 +158,210 @@ __device__ __forceinline__ uint32_t fold_tail(const uint32_t (&lb)[8]) {
   return s;
 }
 
-__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  return v;
+// dp4a with unsigned text bytes and signed weights (PTX dp4a.u32.s32).
+__device__ __forceinline__ uint32_t dp4a_us(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
 }
 
+// ---------------------------------------------------------------------------------
+// The fast roll over one chunk: the lane owns window END positions [J, J+32), its 32
+// bytes in v; for M < 32, lb holds the 32 bytes before J.  Returns whether
+// pred(low32 hash) held at any of its positions.
+//
+//  M >= 32: S(j) = fold of t[j-31..j] (mod 2^32) = low32 of every window hash.  Per
+//    4-byte word w starting from S:  S1 = 2S + b0, S2 = 2S1 + b1 (PRMT + IMAD),
+//    S3 = 8S + dp4a(w,{4,2,1,0}), S4 = 16S + dp4a(w,{8,4,2,1}) (IDP + IMAD): 6 ALU +
+//    6 FMA-pipe instructions per 4 bytes including the 4 compares.  The lane's seed
+//    S(J-1) is the previous lane's 32-byte fold F (one shfl), because 2^32 = 0; lane 0
+//    takes carryS (the previous chunk's lane 31, or the tile's lookback fold).
+//  M < 32: exact roll L' = 2L + in - 2^M out seeded with the fold of the M bytes before
+//    J, alternating two instruction mixes so the ALU and FMA pipes carry ~2.5
+//    instructions per byte each.
+template <int M, class Pred>
+__device__ __forceinline__ bool fast_chunk(const Vec32& v, const uint32_t (&lb)[8], int lane,
+                                           uint32_t& carryS, const RollConsts& K, Pred pred) {
+  bool any = false;
+  if constexpr (M >= 32) {
+    uint32_t c4[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c4[i] = __dp4a(v.w[i], kFoldW, 0u);
+    uint32_t F = c4[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) F = F * K.k16 + c4[i];
+    const uint32_t up = __shfl_up_sync(kFull, F, 1);
+    const uint32_t top = __shfl_sync(kFull, F, 31);
+    uint32_t S = lane == 0 ? carryS : up;
+    carryS = top;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t w = v.w[i];
+      const uint32_t s1 = S * K.k2 + bsel(w, 0);
+      const uint32_t s2 = s1 * K.k2 + bsel(w, 1);
+      const uint32_t s3 = S * K.k8 + __dp4a(w, 0x00010204u, 0u);
+      const uint32_t s4 = S * K.k16 + c4[i];
+      any |= pred(s1);
+      any |= pred(s2);
+      any |= pred(s3);
+      any |= pred(s4);
+      S = s4;
+    }
+  } else {
+    uint32_t L = fold_tail<M>(lb);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const int io = 32 + k - M;
+      const uint32_t wout = io < 32 ? lb[io >> 2] : v.w[(io - 32) >> 2];
+      if (k & 1) {
+        // ALU-heavy mix: both bytes by PRMT, two IMADs
+        L = L * K.k2 + bsel(v.w[k >> 2], k & 3);
+        L = bsel(wout, io & 3) * K.negpow + L;
+      } else if constexpr (M <= 7) {
+        // out weight -2^M fits a signed byte: both bytes extracted by dp4a (FMA pipe)
+        const uint32_t t = __dp4a(v.w[k >> 2], 1u << (8 * (k & 3)), L * K.k2);
+        L = dp4a_us(wout, (uint32_t)(uint8_t)(-(1 << M)) << (8 * (io & 3)), t);
+      } else {
+        // FMA-heavy mix: in by dp4a extract-and-add, out by PRMT + IMAD
+        const uint32_t t = __dp4a(v.w[k >> 2], 1u << (8 * (k & 3)), L * K.k2);
+        L = bsel(wout, io & 3) * K.negpow + t;
+      }
+      any |= pred(L);
+    }
+  }
+  return any;
+}
+
+// ------------------------------------------------------------------------- TMA ring
+struct __align__(16) WarpRing {
+  uint8_t buf[kStages][kStageBytes];
+  unsigned long long bar[kStages];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void ring_init(WarpRing* R, int lane) {
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&R->bar[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Producer side of a warp's stream: issues the stages of the warp's interior tiles in
+// consumption order, keeping at most kStages in flight.  Warp-uniform state; lane 0
+// issues the copies.
+struct Producer {
+  uint64_t pt;      // tile of the next stage to issue
+  uint32_t ps;      // stage index within that tile
+  uint32_t issued;  // stages issued so far
+};
+
+__device__ __forceinline__ void produce(const TextGeom& g, WarpRing* R, Producer& P,
+                                        uint32_t consumed, uint64_t W, int lane) {
+  while (P.issued < consumed + kStages && P.pt < g.num_tiles) {
+    const int64_t ta = g.tile_a(P.pt);
+    if (!g.interior(ta)) {  // edge tiles are read directly by the consumer
+      P.pt += W;
+      P.ps = 0;
+      continue;
+    }
+    const int slot = P.issued % kStages;
+    if (lane == 0)
+      bulk_g2s(R->buf[slot], g.abase + ta + (int64_t)P.ps * (kStageChunks * kChunk) - 32,
+               kStageBytes, &R->bar[slot]);
+    ++P.issued;
+    if (++P.ps == kStagesPerTile) {
+      P.ps = 0;
+      P.pt += W;
+    }
+  }
+}
+
+// Fast pass over tile t: bitmask of its chunks in which some lane saw pred() hold.
+// Interior tiles come from the ring; edge tiles go through the bounds-checked loader.
+template <int M, class Pred>
+__device__ __forceinline__ uint32_t fast_tile(const TextGeom& g, WarpRing* R, Producer& P,
+                                              uint32_t& consumed, uint64_t t, uint64_t W,
+                                              int lane, Pred pred) {
+  const int64_t ta = g.tile_a(t);
+  uint32_t cand = 0;
+  uint32_t carryS = 0;
+  uint32_t lb[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) lb[i] = 0;
+  if (g.interior(ta)) {
+#pragma unroll 1
+    for (int s = 0; s < kStagesPerTile; ++s) {
+      const int slot = consumed % kStages;
+      mbar_wait(&R->bar[slot], (consumed / kStages) & 1u);
+      const uint8_t* st = R->buf[slot];
+      if constexpr (M >= 32) {
+        if (s == 0) carryS = fold32(lds32(st).w);  // tile lookback, broadcast read
+      }
+#pragma unroll
+      for (int j = 0; j < kStageChunks; ++j) {
+        const Vec32 v = lds32(st + 32 + j * kChunk + lane * kR);
+        if constexpr (M < 32) {
+          const Vec32 l = lds32(st + j * kChunk + lane * kR);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) lb[i] = l.w[i];
+        }
+        const bool any = fast_chunk<M>(v, lb, lane, carryS, g.K, pred);
+        if (__any_sync(kFull, any)) cand |= 1u << (s * kStageChunks + j);
+      }
+      ++consumed;
+      produce(g, R, P, consumed, W, lane);  // refill the slot just read
+    }
+  } else {
+    if constexpr (M >= 32) carryS = fold32(load_edge(g, ta - 32).w);
+#pragma unroll 1
+    for (int c = 0; c < kTileChunks; ++c) {
+      const int64_t J = ta + c * kChunk + lane * kR;
+      const Vec32 v = load_edge(g, J);
+      if constexpr (M < 32) {
+        const Vec32 l = load_edge(g, J - 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) lb[i] = l.w[i];
+      }
+      const bool any = fast_chunk<M>(v, lb, lane, carryS, g.K, pred);
+      if (__any_sync(kFull, any)) cand |= 1u << c;
+    }
+  }
+  return cand;
+}
+
+// ------------------------------------------------------------------------- warp utils
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -145,52 +369,6 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
     if (lane >= o) v += u;
   }
   return v;
-}
-
-__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// Decoupled look-back (single-pass ordered prefix over tiles).  Every tile publishes its
-// aggregate before waiting, and only waits on tiles with a smaller sequence number that
-// a running warp already owns, so progress is guaranteed.  Returns the exclusive prefix.
-__device__ __forceinline__ uint64_t lookback(uint64_t* status, uint64_t seq, uint32_t epoch,
-                                             uint64_t agg, int lane) {
-  if (seq == 0) {
-    if (lane == 0) st_relaxed_u64(&status[0], pack_status(epoch, kFlagIncl, agg));
-    return 0;
-  }
-  if (lane == 0) st_relaxed_u64(&status[seq], pack_status(epoch, kFlagAgg, agg));
-  uint64_t excl = 0;
-  int64_t pred = (int64_t)seq - 1;
-  for (;;) {
-    const int64_t idx = pred - lane;
-    uint64_t s = 0, flag = 0;
-    for (;;) {
-      if (idx >= 0) {
-        s = ld_relaxed_u64(&status[idx]);
-        flag = ((s >> 48) == (epoch & 0xffff)) ? ((s >> 46) & 3) : 0;
-      } else {
-        s = 0;
-        flag = kFlagIncl;  // before the first tile: prefix 0
-      }
-      if (!__any_sync(kFull, flag == 0)) break;
-      __nanosleep(32);
-    }
-    const unsigned incl = __ballot_sync(kFull, flag == kFlagIncl);
-    const int first = incl ? __ffs(incl) - 1 : 31;
-    const uint64_t v = (lane <= first) ? (s & ((1ull << 46) - 1)) : 0;
-    excl += warp_sum_u64(v);
-    if (incl) break;
-    pred -= 32;
-  }
-  if (lane == 0) st_relaxed_u64(&status[seq], pack_status(epoch, kFlagIncl, excl + agg));
-  return excl;
 }
 
 }  // namespace rkb

@@ -7,28 +7,54 @@
 
 namespace rkb {
 
-// single pattern (rk_scan.cu)
+// single pattern (rk_scan.cu, kernels in rk_scan_impl.cuh)
+struct ScanArgs {
+  TextGeom g;
+  const uint8_t* pattern;         // device copy of the pattern (m bytes)
+  uint64_t hx;                    // 64-bit pattern hash
+  unsigned long long* counters;   // [1]=hash_hits, [2]=collisions ([0] set by emit)
+  unsigned long long* block_sums; // matches per kEmitTiles consecutive tiles
+  uint32_t* tile_info;            // per sequence number: matches | chunk bitmap << 16
+  uint32_t* masks;                // per sequence number: kTileChunks x 32 lane hit masks
+  PatWords pw;
+};
+size_t scan_smem_bytes();
 int scan_blocks_per_sm(uint32_t m);
 cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t s);
 
-// multi pattern (rk_multi.cu)
-struct MultiHostPlan {
-  const uint8_t* abase;
-  uint64_t amis, n, ja_lo, ja_hi, tile0, num_tiles, ticket_base, cap;
-  const uint8_t* pats;
-  const uint64_t* phash;
-  const uint32_t* filter;
-  const uint2* table;
-  const uint32_t* order;
-  int64_t* out_off;
-  uint32_t* out_idx;
-  unsigned long long* ticket;
-  unsigned long long* counters;
-  uint32_t m, P, tsize;
+// ordered emission (rk_emit.cu)
+struct EmitArgs {
+  const uint32_t* tile_info;
+  const uint32_t* masks;
+  const unsigned long long* block_sums;
+  uint64_t num_tiles;   // sequence numbers of the logical scan
+  uint64_t tile0;       // a-space tile index of sequence number 0
+  int64_t start_bias;   // written value = a-space end position + start_bias
+  int64_t* out;
+  uint64_t cap;
+  unsigned long long* counters;  // [0] <- total matches
 };
+cudaError_t launch_emit(const EmitArgs& e, cudaStream_t s);
+
+// multi pattern (rk_multi.cu, kernels in rk_multi_impl.cuh)
 constexpr int kMultiFilterWords = (1 << 16) / 32;
 constexpr uint32_t kMultiEmpty = 0xffffffffu;
-cudaError_t launch_multi_plan(const MultiHostPlan& p, int grid, cudaStream_t s);
+struct MultiArgs {
+  TextGeom g;
+  const uint8_t* pats;        // P * m bytes, deduplicated, index order
+  const uint64_t* phash;      // 64-bit hash per pattern
+  const uint32_t* filter;     // kMultiFilterWords words
+  const uint2* table;         // tsize entries: {key, (first << 13) | count}, y = empty marker
+  const uint32_t* order;      // pattern indices grouped by key
+  int64_t* out_off;
+  uint32_t* out_idx;
+  uint64_t cap;
+  unsigned long long* counters;  // [0] = pairs found
+  uint32_t P, tsize;
+};
+size_t multi_smem_bytes(uint32_t tsize);
+int multi_blocks_per_sm(uint32_t m, uint32_t tsize);
+cudaError_t launch_multi(const MultiArgs& a, int grid, cudaStream_t s);
 
 // auxiliaries (rk_aux.cu)
 cudaError_t launch_window_hashes(const uint8_t* text, uint64_t n, uint32_t m, uint64_t start,

@@ -1,0 +1,180 @@
+// rk_scan_impl.cuh -- single-pattern exact scan for sm_100a (the reference's _scan_range,
+// /root/reference/pkg/src/rkmatch/_scan.py:28-50, and the range partition + ordered merge
+// of search_parallel, parallel.py:155-172):
+//
+//   TMA bulk copies (2 KiB stages, 4 in flight per warp) -> shared memory
+//     -> exact 32-bit rolling hash per window, compared with low32(hx)
+//        (candidates are ~2^-32 of windows on random text)
+//     -> candidate chunks: 64-bit hash + byte verify -> match / collision counters
+//     -> per-tile match count + hit masks (global), consumed by rk_emit.cu, which
+//        writes the ordered int64 window starts.
+//
+// The scan kernel never waits on another warp, and reads the text from HBM once.
+#pragma once
+#include "rk_device.cuh"
+#include "rk_internal.h"
+
+namespace rkb {
+
+// 64-bit hash of the window whose last byte is at text index je (global memory).
+static __device__ __noinline__ uint64_t hash_window_global(const uint8_t* text, uint32_t m,
+                                                          int64_t je) {
+  const int64_t span = m < 64 ? (int64_t)m : 64;
+  uint64_t h = 0;
+  for (int64_t i = je - span + 1; i <= je; ++i) h = (h << 1) + (uint64_t)text[i];
+  return h;
+}
+
+static __device__ __noinline__ bool verify_global(const uint8_t* text, const uint8_t* pattern,
+                                                  uint32_t m) {
+  for (uint32_t i = 0; i < m; ++i)
+    if (text[i] != pattern[i]) return false;
+  return true;
+}
+
+struct SlowOut {
+  uint32_t hm;    // hit bits (window end = J + k)
+  uint32_t hits;  // hash hits (matches + collisions)
+};
+
+// Slow pass over one chunk that had a candidate: exact per-window decisions.  The bytes
+// are re-read from global memory (L2-resident: the chunk was just streamed).
+template <int M>
+__device__ __forceinline__ SlowOut slow_chunk(const ScanArgs& a, int64_t J) {
+  const TextGeom& g = a.g;
+  SlowOut r{0u, 0u};
+  const Vec32 v = load_edge(g, J);
+  const Vec32 lbv = load_edge(g, J - 32);
+  const uint32_t T = (uint32_t)a.hx;
+  if constexpr (M >= 32) {
+    uint32_t S = fold32(lbv.w);
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k) {
+      S = 2u * S + bsel(v.w[k >> 2], k & 3);
+      if (S == T && g.valid_end(J + k)) {
+        const int64_t je = J + k - (int64_t)g.amis;  // text index of the last byte
+        const uint8_t* text = g.abase + g.amis;
+        if (hash_window_global(text, g.m, je) == a.hx) {
+          ++r.hits;
+          if (verify_global(text + je - (int64_t)g.m + 1, a.pattern, g.m)) r.hm |= 1u << k;
+        }
+      }
+    }
+  } else {
+    uint32_t L = fold_tail<M>(lbv.w);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const int io = 32 + k - M;
+      const uint32_t in = bsel(v.w[k >> 2], k & 3);
+      const uint32_t out =
+          io < 32 ? bsel(lbv.w[io >> 2], io & 3) : bsel(v.w[(io - 32) >> 2], io & 3);
+      L = 2u * L + in - (out << M);
+      if (L == T && g.valid_end(J + k)) {
+        // window bytes are positions [33+k-M, 32+k] of lbv ++ v
+        bool hit = true;
+        if constexpr (M > 24) {
+          uint64_t h = 0;
+#pragma unroll
+          for (int i = 0; i < M; ++i) {
+            const int p = 33 + k - M + i;
+            const uint32_t b =
+                p < 32 ? bsel(lbv.w[p >> 2], p & 3) : bsel(v.w[(p - 32) >> 2], p & 3);
+            h = (h << 1) + b;
+          }
+          hit = (h == a.hx);
+        }
+        if (hit) {
+          ++r.hits;
+          bool eq = true;
+#pragma unroll
+          for (int i = 0; i < M; ++i) {
+            const int p = 33 + k - M + i;
+            const uint32_t b =
+                p < 32 ? bsel(lbv.w[p >> 2], p & 3) : bsel(v.w[(p - 32) >> 2], p & 3);
+            eq &= (b == bsel(a.pw.w[i >> 2], i & 3));
+          }
+          if (eq) r.hm |= 1u << k;
+        }
+      }
+    }
+  }
+  return r;
+}
+
+// Exact pass over the candidate chunks of tile t; records the tile's match count,
+// chunk bitmap and hit masks for the ordered emission and adds the counters.
+template <int M>
+__device__ __forceinline__ void finish_tile(const ScanArgs& a, uint64_t t, uint32_t cand,
+                                            int lane) {
+  const TextGeom& g = a.g;
+  const int64_t ta = g.tile_a(t);
+  const uint64_t seq = g.seq_base + t;
+  uint32_t* tmask = a.masks + seq * (kTileChunks * 32);
+  uint32_t hitflags = 0, my_matches = 0, my_hits = 0;
+  while (cand) {
+    const int c = __ffs(cand) - 1;
+    cand &= cand - 1;
+    const SlowOut r = slow_chunk<M>(a, ta + c * kChunk + lane * kR);
+    my_hits += r.hits;
+    my_matches += __popc(r.hm);
+    if (__ballot_sync(kFull, r.hm != 0)) {
+      tmask[c * 32 + lane] = r.hm;
+      hitflags |= 1u << c;
+    }
+  }
+  const uint32_t agg = __reduce_add_sync(kFull, my_matches);
+  const uint32_t hits = __reduce_add_sync(kFull, my_hits);
+  if (lane == 0) {
+    a.tile_info[seq] = agg | (hitflags << 16);
+    if (agg) atomicAdd(&a.block_sums[seq / kEmitTiles], (unsigned long long)agg);
+    if (hits) {
+      atomicAdd(&a.counters[1], (unsigned long long)hits);
+      atomicAdd(&a.counters[2], (unsigned long long)(hits - agg));
+    }
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(kBlock) rk_scan_kernel(const ScanArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  WarpRing* R = reinterpret_cast<WarpRing*>(smem) + warp;
+  ring_init(R, lane);
+  const uint64_t W = (uint64_t)gridDim.x * kWarpsPerBlock;
+  const uint64_t w = (uint64_t)blockIdx.x * kWarpsPerBlock + warp;
+  const uint32_t T = (uint32_t)a.hx;
+  const auto pred = [T](uint32_t L) { return L == T; };
+  Producer P{w, 0u, 0u};
+  uint32_t consumed = 0;
+  produce(a.g, R, P, consumed, W, lane);
+  for (uint64_t t = w; t < a.g.num_tiles; t += W) {
+    const uint32_t cand = fast_tile<M>(a.g, R, P, consumed, t, W, lane, pred);
+    finish_tile<M>(a, t, cand, lane);
+  }
+}
+
+template <int M>
+cudaError_t launch_m(const ScanArgs& a, int grid, cudaStream_t s) {
+  const size_t smem = scan_smem_bytes();
+  static bool attr = false;  // per-variant one-time opt-in to > 48 KiB dynamic smem
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(rk_scan_kernel<M>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  rk_scan_kernel<M><<<grid, kBlock, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int M>
+int occupancy_m() {
+  cudaFuncSetAttribute(rk_scan_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)scan_smem_bytes());
+  int b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rk_scan_kernel<M>, kBlock, scan_smem_bytes());
+  return b > 0 ? b : 1;
+}
+
+}  // namespace rkb
