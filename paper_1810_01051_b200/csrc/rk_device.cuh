@@ -278,54 +278,78 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
       : "memory");
 }
 
-// Producer side of a warp's stream: issues the stages of the warp's interior tiles in
-// consumption order, keeping at most kStages in flight.  Warp-uniform state; lane 0
-// issues the copies.
-struct Producer {
-  uint64_t pt;      // tile of the next stage to issue
-  uint32_t ps;      // stage index within that tile
-  uint32_t issued;  // stages issued so far
+// A warp's stream: the stages of its interior tiles in order, kStages in flight.
+// Warp-uniform bookkeeping kept in 32-bit registers with incremental addressing; lane 0
+// issues the TMA copies.  Tiles outside [int_lo, int_hi) (at most the first and last of a
+// launch) are not staged -- the consumer reads them directly.
+struct Stream {
+  const uint8_t* psrc;  // global address of the next stage to issue (its lookback start)
+  uint32_t pt;          // tile of the next stage to issue
+  uint32_t ps;          // stage index within that tile
+  uint32_t pending;     // stages issued and not yet consumed
+  uint32_t cslot;       // ring slot the consumer reads next
+  uint32_t cphase;      // its mbarrier parity
+  uint32_t pslot;       // ring slot the producer fills next
+  uint32_t W, int_lo, int_hi, ntiles;
+  int64_t tile_jump;    // bytes from the end of one of the warp's tiles to its next one
 };
 
-__device__ __forceinline__ void produce(const TextGeom& g, WarpRing* R, Producer& P,
-                                        uint32_t consumed, uint64_t W, int lane) {
-  while (P.issued < consumed + kStages && P.pt < g.num_tiles) {
-    const int64_t ta = g.tile_a(P.pt);
-    if (!g.interior(ta)) {  // edge tiles are read directly by the consumer
-      P.pt += W;
-      P.ps = 0;
-      continue;
-    }
-    const int slot = P.issued % kStages;
-    if (lane == 0)
-      bulk_g2s(R->buf[slot], g.abase + ta + (int64_t)P.ps * (kStageChunks * kChunk) - 32,
-               kStageBytes, &R->bar[slot]);
-    ++P.issued;
-    if (++P.ps == kStagesPerTile) {
-      P.ps = 0;
-      P.pt += W;
-    }
+__device__ __forceinline__ void stream_seek(const TextGeom& g, Stream& S) {
+  while (S.pt < S.ntiles && (S.pt < S.int_lo || S.pt >= S.int_hi)) S.pt += S.W;
+  S.psrc = g.abase + g.tile_a(S.pt) - 32;
+}
+
+__device__ __forceinline__ void stream_issue(WarpRing* R, Stream& S, int lane) {
+  if (S.pt >= S.ntiles || S.pt >= S.int_hi) return;
+  if (lane == 0) bulk_g2s(R->buf[S.pslot], S.psrc, kStageBytes, &R->bar[S.pslot]);
+  S.pslot = (S.pslot + 1) & (kStages - 1);
+  ++S.pending;
+  S.psrc += kStageChunks * kChunk;
+  if (++S.ps == kStagesPerTile) {
+    S.ps = 0;
+    S.pt += S.W;
+    S.psrc += S.tile_jump;
   }
+}
+
+__device__ __forceinline__ void stream_init(const TextGeom& g, WarpRing* R, Stream& S, uint32_t w,
+                                            uint32_t W, int lane) {
+  static_assert((kStages & (kStages - 1)) == 0, "ring size must be a power of two");
+  // interior tiles are exactly [int_lo, int_hi): tile_a - 32 >= amis and
+  // tile_a + kTile <= amis + n, with tile_a = (tile0 + t) * kTile
+  const int64_t lo_a = (int64_t)g.amis + 32, hi_a = (int64_t)(g.amis + g.n) - kTile;
+  int64_t lo = (lo_a + kTile - 1) / kTile - (int64_t)g.tile0;
+  int64_t hi = (hi_a >= 0 ? hi_a / kTile + 1 : 0) - (int64_t)g.tile0;
+  S.int_lo = (uint32_t)(lo < 0 ? 0 : lo);
+  S.int_hi = (uint32_t)(hi < (int64_t)S.int_lo ? S.int_lo : (hi > (int64_t)g.num_tiles ? g.num_tiles : hi));
+  S.ntiles = (uint32_t)g.num_tiles;
+  S.W = W;
+  S.pt = w;
+  S.ps = 0;
+  S.pending = 0;
+  S.cslot = S.pslot = 0;
+  S.cphase = 0;
+  S.tile_jump = (int64_t)(W - 1) * kTile;
+  stream_seek(g, S);
+  for (int i = 0; i < kStages; ++i) stream_issue(R, S, lane);
 }
 
 // Fast pass over tile t: bitmask of its chunks in which some lane saw pred() hold.
 // Interior tiles come from the ring; edge tiles go through the bounds-checked loader.
 template <int M, class Pred>
-__device__ __forceinline__ uint32_t fast_tile(const TextGeom& g, WarpRing* R, Producer& P,
-                                              uint32_t& consumed, uint64_t t, uint64_t W,
-                                              int lane, Pred pred) {
+__device__ __forceinline__ uint32_t fast_tile(const TextGeom& g, WarpRing* R, Stream& S,
+                                              uint32_t t, int lane, Pred pred) {
   const int64_t ta = g.tile_a(t);
   uint32_t cand = 0;
   uint32_t carryS = 0;
   uint32_t lb[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) lb[i] = 0;
-  if (g.interior(ta)) {
+  if (t >= S.int_lo && t < S.int_hi) {
 #pragma unroll 1
     for (int s = 0; s < kStagesPerTile; ++s) {
-      const int slot = consumed % kStages;
-      mbar_wait(&R->bar[slot], (consumed / kStages) & 1u);
-      const uint8_t* st = R->buf[slot];
+      mbar_wait(&R->bar[S.cslot], S.cphase);
+      const uint8_t* st = R->buf[S.cslot];
       if constexpr (M >= 32) {
         if (s == 0) carryS = fold32(lds32(st).w);  // tile lookback, broadcast read
       }
@@ -340,8 +364,12 @@ __device__ __forceinline__ uint32_t fast_tile(const TextGeom& g, WarpRing* R, Pr
         const bool any = fast_chunk<M>(v, lb, lane, carryS, g.K, pred);
         if (__any_sync(kFull, any)) cand |= 1u << (s * kStageChunks + j);
       }
-      ++consumed;
-      produce(g, R, P, consumed, W, lane);  // refill the slot just read
+      // the slot's bytes are consumed: hand it back to the producer
+      S.cslot = (S.cslot + 1) & (kStages - 1);
+      S.cphase ^= (S.cslot == 0);
+      --S.pending;
+      __syncwarp();
+      stream_issue(R, S, lane);
     }
   } else {
     if constexpr (M >= 32) carryS = fold32(load_edge(g, ta - 32).w);

@@ -131,11 +131,10 @@ __global__ void __launch_bounds__(kBlock) rk_multi_kernel(const MultiArgs a) {
   const uint64_t W = (uint64_t)gridDim.x * kWarpsPerBlock;
   const uint64_t w = (uint64_t)blockIdx.x * kWarpsPerBlock + warp;
   const auto pred = [sfilter](uint32_t L) { return filter_test(sfilter, L); };
-  Producer P{w, 0u, 0u};
-  uint32_t consumed = 0;
-  produce(a.g, R, P, consumed, W, lane);
-  for (uint64_t t = w; t < a.g.num_tiles; t += W) {
-    uint32_t cand = fast_tile<M>(a.g, R, P, consumed, t, W, lane, pred);
+  Stream S;
+  stream_init(a.g, R, S, (uint32_t)w, (uint32_t)W, lane);
+  for (uint32_t t = (uint32_t)w; t < (uint32_t)a.g.num_tiles; t += (uint32_t)W) {
+    uint32_t cand = fast_tile<M>(a.g, R, S, t, lane, pred);
     const int64_t ta = a.g.tile_a(t);
     while (cand) {
       const int c = __ffs(cand) - 1;

@@ -145,11 +145,10 @@ __global__ void __launch_bounds__(kBlock) rk_scan_kernel(const ScanArgs a) {
   const uint64_t w = (uint64_t)blockIdx.x * kWarpsPerBlock + warp;
   const uint32_t T = (uint32_t)a.hx;
   const auto pred = [T](uint32_t L) { return L == T; };
-  Producer P{w, 0u, 0u};
-  uint32_t consumed = 0;
-  produce(a.g, R, P, consumed, W, lane);
-  for (uint64_t t = w; t < a.g.num_tiles; t += W) {
-    const uint32_t cand = fast_tile<M>(a.g, R, P, consumed, t, W, lane, pred);
+  Stream S;
+  stream_init(a.g, R, S, (uint32_t)w, (uint32_t)W, lane);
+  for (uint32_t t = (uint32_t)w; t < (uint32_t)a.g.num_tiles; t += (uint32_t)W) {
+    const uint32_t cand = fast_tile<M>(a.g, R, S, t, lane, pred);
     finish_tile<M>(a, t, cand, lane);
   }
 }
