@@ -36,9 +36,9 @@ constexpr int kEmitTiles = 256;              // tiles per block of the ordered e
 
 // TMA ring: kStages stages of kStageChunks chunks, each stage preceded by the 32 bytes
 // before its first chunk (the lookback the first lane needs).
-constexpr int kStageChunks = 2;
-constexpr int kStages = 4;
-constexpr int kStageBytes = kStageChunks * kChunk + 32;  // 2080 (multiple of 16)
+constexpr int kStageChunks = 4;
+constexpr int kStages = 2;
+constexpr int kStageBytes = kStageChunks * kChunk + 32;  // 4128 (multiple of 16)
 constexpr int kStagesPerTile = kTileChunks / kStageChunks;
 static_assert(kTileChunks % kStageChunks == 0, "stage/tile");
 
@@ -155,6 +155,25 @@ __device__ __forceinline__ uint32_t fold_tail(const uint32_t (&lb)[8]) {
   for (int i = first; i < ((first + 3) & ~3); ++i) s = 2u * s + bsel(lb[i >> 2], i & 3);
 #pragma unroll
   for (int wi = (first + 3) >> 2; wi < 8; ++wi) s = __dp4a(lb[wi], kFoldW, s << 4);
+  return s;
+}
+
+// fold of bytes [E-M, E) of the 64-byte array lb ++ v, exact mod 2^32 (E, M static).
+template <int M, int E>
+__device__ __forceinline__ uint32_t fold_at(const uint32_t (&lb)[8], const uint32_t (&v)[8]) {
+  static_assert(M >= 1 && M < 32 && E >= M && E <= 64, "fold_at");
+  constexpr int first = E - M;
+  constexpr int a4 = (first + 3) & ~3;  // first word-aligned byte
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = first; i < (a4 < E ? a4 : E); ++i)
+    s = 2u * s + (i < 32 ? bsel(lb[i >> 2], i & 3) : bsel(v[(i - 32) >> 2], i & 3));
+#pragma unroll
+  for (int i = a4; i + 4 <= E; i += 4)
+    s = __dp4a(i < 32 ? lb[i >> 2] : v[(i - 32) >> 2], kFoldW, s << 4);
+#pragma unroll
+  for (int i = (E & ~3) > a4 ? (E & ~3) : a4; i < E; ++i)
+    s = 2u * s + (i < 32 ? bsel(lb[i >> 2], i & 3) : bsel(v[(i - 32) >> 2], i & 3));
   return s;
 }
 
@@ -334,13 +353,14 @@ __device__ __forceinline__ void stream_init(const TextGeom& g, WarpRing* R, Stre
   for (int i = 0; i < kStages; ++i) stream_issue(R, S, lane);
 }
 
-// Fast pass over tile t: bitmask of its chunks in which some lane saw pred() hold.
-// Interior tiles come from the ring; edge tiles go through the bounds-checked loader.
-template <int M, class Pred>
-__device__ __forceinline__ uint32_t fast_tile(const TextGeom& g, WarpRing* R, Stream& S,
-                                              uint32_t t, int lane, Pred pred) {
+// Streams tile t chunk by chunk into op(v, lb, carryS, J, c): v = the lane's 32 bytes
+// (window ends [J, J+32)), lb = the 32 bytes before J (M < 32 only), carryS = the fold
+// seed for M >= 32 (see fast_chunk), c = chunk index in the tile.  Interior tiles come
+// from the TMA ring; edge tiles go through the bounds-checked loader.
+template <int M, bool UNROLL = true, class Op>
+__device__ __forceinline__ void stream_tile(const TextGeom& g, WarpRing* R, Stream& S,
+                                            uint32_t t, int lane, Op&& op) {
   const int64_t ta = g.tile_a(t);
-  uint32_t cand = 0;
   uint32_t carryS = 0;
   uint32_t lb[8];
 #pragma unroll
@@ -353,7 +373,7 @@ __device__ __forceinline__ uint32_t fast_tile(const TextGeom& g, WarpRing* R, St
       if constexpr (M >= 32) {
         if (s == 0) carryS = fold32(lds32(st).w);  // tile lookback, broadcast read
       }
-#pragma unroll
+#pragma unroll(UNROLL ? kStageChunks : 1)
       for (int j = 0; j < kStageChunks; ++j) {
         const Vec32 v = lds32(st + 32 + j * kChunk + lane * kR);
         if constexpr (M < 32) {
@@ -361,8 +381,8 @@ __device__ __forceinline__ uint32_t fast_tile(const TextGeom& g, WarpRing* R, St
 #pragma unroll
           for (int i = 0; i < 8; ++i) lb[i] = l.w[i];
         }
-        const bool any = fast_chunk<M>(v, lb, lane, carryS, g.K, pred);
-        if (__any_sync(kFull, any)) cand |= 1u << (s * kStageChunks + j);
+        const int c = s * kStageChunks + j;
+        op(v, lb, carryS, ta + c * kChunk + lane * kR, c);
       }
       // the slot's bytes are consumed: hand it back to the producer
       S.cslot = (S.cslot + 1) & (kStages - 1);
@@ -382,10 +402,21 @@ __device__ __forceinline__ uint32_t fast_tile(const TextGeom& g, WarpRing* R, St
 #pragma unroll
         for (int i = 0; i < 8; ++i) lb[i] = l.w[i];
       }
-      const bool any = fast_chunk<M>(v, lb, lane, carryS, g.K, pred);
-      if (__any_sync(kFull, any)) cand |= 1u << c;
+      op(v, lb, carryS, J, c);
     }
   }
+}
+
+// Fast pass over tile t: bitmask of its chunks in which some lane saw pred() hold.
+template <int M, bool UNROLL = true, class Pred>
+__device__ __forceinline__ uint32_t fast_tile(const TextGeom& g, WarpRing* R, Stream& S,
+                                              uint32_t t, int lane, Pred pred) {
+  uint32_t cand = 0;
+  stream_tile<M, UNROLL>(g, R, S, t, lane,
+                 [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t& carryS, int64_t, int c) {
+                   const bool any = fast_chunk<M>(v, lb, lane, carryS, g.K, pred);
+                   if (__any_sync(kFull, any)) cand |= 1u << c;
+                 });
   return cand;
 }
 

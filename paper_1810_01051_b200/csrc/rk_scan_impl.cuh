@@ -101,6 +101,111 @@ __device__ __forceinline__ SlowOut slow_chunk(const ScanArgs& a, int64_t J) {
   return r;
 }
 
+// ---------------------------------------------------------------------------------
+// Short patterns (M < 32) have frequent exact-hash hits on small alphabets (m = 4 over
+// printable ASCII: ~1.2e-3 per window, most 1 KiB chunks), so their candidates are
+// settled inside the fast pass while the bytes are still in registers: the 32 positions
+// roll in four groups of 8, each group ORs its compares into one predicate, and a lane
+// whose group fired re-rolls just those 8 positions exactly (64-bit hash for M > 24,
+// bytes against the pattern).  No chunk is re-read.
+
+// Patterns shorter than this settle candidates inline (see short_chunk).
+constexpr int kShortInline = 8;
+
+// byte i of lb ++ v (i static after unrolling)
+__device__ __forceinline__ uint32_t b64(const uint32_t (&lb)[8], const Vec32& v, int i) {
+  return i < 32 ? bsel(lb[i >> 2], i & 3) : bsel(v.w[(i - 32) >> 2], i & 3);
+}
+
+template <int M, int G>
+__device__ __forceinline__ void exact_group(const ScanArgs& a, const Vec32& v,
+                                            const uint32_t (&lb)[8], int64_t J, uint32_t L,
+                                            uint32_t& hm, uint32_t& hits) {
+  const uint32_t T = (uint32_t)a.hx;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const int k = G * 8 + kk;
+    L = 2u * L + b64(lb, v, 32 + k) - (b64(lb, v, 32 + k - M) << M);
+    if (L == T && a.g.valid_end(J + k)) {
+      bool hit = true;
+      if constexpr (M > 24) {  // low 32 bits agree; confirm the high half
+        uint64_t h = 0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) h = (h << 1) + b64(lb, v, 33 + k - M + i);
+        hit = (h == a.hx);
+      }
+      if (hit) {
+        ++hits;
+        bool eq = true;
+#pragma unroll
+        for (int i = 0; i < M; ++i) eq &= (b64(lb, v, 33 + k - M + i) == bsel(a.pw.w[i >> 2], i & 3));
+        if (eq) hm |= 1u << k;
+      }
+    }
+  }
+}
+
+// One step of the exact 32-bit roll at position k (alternating instruction mixes so the
+// ALU and FMA pipes share the work; see fast_chunk).
+template <int M>
+__device__ __forceinline__ uint32_t roll_step(uint32_t L, const uint32_t (&lb)[8], const Vec32& v,
+                                              int k, const RollConsts& K) {
+  const int io = 32 + k - M;
+  const uint32_t wout = io < 32 ? lb[io >> 2] : v.w[(io - 32) >> 2];
+  if (k & 1) {
+    L = L * K.k2 + bsel(v.w[k >> 2], k & 3);
+    return bsel(wout, io & 3) * K.negpow + L;
+  } else if constexpr (M <= 7) {
+    const uint32_t t = __dp4a(v.w[k >> 2], 1u << (8 * (k & 3)), L * K.k2);
+    return dp4a_us(wout, (uint32_t)(uint8_t)(-(1 << M)) << (8 * (io & 3)), t);
+  } else {
+    const uint32_t t = __dp4a(v.w[k >> 2], 1u << (8 * (k & 3)), L * K.k2);
+    return bsel(wout, io & 3) * K.negpow + t;
+  }
+}
+
+// The 32 positions roll in four groups of 8; each group ORs its compares into one
+// predicate, and a lane whose group fired re-rolls those 8 positions exactly.
+template <int M>
+__device__ __forceinline__ void short_chunk(const ScanArgs& a, const Vec32& v,
+                                            const uint32_t (&lb)[8], int64_t J, uint32_t& hm,
+                                            uint32_t& hits) {
+  const RollConsts& K = a.g.K;
+  const uint32_t T = (uint32_t)a.hx;
+  uint32_t L = fold_tail<M>(lb);
+#pragma unroll
+  for (int grp = 0; grp < 4; ++grp) {
+    const uint32_t L0 = L;
+    bool anyg = false;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      L = roll_step<M>(L, lb, v, grp * 8 + kk, K);
+      anyg |= (L == T);
+    }
+    if (anyg) {
+      if (grp == 0) exact_group<M, 0>(a, v, lb, J, L0, hm, hits);
+      if (grp == 1) exact_group<M, 1>(a, v, lb, J, L0, hm, hits);
+      if (grp == 2) exact_group<M, 2>(a, v, lb, J, L0, hm, hits);
+      if (grp == 3) exact_group<M, 3>(a, v, lb, J, L0, hm, hits);
+    }
+  }
+}
+
+// Records a tile's results for the ordered emission and adds the counters.
+__device__ __forceinline__ void record_tile(const ScanArgs& a, uint64_t seq, uint32_t my_matches,
+                                            uint32_t my_hits, uint32_t hitflags, int lane) {
+  const uint32_t agg = __reduce_add_sync(kFull, my_matches);
+  const uint32_t hits = __reduce_add_sync(kFull, my_hits);
+  if (lane == 0) {
+    a.tile_info[seq] = agg | (hitflags << 16);
+    if (agg) atomicAdd(&a.block_sums[seq / kEmitTiles], (unsigned long long)agg);
+    if (hits) {
+      atomicAdd(&a.counters[1], (unsigned long long)hits);
+      atomicAdd(&a.counters[2], (unsigned long long)(hits - agg));
+    }
+  }
+}
+
 // Exact pass over the candidate chunks of tile t; records the tile's match count,
 // chunk bitmap and hit masks for the ordered emission and adds the counters.
 template <int M>
@@ -122,20 +227,11 @@ __device__ __forceinline__ void finish_tile(const ScanArgs& a, uint64_t t, uint3
       hitflags |= 1u << c;
     }
   }
-  const uint32_t agg = __reduce_add_sync(kFull, my_matches);
-  const uint32_t hits = __reduce_add_sync(kFull, my_hits);
-  if (lane == 0) {
-    a.tile_info[seq] = agg | (hitflags << 16);
-    if (agg) atomicAdd(&a.block_sums[seq / kEmitTiles], (unsigned long long)agg);
-    if (hits) {
-      atomicAdd(&a.counters[1], (unsigned long long)hits);
-      atomicAdd(&a.counters[2], (unsigned long long)(hits - agg));
-    }
-  }
+  record_tile(a, seq, my_matches, my_hits, hitflags, lane);
 }
 
 template <int M>
-__global__ void __launch_bounds__(kBlock) rk_scan_kernel(const ScanArgs a) {
+__global__ void __launch_bounds__(kBlock, 3) rk_scan_kernel(const ScanArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -148,8 +244,38 @@ __global__ void __launch_bounds__(kBlock) rk_scan_kernel(const ScanArgs a) {
   Stream S;
   stream_init(a.g, R, S, (uint32_t)w, (uint32_t)W, lane);
   for (uint32_t t = (uint32_t)w; t < (uint32_t)a.g.num_tiles; t += (uint32_t)W) {
-    const uint32_t cand = fast_tile<M>(a.g, R, S, t, lane, pred);
-    finish_tile<M>(a, t, cand, lane);
+    if constexpr (M >= 32) {
+      // candidates are ~2^-32 per window: one vote per tile, and a tile with any
+      // candidate gets the exact pass over all of its chunks
+      bool any = false;
+      stream_tile<M>(a.g, R, S, t, lane,
+                     [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t& carryS, int64_t, int) {
+                       any |= fast_chunk<M>(v, lb, lane, carryS, a.g.K, pred);
+                     });
+      finish_tile<M>(a, t, __any_sync(kFull, any) ? (1u << kTileChunks) - 1 : 0u, lane);
+    } else if constexpr (M >= kShortInline) {
+      // exact hits are rare (m = 8 printable ASCII: ~2% of chunks): flag chunks, settle
+      // them in the exact pass
+      const uint32_t cand = fast_tile<M, false>(a.g, R, S, t, lane, pred);
+      finish_tile<M>(a, t, cand, lane);
+    } else {
+      const uint64_t seq = a.g.seq_base + t;
+      uint32_t* tmask = a.masks + seq * (kTileChunks * 32);
+      uint32_t hitflags = 0, my_matches = 0, my_hits = 0;
+      stream_tile<M, false>(a.g, R, S, t, lane,
+                            [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J,
+                                int c) {
+                       uint32_t hm = 0, hits = 0;
+                       short_chunk<M>(a, v, lb, J, hm, hits);
+                       my_hits += hits;
+                       my_matches += __popc(hm);
+                       if (__ballot_sync(kFull, hm != 0)) {
+                         tmask[c * 32 + lane] = hm;
+                         hitflags |= 1u << c;
+                       }
+                     });
+      record_tile(a, seq, my_matches, my_hits, hitflags, lane);
+    }
   }
 }
 
