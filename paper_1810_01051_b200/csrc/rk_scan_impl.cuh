@@ -16,20 +16,27 @@
 
 namespace rkb {
 
-// 64-bit hash of the window whose last byte is at text index je (global memory).
-static __device__ __noinline__ uint64_t hash_window_global(const uint8_t* text, uint32_t m,
-                                                          int64_t je) {
-  const int64_t span = m < 64 ? (int64_t)m : 64;
+// Warp-cooperative exact checks of one candidate window (all 32 lanes call them with the
+// same arguments): the bytes are read in parallel, lane l taking bytes l, l+32, ...,
+// instead of one lane walking up to m bytes with a dependent load per byte.
+
+// 64-bit hash of the window whose last byte is at text index je: sum over its last
+// min(m, 64) bytes of b * 2^(je - pos), mod 2^64.
+__device__ __forceinline__ uint64_t warp_hash64(const uint8_t* text, uint32_t m, int64_t je,
+                                                int lane) {
+  const int span = m < 64 ? (int)m : 64;
   uint64_t h = 0;
-  for (int64_t i = je - span + 1; i <= je; ++i) h = (h << 1) + (uint64_t)text[i];
+  for (int d = lane; d < span; d += 32) h += (uint64_t)text[je - d] << d;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(kFull, h, o);
   return h;
 }
 
-static __device__ __noinline__ bool verify_global(const uint8_t* text, const uint8_t* pattern,
-                                                  uint32_t m) {
-  for (uint32_t i = 0; i < m; ++i)
-    if (text[i] != pattern[i]) return false;
-  return true;
+__device__ __forceinline__ bool warp_equal(const uint8_t* text, const uint8_t* pattern,
+                                           uint32_t m, int lane) {
+  bool eq = true;
+  for (uint32_t i = lane; i < m; i += 32) eq &= (text[i] == pattern[i]);
+  return __all_sync(kFull, eq);
 }
 
 struct SlowOut {
@@ -47,16 +54,24 @@ __device__ __forceinline__ SlowOut slow_chunk(const ScanArgs& a, int64_t J) {
   const Vec32 lbv = load_edge(g, J - 32);
   const uint32_t T = (uint32_t)a.hx;
   if constexpr (M >= 32) {
+    // one candidate at a time, checked by the whole warp
+    const uint8_t* text = g.abase + g.amis;
+    const int lane = threadIdx.x & 31;
     uint32_t S = fold32(lbv.w);
 #pragma unroll 4
     for (int k = 0; k < 32; ++k) {
       S = 2u * S + bsel(v.w[k >> 2], k & 3);
-      if (S == T && g.valid_end(J + k)) {
-        const int64_t je = J + k - (int64_t)g.amis;  // text index of the last byte
-        const uint8_t* text = g.abase + g.amis;
-        if (hash_window_global(text, g.m, je) == a.hx) {
-          ++r.hits;
-          if (verify_global(text + je - (int64_t)g.m + 1, a.pattern, g.m)) r.hm |= 1u << k;
+      unsigned todo = __ballot_sync(kFull, S == T && g.valid_end(J + k));
+      while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int64_t je = __shfl_sync(kFull, J, src) + k - (int64_t)g.amis;  // last byte
+        if (warp_hash64(text, g.m, je, lane) == a.hx) {
+          const bool eq = warp_equal(text + je - (int64_t)g.m + 1, a.pattern, g.m, lane);
+          if (lane == src) {
+            ++r.hits;
+            if (eq) r.hm |= 1u << k;
+          }
         }
       }
     }
