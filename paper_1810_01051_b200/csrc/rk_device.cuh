@@ -33,6 +33,7 @@ constexpr int kWarpsPerBlock = 8;
 constexpr int kBlock = 32 * kWarpsPerBlock;
 constexpr uint32_t kFoldW = 0x01020408u;     // dp4a weights: 8*b0 + 4*b1 + 2*b2 + b3
 constexpr int kEmitTiles = 256;              // tiles per block of the ordered emission
+constexpr int kMaxDevices = 64;
 
 // TMA ring: kStages stages of kStageChunks chunks, each stage preceded by the 32 bytes
 // before its first chunk (the lookback the first lane needs).

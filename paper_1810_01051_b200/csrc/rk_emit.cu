@@ -1,22 +1,38 @@
 // rk_emit.cu -- ordered emission of match offsets (the ordered concatenation of
 // /root/reference/pkg/src/rkmatch/parallel.py:168-172, done on the device).
 //
-// The scan kernel never waits on other tiles: it leaves, per 16 KiB tile, its match
+// The scan kernel never waits on other tiles: it leaves, per 8 KiB tile, its match
 // count and chunk bitmap (tile_info), the per-lane hit masks of the chunks that matched
 // (masks), and per-256-tile sums (block_sums).  This kernel turns that into the ordered
 // int64 offsets: block b adds up block_sums[0..b), scans its 256 tile counts, and each
-// warp expands the masks of its tiles that have matches into window starts written at
-// their final positions -- ascending, deterministic, no sort.  Text bytes are not
-// touched again, so for sparse matches this is a few microseconds.
+// warp expands the masks of its tiles with matches into window starts written at their
+// final positions -- ascending, deterministic, no sort, no text re-read.  For sparse
+// matches this is a few microseconds per GiB.
+//
+// Dense outputs (every window matching, BASELINE config C5) are write-bound: a chunk's
+// offsets are staged in shared memory (padded so the lane-strided fill is nearly
+// conflict-free) and written back as contiguous, coalesced 16-byte stores; a chunk whose
+// 1024 windows all match is written directly as an arithmetic run.
 #include "rk_device.cuh"
 #include "rk_internal.h"
 
 namespace rkb {
 
+constexpr int kEmitWarps = kEmitTiles / 32;
+constexpr int kPadded = kChunk + kChunk / 32;  // 1056 slots: +1 per 32
+
+__device__ __forceinline__ int padded(int i) { return i + (i >> 5); }
+
+__device__ __forceinline__ void st_global_v2(int64_t* p, int64_t a, int64_t b) {
+  asm volatile("st.global.v2.s64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
 __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
-  __shared__ unsigned long long red[kEmitTiles / 32];
-  __shared__ uint32_t wsum[kEmitTiles / 32];
+  extern __shared__ __align__(16) int64_t stage_all[];
+  __shared__ unsigned long long red[kEmitWarps];
+  __shared__ uint32_t wsum[kEmitWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int64_t* stage = stage_all + warp * kPadded;
   const uint64_t b = blockIdx.x;
 
   unsigned long long pre = 0;
@@ -34,7 +50,7 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
   unsigned long long base = 0;
   uint32_t wpre = 0;
 #pragma unroll
-  for (int w = 0; w < kEmitTiles / 32; ++w) {
+  for (int w = 0; w < kEmitWarps; ++w) {
     base += red[w];
     if (w < warp) wpre += wsum[w];
   }
@@ -54,25 +70,57 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
       const int c = __ffs(flags) - 1;
       flags &= flags - 1;
       uint32_t hm = tm[c * 32 + lane];
+      const int64_t chunk0 = tile_a + c * kChunk + e.start_bias;  // value of window 0
+      if (__all_sync(kFull, hm == 0xffffffffu)) {
+        // all 1024 windows match: a contiguous arithmetic run
+        const uint64_t lim = e.cap > run ? e.cap - run : 0;
+        if (run + kChunk <= e.cap && (run & 1) == 0) {
+          int64_t* o = e.out + run;
+#pragma unroll 4
+          for (int i = 2 * lane; i < kChunk; i += 64) st_global_v2(o + i, chunk0 + i, chunk0 + i + 1);
+        } else {
+          for (int i = lane; i < kChunk; i += 32)
+            if ((uint64_t)i < lim) e.out[run + i] = chunk0 + i;
+        }
+        run += kChunk;
+        continue;
+      }
       const uint32_t n = __popc(hm);
       const uint32_t i2 = warp_incl_scan(n, lane);
       const uint32_t tot = __shfl_sync(kFull, i2, 31);
-      uint64_t pos = run + i2 - n;
-      const int64_t v0 = tile_a + c * kChunk + lane * kR + e.start_bias;
+      // stage this chunk's offsets in order, then write them back coalesced
+      int r = (int)(i2 - n);
+      const int64_t v0 = chunk0 + lane * kR;
       while (hm) {
         const int k = __ffs(hm) - 1;
         hm &= hm - 1;
-        if (pos < e.cap) e.out[pos] = v0 + k;
-        ++pos;
+        stage[padded(r++)] = v0 + k;
       }
+      __syncwarp();
+      const uint64_t lim = e.cap > run ? e.cap - run : 0;
+      for (int i = lane; i < (int)tot; i += 32)
+        if ((uint64_t)i < lim) e.out[run + i] = stage[padded(i)];
+      __syncwarp();
       run += tot;
     }
   }
 }
 
+size_t emit_smem_bytes() { return (size_t)kEmitWarps * kPadded * sizeof(int64_t); }
+
 cudaError_t launch_emit(const EmitArgs& e, cudaStream_t s) {
   const uint64_t blocks = (e.num_tiles + kEmitTiles - 1) / kEmitTiles;
-  rk_emit_kernel<<<(unsigned)blocks, kEmitTiles, 0, s>>>(e);
+  static bool attr[kMaxDevices] = {};  // the smem opt-in is per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= kMaxDevices || !attr[dev]) {
+    cudaError_t err = cudaFuncSetAttribute(rk_emit_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)emit_smem_bytes());
+    if (err != cudaSuccess) return err;
+    if (dev < kMaxDevices) attr[dev] = true;
+  }
+  rk_emit_kernel<<<(unsigned)blocks, kEmitTiles, emit_smem_bytes(), s>>>(e);
   return cudaGetLastError();
 }
 

@@ -25,7 +25,7 @@ static int variant_of(uint32_t m) { return m >= 32 ? 31 : (int)m - 1; }
 size_t scan_smem_bytes() { return sizeof(WarpRing) * kWarpsPerBlock; }
 
 int scan_blocks_per_sm(uint32_t m) {
-  static int cache[32] = {0};
+  static int cache[32] = {0};  // same on every B200
   const int v = variant_of(m);
   if (!cache[v]) cache[v] = ScanTable::occ[v]();
   return cache[v];

@@ -132,6 +132,38 @@ __device__ __forceinline__ uint32_t b64(const uint32_t (&lb)[8], const Vec32& v,
   return i < 32 ? bsel(lb[i >> 2], i & 3) : bsel(v.w[(i - 32) >> 2], i & 3);
 }
 
+// word (4 bytes) of lb ++ v starting at byte p (static after unrolling; p + 4 <= 64)
+__device__ __forceinline__ uint32_t w64(const uint32_t (&lb)[8], const Vec32& v, int p) {
+  const int q = p >> 2, r = p & 3;
+  const uint32_t lo = q < 8 ? lb[q] : v.w[q - 8];
+  if (r == 0) return lo;
+  const uint32_t hi = (q + 1) < 8 ? lb[q + 1] : ((q + 1) < 16 ? v.w[q + 1 - 8] : 0u);
+  return __funnelshift_r(lo, hi, 8 * r);
+}
+
+// bytes [s, s+M) of lb ++ v equal the pattern (word compares via funnel shifts)
+template <int M>
+__device__ __forceinline__ bool window_eq(const uint32_t (&lb)[8], const Vec32& v, int s,
+                                          const PatWords& pw) {
+  bool eq = true;
+#pragma unroll
+  for (int q = 0; q < (M + 3) / 4; ++q) {
+    const int rem = M - 4 * q;
+    const uint32_t mask = rem >= 4 ? 0xffffffffu : ((1u << (8 * rem)) - 1u);
+    uint32_t w;
+    if (s + 4 * q + 4 <= 64) {
+      w = w64(lb, v, s + 4 * q);
+    } else {  // last partial word at the end of the array
+      w = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (s + 4 * q + b < 64) w |= b64(lb, v, s + 4 * q + b) << (8 * b);
+    }
+    eq &= ((w ^ pw.w[q]) & mask) == 0u;
+  }
+  return eq;
+}
+
 template <int M, int G>
 __device__ __forceinline__ void exact_group(const ScanArgs& a, const Vec32& v,
                                             const uint32_t (&lb)[8], int64_t J, uint32_t L,
@@ -151,10 +183,7 @@ __device__ __forceinline__ void exact_group(const ScanArgs& a, const Vec32& v,
       }
       if (hit) {
         ++hits;
-        bool eq = true;
-#pragma unroll
-        for (int i = 0; i < M; ++i) eq &= (b64(lb, v, 33 + k - M + i) == bsel(a.pw.w[i >> 2], i & 3));
-        if (eq) hm |= 1u << k;
+        if (window_eq<M>(lb, v, 33 + k - M, a.pw)) hm |= 1u << k;
       }
     }
   }
@@ -297,12 +326,14 @@ __global__ void __launch_bounds__(kBlock, 3) rk_scan_kernel(const ScanArgs a) {
 template <int M>
 cudaError_t launch_m(const ScanArgs& a, int grid, cudaStream_t s) {
   const size_t smem = scan_smem_bytes();
-  static bool attr = false;  // per-variant one-time opt-in to > 48 KiB dynamic smem
-  if (!attr) {
+  static bool attr[kMaxDevices] = {};  // per-variant, per-device opt-in to > 48 KiB smem
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= kMaxDevices || !attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(rk_scan_kernel<M>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    if (dev < kMaxDevices) attr[dev] = true;
   }
   rk_scan_kernel<M><<<grid, kBlock, smem, s>>>(a);
   return cudaGetLastError();
