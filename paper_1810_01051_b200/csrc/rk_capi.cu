@@ -92,6 +92,7 @@ struct rk_ctx {
   uint64_t* d_mphash = nullptr;
   uint32_t* d_morder = nullptr;
   uint32_t* d_mfilter = nullptr;
+  uint32_t* d_qfilter = nullptr;
   uint2* d_mtable = nullptr;
   uint64_t mslots_cap = 0;
   std::mutex mu;
@@ -350,6 +351,7 @@ int rk_ctx_destroy(rk_ctx_t* c) {
   cudaFree(c->d_mphash);
   cudaFree(c->d_morder);
   cudaFree(c->d_mfilter);
+  cudaFree(c->d_qfilter);
   cudaFree(c->d_mtable);
   delete c;
   return RK_OK;
@@ -593,6 +595,28 @@ int rk_multi_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
     c->mslots_cap = pcap;
   }
   if (!c->d_mfilter) RK_CUDA(cudaMalloc(&c->d_mfilter, kMultiFilterWords * sizeof(uint32_t)));
+  if (!c->d_qfilter) RK_CUDA(cudaMalloc(&c->d_qfilter, kQFilterWords * sizeof(uint32_t)));
+  // q-gram sampling filter (see rk_multi_impl.cuh): step s, q-gram length q <= m - s + 1
+  const uint32_t qmode = m >= 16 ? 8u : (m >= 7 ? 4u : 0u);
+  std::vector<uint32_t> qfilter;
+  if (qmode) {
+    qfilter.assign(kQFilterWords, 0u);
+    for (uint32_t i = 0; i < P; ++i) {
+      const uint8_t* p = h_patterns + (uint64_t)i * m;
+      for (uint32_t j = 0; j < qmode; ++j) {
+        uint32_t w0 = 0, w1 = 0;
+        memcpy(&w0, p + j, 4);
+        if (qmode == 8) memcpy(&w1, p + j + 4, 4);
+        else w1 = kQ4Salt;
+        uint32_t i1, i2;
+        qgram_bits(w0, w1, i1, i2);
+        qfilter[i1 >> 5] |= 1u << (i1 & 31);
+        qfilter[i2 >> 5] |= 1u << (i2 & 31);
+      }
+    }
+    RK_CUDA(cudaMemcpyAsync(c->d_qfilter, qfilter.data(), kQFilterWords * sizeof(uint32_t),
+                            cudaMemcpyHostToDevice, s));
+  }
   RK_CUDA(cudaMemcpyAsync(c->d_mpats, h_patterns, (uint64_t)P * m, cudaMemcpyHostToDevice, s));
   RK_CUDA(cudaMemcpyAsync(c->d_mphash, h_hashes, P * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   RK_CUDA(cudaMemcpyAsync(c->d_morder, order.data(), P * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
@@ -602,9 +626,20 @@ int rk_multi_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
   RK_CUDA(cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), s));
 
   const uint64_t nw = n - m + 1;
-  const Geometry gg = geometry(d_text, m, 0, nw);
+  Geometry gg = geometry(d_text, m, 0, nw);
   MultiArgs p{};
+  p.ys_lo = gg.amis;
+  p.ys_hi = gg.amis + nw;
+  if (qmode) {
+    // tiles over aligned q-gram positions x in [first window start, last start + s)
+    gg.ja_lo = gg.amis;
+    gg.ja_hi = std::min<uint64_t>(gg.amis + nw - 1 + qmode, gg.amis + n);
+    gg.tile_first = gg.ja_lo / kTile;
+    gg.num_tiles = (gg.ja_hi - 1) / kTile - gg.tile_first + 1;
+  }
   p.g = text_geom(gg, n, m, 0);
+  p.qfilter = c->d_qfilter;
+  p.qmode = qmode;
   p.pats = c->d_mpats;
   p.phash = c->d_mphash;
   p.filter = c->d_mfilter;
@@ -616,7 +651,10 @@ int rk_multi_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
   p.counters = c->d_counters;
   p.P = P;
   p.tsize = tsize;
-  RK_CUDA(launch_multi(p, grid_for(gg.num_tiles, c->num_sms, multi_blocks_per_sm(m, tsize)), s));
+  const uint64_t mgrid = std::max<uint64_t>(
+      1, std::min<uint64_t>((uint64_t)c->num_sms * multi_blocks_per_sm(m, tsize),
+                            (gg.num_tiles + 15) / 16));
+  RK_CUDA(launch_multi(p, (int)mgrid, s));
   ++c->launches;
   RK_CUDA(cudaMemcpyAsync(c->h_counters, c->d_counters, sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, s));

@@ -38,9 +38,29 @@ cudaError_t launch_emit(const EmitArgs& e, cudaStream_t s);
 
 // multi pattern (rk_multi.cu, kernels in rk_multi_impl.cuh)
 constexpr int kMultiFilterWords = (1 << 16) / 32;
+constexpr int kQFilterWords = (1 << 19) / 32;  // q-gram Bloom filter, 64 KiB
 constexpr uint32_t kMultiEmpty = 0xffffffffu;
+constexpr uint32_t kQ4Salt = 0x5bd1e995u;      // second word of a 4-byte q-gram
+
+// The two Bloom-filter bit indices (19 bits each) of an 8-byte q-gram (w0, w1) -- the
+// same function on the host (filter build) and the device (text q-grams).
+__host__ __device__ __forceinline__ void qgram_bits(uint32_t w0, uint32_t w1, uint32_t& i1,
+                                                    uint32_t& i2) {
+  uint32_t h = w0 * 0x9E3779B1u;
+  h ^= h >> 15;
+  h ^= w1 * 0x85EBCA77u;
+  h ^= h >> 13;
+  h *= 0xC2B2AE3Du;
+  h ^= h >> 16;
+  i1 = h >> 13;
+  i2 = (h * 0x27D4EB2Fu) >> 13;
+}
+
 struct MultiArgs {
-  TextGeom g;
+  TextGeom g;                 // q-gram mode: tiles cover aligned q-gram positions
+  const uint32_t* qfilter;    // kQFilterWords words (q-gram mode)
+  uint32_t qmode;             // sampling step s (8 or 4), 0 = per-window filter
+  uint64_t ys_lo, ys_hi;      // valid window starts, a-space
   const uint8_t* pats;        // P * m bytes, deduplicated, index order
   const uint64_t* phash;      // 64-bit hash per pattern
   const uint32_t* filter;     // kMultiFilterWords words

@@ -22,9 +22,8 @@ using MTable = MultiTable<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16,
 
 static int mvariant(uint32_t m) { return m >= 32 ? 31 : (int)m - 1; }
 
-size_t multi_smem_bytes(uint32_t tsize) {
-  return sizeof(WarpRing) * kWarpsPerBlock + kMultiFilterWords * sizeof(uint32_t) +
-         (size_t)tsize * sizeof(uint2);
+size_t multi_smem_bytes(uint32_t) {
+  return sizeof(WarpRing) * 16 + kQFilterWords * sizeof(uint32_t);
 }
 
 int multi_blocks_per_sm(uint32_t m, uint32_t tsize) { return MTable::occ[mvariant(m)](tsize); }

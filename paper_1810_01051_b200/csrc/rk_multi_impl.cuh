@@ -2,14 +2,24 @@
 // (/root/reference/pkg/src/rkmatch/matcher.py:139-153: per length, hash every window,
 // look the hash up in the set's hash index, byte-verify every pattern carrying it).
 //
-// Same streaming engine as the single-pattern scan (TMA ring, exact 32-bit roll); the
-// reference's O(P) compare per window becomes shared-memory lookups:
-//   * a 2^16-bit filter (8 KiB smem) keyed by a multiplicative hash of low32(window hash)
-//     rejects ~98% of windows at P = 1024 with one LDS;
-//   * survivors probe an open-addressing table (smem) of the distinct low32 keys, whose
-//     entries point at the run of patterns sharing that key (several patterns may share
-//     a hash, e.g. "ac"/"ba", tests/test_matcher.py:139-146);
-//   * each such pattern is confirmed by its 64-bit hash (m > 24) and by its bytes.
+// The exact test is the reference's: a window matches pattern i iff its Rabin hash
+// equals hash_full(pattern i) and its bytes equal the pattern.  Hashes are looked up in a
+// table of the distinct low-32 keys whose entries point at the run of patterns sharing the
+// key (several patterns may share a hash, e.g. "ac"/"ba", tests/test_matcher.py:139-146);
+// the 64-bit hash (m > 24) and the bytes confirm.
+//
+// Which windows get that test is decided by a filter that never rejects a match:
+//   * q-gram sampling (m >= 7): every occurrence of a pattern p at y covers the aligned
+//     position x = y rounded up to a multiple of s, and the q bytes at x are p[j:j+q] with
+//     j = x - y < s, j + q <= m.  All P*s such q-grams go into a 2^19-bit, 2-probe Bloom
+//     filter in shared memory; the fast pass tests only the aligned q-grams of the text
+//     (one test per s bytes, straight from the 8-byte-aligned words, no rolling hash).  A
+//     q-gram that hits makes the s windows whose aligned position it is candidates; s
+//     lanes of the warp check them at once (exact hash + table + bytes).  Each window has
+//     exactly one aligned position, so nothing is reported twice.
+//     (s, q) = (8, 8) for m >= 16, (4, 4) for 7 <= m < 16.
+//   * m < 7: every window's exact 32-bit rolling hash is tested against a 2^16-bit
+//     filter of the pattern hashes.
 // Hits are appended with warp ballot/popc and one atomic per warp; the host orders them
 // by (pattern index, offset), which is exactly the reference's per-pattern ascending lists.
 #pragma once
@@ -18,11 +28,21 @@
 
 namespace rkb {
 
+constexpr int kMultiWarps = 16;  // one 16-warp CTA per SM shares the 64 KiB q-gram filter
+constexpr int kMultiBlock = 32 * kMultiWarps;
+
 __device__ __forceinline__ uint32_t mhash(uint32_t key) { return key * 0x9E3779B1u; }
 
 __device__ __forceinline__ bool filter_test(const uint32_t* __restrict__ f, uint32_t L) {
   const uint32_t b = mhash(L) >> 16;
   return (f[b >> 5] >> (b & 31)) & 1u;
+}
+
+__device__ __forceinline__ bool qfilter_test(const uint32_t* __restrict__ f, uint32_t w0,
+                                             uint32_t w1) {
+  uint32_t i1, i2;
+  qgram_bits(w0, w1, i1, i2);
+  return ((f[i1 >> 5] >> (i1 & 31)) & (f[i2 >> 5] >> (i2 & 31)) & 1u) != 0u;
 }
 
 static __device__ __noinline__ uint64_t multi_hash_global(const uint8_t* text, uint32_t m,
@@ -72,9 +92,12 @@ static __device__ __noinline__ int multi_resolve(const uint8_t* text, const uint
   }
 }
 
+// Exact pass over the 32 windows ending at [J, J+32) of this lane (a-space).  With
+// q-gram sampling on (s > 0) a window is taken only if its aligned position
+// x = roundup(start, s) lies in [X0, X0 + kChunk).
 template <int M>
-__device__ __forceinline__ void multi_slow_chunk(const MultiArgs& a, const uint2* tbl,
-                                                 const uint32_t* f, int64_t J, int lane) {
+__device__ __forceinline__ void multi_exact(const MultiArgs& a, int64_t J, int lane, int s,
+                                            int64_t X0) {
   const TextGeom& g = a.g;
   const Vec32 v = load_edge(g, J);
   const Vec32 lbv = load_edge(g, J - 32);
@@ -93,10 +116,16 @@ __device__ __forceinline__ void multi_slow_chunk(const MultiArgs& a, const uint2
           io < 32 ? bsel(lbv.w[io >> 2], io & 3) : bsel(v.w[(io - 32) >> 2], io & 3);
       L = 2u * L + in - (out << M);
     }
-    const int64_t ja = J + k;
+    const int64_t ja = J + k;                  // window end (a-space)
+    const int64_t ya = ja - (int64_t)g.m + 1;  // window start (a-space)
+    bool take = ya >= (int64_t)a.ys_lo && ya < (int64_t)a.ys_hi;
+    if (s > 0) {  // s is a power of two
+      const int64_t xa = (ya + s - 1) & ~(int64_t)(s - 1);
+      take = take && xa >= X0 && xa < X0 + kChunk;
+    }
     int idx = -1;
-    if (g.valid_end(ja) && filter_test(f, L))
-      idx = multi_resolve(text, a.pats, a.phash, a.order, tbl, a.tsize, g.m, L,
+    if (take && filter_test(a.filter, L))
+      idx = multi_resolve(text, a.pats, a.phash, a.order, a.table, a.tsize, g.m, L,
                           ja - (int64_t)g.amis);
     const unsigned hit = __ballot_sync(kFull, idx >= 0);
     if (hit) {
@@ -106,7 +135,7 @@ __device__ __forceinline__ void multi_slow_chunk(const MultiArgs& a, const uint2
       if (idx >= 0) {
         const uint64_t pos = base + __popc(hit & ((1u << lane) - 1u));
         if (pos < a.cap) {
-          a.out_off[pos] = ja - (int64_t)g.amis - (int64_t)g.m + 1;
+          a.out_off[pos] = ya - (int64_t)g.amis;
           a.out_idx[pos] = (uint32_t)idx;
         }
       }
@@ -114,32 +143,96 @@ __device__ __forceinline__ void multi_slow_chunk(const MultiArgs& a, const uint2
   }
 }
 
+// Exact check of the window starting at a-position ya (lanes with active == false only
+// take part in the warp collectives).  Appends (offset, pattern) on a match.
+__device__ __forceinline__ void multi_check_window(const MultiArgs& a, int64_t ya, bool active,
+                                                   int lane) {
+  const TextGeom& g = a.g;
+  int idx = -1;
+  if (active && ya >= (int64_t)a.ys_lo && ya < (int64_t)a.ys_hi) {
+    const uint8_t* text = g.abase + g.amis;
+    const int64_t y = ya - (int64_t)g.amis;     // text index of the first byte
+    const int64_t je = y + (int64_t)g.m - 1;    // ... and of the last
+    const uint32_t span = g.m < 32 ? g.m : 32;  // low 32 bits of the hash: last <= 32 bytes
+    uint32_t L = 0;
+    for (uint32_t i = 0; i < span; ++i) L = 2u * L + text[je - span + 1 + i];
+    if (filter_test(a.filter, L))
+      idx = multi_resolve(text, a.pats, a.phash, a.order, a.table, a.tsize, g.m, L, je);
+  }
+  const unsigned hit = __ballot_sync(kFull, idx >= 0);
+  if (hit) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&a.counters[0], (unsigned long long)__popc(hit));
+    base = __shfl_sync(kFull, base, 0);
+    if (idx >= 0) {
+      const uint64_t pos = base + __popc(hit & ((1u << lane) - 1u));
+      if (pos < a.cap) {
+        a.out_off[pos] = ya - (int64_t)g.amis;
+        a.out_idx[pos] = (uint32_t)idx;
+      }
+    }
+  }
+}
+
 template <int M>
-__global__ void __launch_bounds__(kBlock) rk_multi_kernel(const MultiArgs a) {
+__global__ void __launch_bounds__(kMultiBlock) rk_multi_kernel(const MultiArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   WarpRing* rings = reinterpret_cast<WarpRing*>(smem);
-  uint32_t* sfilter = reinterpret_cast<uint32_t*>(smem + sizeof(WarpRing) * kWarpsPerBlock);
-  uint2* stable = reinterpret_cast<uint2*>(sfilter + kMultiFilterWords);
-  for (int i = threadIdx.x; i < kMultiFilterWords; i += blockDim.x) sfilter[i] = a.filter[i];
-  for (uint32_t i = threadIdx.x; i < a.tsize; i += blockDim.x) stable[i] = a.table[i];
+  uint32_t* sfilter = reinterpret_cast<uint32_t*>(smem + sizeof(WarpRing) * kMultiWarps);
+  const int nwords = a.qmode ? kQFilterWords : kMultiFilterWords;
+  const uint32_t* gsrc = a.qmode ? a.qfilter : a.filter;
+  for (int i = threadIdx.x; i < nwords; i += blockDim.x) sfilter[i] = gsrc[i];
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   WarpRing* R = rings + warp;
   ring_init(R, lane);
-  const uint64_t W = (uint64_t)gridDim.x * kWarpsPerBlock;
-  const uint64_t w = (uint64_t)blockIdx.x * kWarpsPerBlock + warp;
-  const auto pred = [sfilter](uint32_t L) { return filter_test(sfilter, L); };
+  const uint64_t W = (uint64_t)gridDim.x * kMultiWarps;
+  const uint64_t w = (uint64_t)blockIdx.x * kMultiWarps + warp;
   Stream S;
   stream_init(a.g, R, S, (uint32_t)w, (uint32_t)W, lane);
+  const int s = (int)a.qmode;
   for (uint32_t t = (uint32_t)w; t < (uint32_t)a.g.num_tiles; t += (uint32_t)W) {
-    uint32_t cand = fast_tile<M>(a.g, R, S, t, lane, pred);
     const int64_t ta = a.g.tile_a(t);
-    while (cand) {
-      const int c = __ffs(cand) - 1;
-      cand &= cand - 1;
-      multi_slow_chunk<M>(a, stable, sfilter, ta + c * kChunk + lane * kR, lane);
+    if (s == 0) {
+      const auto pred = [sfilter](uint32_t L) { return filter_test(sfilter, L); };
+      uint32_t cand = fast_tile<M, false>(a.g, R, S, t, lane, pred);
+      while (cand) {
+        const int c = __ffs(cand) - 1;
+        cand &= cand - 1;
+        multi_exact<M>(a, ta + c * kChunk + lane * kR, lane, 0, 0);
+      }
+    } else {
+      // aligned q-grams of the lane's 32 bytes (positions x = J + s*q, J 32-aligned); a
+      // q-gram that passes the Bloom filter makes windows x-s+1 .. x candidates, checked
+      // right away by s lanes of the warp together
+      stream_tile<32, false>(
+          a.g, R, S, t, lane,
+          [&](const Vec32& v, const uint32_t (&)[8], uint32_t&, int64_t J, int) {
+            uint32_t qm = 0;
+            if (s == 8) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                qm |= (uint32_t)qfilter_test(sfilter, v.w[2 * q], v.w[2 * q + 1]) << q;
+            } else {
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                qm |= (uint32_t)qfilter_test(sfilter, v.w[q], kQ4Salt) << q;
+            }
+            unsigned lanes = __ballot_sync(kFull, qm != 0);
+            while (lanes) {
+              const int src = __ffs(lanes) - 1;
+              lanes &= lanes - 1;
+              uint32_t ms = __shfl_sync(kFull, qm, src);
+              const int64_t Js = __shfl_sync(kFull, J, src);
+              while (ms) {
+                const int q = __ffs(ms) - 1;
+                ms &= ms - 1;
+                multi_check_window(a, Js + (int64_t)q * s - lane, lane < s, lane);
+              }
+            }
+          });
     }
   }
 }
@@ -150,7 +243,7 @@ cudaError_t launch_multi_m(const MultiArgs& a, int grid, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(rk_multi_kernel<M>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  rk_multi_kernel<M><<<grid, kBlock, smem, s>>>(a);
+  rk_multi_kernel<M><<<grid, kMultiBlock, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -159,7 +252,7 @@ int multi_occupancy_m(uint32_t tsize) {
   const size_t smem = multi_smem_bytes(tsize);
   cudaFuncSetAttribute(rk_multi_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rk_multi_kernel<M>, kBlock, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rk_multi_kernel<M>, kMultiBlock, smem);
   return b > 0 ? b : 1;
 }
 

@@ -270,3 +270,39 @@ def test_pinned_host_tensor_input(gpu):
     r = rk.search_sequential(host, pat)
     eo, _ = oracle.c_scan(host.numpy(), np.frombuffer(pat, dtype=np.uint8), workers=4)
     assert r.offsets == eo.tolist()
+
+
+def test_multi_qgram_modes_edges(gpu):
+    """q-gram sampled filter (m >= 7): occurrences at both text ends, at every alignment,
+    device views at odd offsets, many patterns sharing q-grams."""
+    torch = _torch()
+    rng = np.random.default_rng(77)
+    for m in (7, 8, 11, 15, 16, 17, 24, 33, 64, 100):
+        n = 50000
+        base = rng.integers(0, 4, n + 40, dtype=np.uint8)
+        for shift in (0, 1, 5, 13):
+            host = base[shift : shift + n].copy()
+            pats = []
+            for x in (0, 1, 2, 3, 7, 8, 9, 4095, 4096, 8191, 8192, n // 2 + 3, n - m - 1, n - m):
+                pats.append(host[x : x + m].tobytes())
+            for _ in range(40):
+                pats.append(rng.integers(0, 4, m, dtype=np.uint8).tobytes())
+            dev = torch.from_numpy(base).cuda()[shift : shift + n]
+            out = rk.search_multi(dev, pats)
+            ps, by_len, _ = oracle.pattern_set(pats)
+            expect = {j: offs.tolist() for j, offs in oracle.c_search_multi_group(host, ps)}
+            for i, r in out:
+                assert r.offsets == expect[i], (m, shift, i)
+
+
+def test_multi_4096_patterns(gpu):
+    rng = np.random.default_rng(78)
+    text = rng.integers(0, 256, 1 << 20, dtype=np.uint8)
+    pats = [text[x : x + 16].tobytes() for x in rng.integers(0, (1 << 20) - 16, 3000)]
+    pats += [rng.integers(0, 256, 16, dtype=np.uint8).tobytes() for _ in range(1096)]
+    out = rk.search_multi(text.tobytes(), pats)
+    ps, _, _ = oracle.pattern_set(pats)
+    expect = {j: offs.tolist() for j, offs in oracle.c_search_multi_group(text, ps)}
+    assert len(out) == len(ps)
+    for i, r in out:
+        assert r.offsets == expect[i]
