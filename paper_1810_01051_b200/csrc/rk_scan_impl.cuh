@@ -125,7 +125,7 @@ __device__ __forceinline__ SlowOut slow_chunk(const ScanArgs& a, int64_t J) {
 // bytes against the pattern).  No chunk is re-read.
 
 // Patterns shorter than this settle candidates inline (see short_chunk).
-constexpr int kShortInline = 8;
+constexpr int kShortInline = 9;
 
 // byte i of lb ++ v (i static after unrolling)
 __device__ __forceinline__ uint32_t b64(const uint32_t (&lb)[8], const Vec32& v, int i) {
@@ -164,11 +164,39 @@ __device__ __forceinline__ bool window_eq(const uint32_t (&lb)[8], const Vec32& 
   return eq;
 }
 
+// dp4a weights of window bytes [4q, 4q+4) in the hash of an M-byte window (M <= 8):
+// byte i carries 2^(M-1-i).
+template <int M>
+__host__ __device__ constexpr uint32_t win_weights(int q) {
+  uint32_t w = 0;
+  for (int b = 0; b < 4; ++b) {
+    const int i = 4 * q + b;
+    if (i < M) w |= (uint32_t)(1u << (M - 1 - i)) << (8 * b);
+  }
+  return w;
+}
+
 template <int M, int G>
 __device__ __forceinline__ void exact_group(const ScanArgs& a, const Vec32& v,
                                             const uint32_t (&lb)[8], int64_t J, uint32_t L,
                                             uint32_t& hm, uint32_t& hits) {
   const uint32_t T = (uint32_t)a.hx;
+  if constexpr (M <= 8) {
+    // the whole hash is a dot product of the window's (at most two) words: no re-roll
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int k = G * 8 + kk;
+      const int s0 = 33 + k - M;  // first byte of the window in lb ++ v
+      uint32_t h = __dp4a(w64(lb, v, s0), win_weights<M>(0), 0u);
+      if constexpr (M > 4) h = __dp4a(w64(lb, v, s0 + 4), win_weights<M>(1), h);
+      if (h == T && a.g.valid_end(J + k)) {
+        ++hits;
+        if (window_eq<M>(lb, v, s0, a.pw)) hm |= 1u << k;
+      }
+    }
+    (void)L;
+    return;
+  }
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     const int k = G * 8 + kk;
@@ -208,29 +236,54 @@ __device__ __forceinline__ uint32_t roll_step(uint32_t L, const uint32_t (&lb)[8
   }
 }
 
-// The 32 positions roll in four groups of 8; each group ORs its compares into one
-// predicate, and a lane whose group fired re-rolls those 8 positions exactly.
+// The 32 positions are checked in four groups of 8; each group ORs its compares into
+// one predicate, and a lane whose group fired settles those 8 positions exactly.
+//  M <= 8: the whole hash is a dot product of the window's (at most two) words with the
+//    weights 2^(M-1-i): per window one funnel shift (shared between neighbours), one or
+//    two dp4a, one compare -- no serial roll chain at all.
+//  M > 8: the exact 32-bit roll.
 template <int M>
 __device__ __forceinline__ void short_chunk(const ScanArgs& a, const Vec32& v,
                                             const uint32_t (&lb)[8], int64_t J, uint32_t& hm,
                                             uint32_t& hits) {
-  const RollConsts& K = a.g.K;
   const uint32_t T = (uint32_t)a.hx;
-  uint32_t L = fold_tail<M>(lb);
+  if constexpr (M <= 8) {
+    constexpr uint32_t W0 = win_weights<M>(0), W1 = win_weights<M>(1);
 #pragma unroll
-  for (int grp = 0; grp < 4; ++grp) {
-    const uint32_t L0 = L;
-    bool anyg = false;
+    for (int grp = 0; grp < 4; ++grp) {
+      bool anyg = false;
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      L = roll_step<M>(L, lb, v, grp * 8 + kk, K);
-      anyg |= (L == T);
+      for (int kk = 0; kk < 8; ++kk) {
+        const int s0 = 33 + grp * 8 + kk - M;
+        uint32_t h = __dp4a(w64(lb, v, s0), W0, 0u);
+        if constexpr (M > 4) h = __dp4a(w64(lb, v, s0 + 4), W1, h);
+        anyg |= (h == T);
+      }
+      if (anyg) {
+        if (grp == 0) exact_group<M, 0>(a, v, lb, J, 0u, hm, hits);
+        if (grp == 1) exact_group<M, 1>(a, v, lb, J, 0u, hm, hits);
+        if (grp == 2) exact_group<M, 2>(a, v, lb, J, 0u, hm, hits);
+        if (grp == 3) exact_group<M, 3>(a, v, lb, J, 0u, hm, hits);
+      }
     }
-    if (anyg) {
-      if (grp == 0) exact_group<M, 0>(a, v, lb, J, L0, hm, hits);
-      if (grp == 1) exact_group<M, 1>(a, v, lb, J, L0, hm, hits);
-      if (grp == 2) exact_group<M, 2>(a, v, lb, J, L0, hm, hits);
-      if (grp == 3) exact_group<M, 3>(a, v, lb, J, L0, hm, hits);
+  } else {
+    const RollConsts& K = a.g.K;
+    uint32_t L = fold_tail<M>(lb);
+#pragma unroll
+    for (int grp = 0; grp < 4; ++grp) {
+      const uint32_t L0 = L;
+      bool anyg = false;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        L = roll_step<M>(L, lb, v, grp * 8 + kk, K);
+        anyg |= (L == T);
+      }
+      if (anyg) {
+        if (grp == 0) exact_group<M, 0>(a, v, lb, J, L0, hm, hits);
+        if (grp == 1) exact_group<M, 1>(a, v, lb, J, L0, hm, hits);
+        if (grp == 2) exact_group<M, 2>(a, v, lb, J, L0, hm, hits);
+        if (grp == 3) exact_group<M, 3>(a, v, lb, J, L0, hm, hits);
+      }
     }
   }
 }
