@@ -58,13 +58,20 @@ static_assert(kStageChunk % kTile == 0, "stage chunk must be tile aligned");
 struct rk_ctx {
   int device = 0;
   int num_sms = 0;
-  unsigned long long* d_counters = nullptr;  // [0] matches, [1] hash_hits, [2] collisions
+  // Two alternating "sets" of {counters[4], block_sums[block_sums_cap]}: a scan uses
+  // the current set, and its emit kernel zeroes the other one for the next scan, so a
+  // scan is exactly two kernel launches (no memsets).  counters: [0] matches,
+  // [1] hash_hits, [2] collisions.
+  unsigned long long* d_sets = nullptr;
+  unsigned long long* d_counters = nullptr;  // counters of the current set
+  int cur_set = 0;
+  unsigned long long* d_mcount = nullptr;    // multi-pattern pair counter
   unsigned long long* h_counters = nullptr;  // pinned mirror
   uint32_t* d_tile_info = nullptr;  // per tile: matches | chunk bitmap << 16
   uint64_t tile_info_cap = 0;
   uint32_t* d_masks = nullptr;      // per tile: kTileChunks x 32 lane hit masks
   uint64_t masks_cap = 0;
-  unsigned long long* d_block_sums = nullptr;
+  unsigned long long* d_block_sums = nullptr;  // block sums of the current set
   uint64_t block_sums_cap = 0;
   uint8_t* d_pattern = nullptr;  // pattern of the current scan (points into a cache slot)
   struct PatSlot {
@@ -148,23 +155,39 @@ Geometry geometry(const uint8_t* d_text, uint32_t m, uint64_t start, uint64_t st
   return g;
 }
 
-// Starts a logical scan of `tiles` tiles: per-tile buffers sized, counters and the
-// per-256-tile match sums zeroed.
+uint64_t set_words(const rk_ctx* c) { return 4 + c->block_sums_cap; }
+
+void select_set(rk_ctx* c, int k) {
+  c->cur_set = k;
+  c->d_counters = c->d_sets + (uint64_t)k * set_words(c);
+  c->d_block_sums = c->d_counters + 4;
+}
+
+// Starts a logical scan of `tiles` tiles: per-tile buffers sized, and the next counter
+// set selected (it was zeroed by the previous scan's emit, or on allocation).
 int begin_scan(rk_ctx* c, uint64_t tiles, cudaStream_t s) {
   if (int r = grow(&c->d_tile_info, &c->tile_info_cap, tiles, false, s)) return r;
   if (int r = grow(&c->d_masks, &c->masks_cap, tiles * (uint64_t)(kTileChunks * 32), false, s))
     return r;
   const uint64_t nb = (tiles + kEmitTiles - 1) / kEmitTiles;
-  if (int r = grow(&c->d_block_sums, &c->block_sums_cap, nb, false, s)) return r;
-  RK_CUDA(cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), s));
-  RK_CUDA(cudaMemsetAsync(c->d_block_sums, 0, nb * sizeof(unsigned long long), s));
+  if (!c->d_sets || c->block_sums_cap < nb) {
+    if (c->d_sets) {
+      RK_CUDA(cudaStreamSynchronize(s));
+      RK_CUDA(cudaFree(c->d_sets));
+    }
+    c->block_sums_cap = std::max<uint64_t>(nb, 1024);
+    RK_CUDA(cudaMalloc(&c->d_sets, 2 * set_words(c) * sizeof(unsigned long long)));
+    RK_CUDA(cudaMemsetAsync(c->d_sets, 0, 2 * set_words(c) * sizeof(unsigned long long), s));
+  }
+  select_set(c, c->cur_set ^ 1);
   return RK_OK;
 }
 
 // Orders the offsets of a logical scan whose tiles are sequence numbers [0, tiles)
-// starting at a-space tile `tile0`.
+// starting at a-space tile `tile0`; copies {matches, hash_hits, collisions} to d_counts
+// if given, and zeroes the other counter set for the next scan.
 int emit(rk_ctx* c, uint64_t tiles, uint64_t tile0, int64_t start_bias, int64_t* d_out,
-         uint64_t cap, cudaStream_t s) {
+         uint64_t cap, cudaStream_t s, uint64_t* d_counts = nullptr) {
   EmitArgs e;
   e.tile_info = c->d_tile_info;
   e.masks = c->d_masks;
@@ -175,8 +198,21 @@ int emit(rk_ctx* c, uint64_t tiles, uint64_t tile0, int64_t start_bias, int64_t*
   e.out = d_out;
   e.cap = d_out ? cap : 0;
   e.counters = c->d_counters;
+  e.counts_out = (unsigned long long*)d_counts;
+  e.clear = c->d_sets + (uint64_t)(c->cur_set ^ 1) * set_words(c);
+  e.clear_words = set_words(c);
   RK_CUDA(launch_emit(e, s));
   ++c->launches;
+  return RK_OK;
+}
+
+// Counters of a scan with no windows (or an unreachable hash): zeros.
+int zero_result(rk_ctx* c, uint64_t* d_counts, cudaStream_t s) {
+  if (!c->d_sets) {
+    if (int r = begin_scan(c, 1, s)) return r;
+  }
+  RK_CUDA(cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), s));
+  if (d_counts) RK_CUDA(cudaMemsetAsync(d_counts, 0, 3 * sizeof(uint64_t), s));
   return RK_OK;
 }
 
@@ -262,18 +298,15 @@ int upload_pattern(rk_ctx* c, const uint8_t* h_pattern, uint32_t m, cudaStream_t
 
 int enqueue_scan(rk_ctx* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_pattern,
                  uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t* d_out,
-                 uint64_t cap, int64_t bias, cudaStream_t s) {
-  if (stop <= start || hash_unreachable(m, hx)) {
-    RK_CUDA(cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), s));
-    return RK_OK;
-  }
+                 uint64_t cap, int64_t bias, cudaStream_t s, uint64_t* d_counts = nullptr) {
+  if (stop <= start || hash_unreachable(m, hx)) return zero_result(c, d_counts, s);
   if (int r = upload_pattern(c, h_pattern, m, s)) return r;
   const Geometry g = geometry(d_text, m, start, stop);
   if (int r = begin_scan(c, g.num_tiles, s)) return r;
   if (int r = launch_one(c, d_text, n, m, hx, start, stop, 0, pack_pattern(h_pattern, m), s))
     return r;
   return emit(c, g.num_tiles, g.tile_first, bias - (int64_t)g.amis - (int64_t)m + 1, d_out, cap,
-              s);
+              s, d_counts);
 }
 
 int read_counters(rk_ctx* c, uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits,
@@ -320,7 +353,7 @@ int rk_ctx_create(int device, rk_ctx_t** out) {
   rk_ctx* c = new rk_ctx();
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
-  RK_CUDA(cudaMalloc(&c->d_counters, 4 * sizeof(unsigned long long)));
+  RK_CUDA(cudaMalloc(&c->d_mcount, sizeof(unsigned long long)));
   RK_CUDA(cudaMallocHost(&c->h_counters, 4 * sizeof(unsigned long long)));
   RK_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
   RK_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
@@ -334,11 +367,11 @@ int rk_ctx_destroy(rk_ctx_t* c) {
   if (!c) return RK_OK;
   DeviceGuard g(c->device);
   cudaDeviceSynchronize();
-  cudaFree(c->d_counters);
+  cudaFree(c->d_sets);
+  cudaFree(c->d_mcount);
   cudaFreeHost(c->h_counters);
   cudaFree(c->d_tile_info);
   cudaFree(c->d_masks);
-  cudaFree(c->d_block_sums);
   for (auto& sl : c->pat_cache) cudaFree(sl.d);
   cudaFree(c->d_stage);
   cudaFree(c->d_out_stage);
@@ -367,12 +400,8 @@ int rk_scan_async(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
-  if (int r = enqueue_scan(c, d_text, n, h_pattern, m, hx, start, stop, d_out, cap, out_bias, s))
-    return r;
-  if (d_counts)
-    RK_CUDA(cudaMemcpyAsync(d_counts, c->d_counters, 3 * sizeof(uint64_t),
-                            cudaMemcpyDeviceToDevice, s));
-  return RK_OK;
+  return enqueue_scan(c, d_text, n, h_pattern, m, hx, start, stop, d_out, cap, out_bias, s,
+                      d_counts);
 }
 
 int rk_scan_result(rk_ctx_t* c, uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits,
@@ -405,7 +434,7 @@ int rk_scan_host(rk_ctx_t* c, const uint8_t* h_text, uint64_t n, const uint8_t* 
   cudaStream_t sc = c->s_comp, sk = c->s_copy;
   c->host_last = 0;
   if (stop <= start || hash_unreachable(m, hx)) {
-    RK_CUDA(cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), sc));
+    if (int r = zero_result(c, nullptr, sc)) return r;
     return read_counters(c, matches, collisions, hash_hits, sc);
   }
   // bytes the windows need: [start, stop + m - 1)
@@ -623,7 +652,7 @@ int rk_multi_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
   RK_CUDA(cudaMemcpyAsync(c->d_mtable, table.data(), tsize * sizeof(uint2), cudaMemcpyHostToDevice, s));
   RK_CUDA(cudaMemcpyAsync(c->d_mfilter, filter.data(), kMultiFilterWords * sizeof(uint32_t),
                           cudaMemcpyHostToDevice, s));
-  RK_CUDA(cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), s));
+  RK_CUDA(cudaMemsetAsync(c->d_mcount, 0, sizeof(unsigned long long), s));
 
   const uint64_t nw = n - m + 1;
   Geometry gg = geometry(d_text, m, 0, nw);
@@ -648,7 +677,7 @@ int rk_multi_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
   p.out_off = d_off;
   p.out_idx = d_idx;
   p.cap = cap;
-  p.counters = c->d_counters;
+  p.counters = c->d_mcount;
   p.P = P;
   p.tsize = tsize;
   const uint64_t mgrid = std::max<uint64_t>(
@@ -656,7 +685,7 @@ int rk_multi_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
                             (gg.num_tiles + 15) / 16));
   RK_CUDA(launch_multi(p, (int)mgrid, s));
   ++c->launches;
-  RK_CUDA(cudaMemcpyAsync(c->h_counters, c->d_counters, sizeof(unsigned long long),
+  RK_CUDA(cudaMemcpyAsync(c->h_counters, c->d_mcount, sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, s));
   RK_CUDA(cudaStreamSynchronize(s));
   const uint64_t total = c->h_counters[0];

@@ -55,7 +55,16 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
     if (w < warp) wpre += wsum[w];
   }
   const uint64_t excl = base + wpre + inc - cnt;
-  if (seq == e.num_tiles - 1) e.counters[0] = excl + cnt;
+  if (seq == e.num_tiles - 1) {
+    e.counters[0] = excl + cnt;
+    if (e.counts_out) {
+      e.counts_out[0] = excl + cnt;
+      e.counts_out[1] = e.counters[1];
+      e.counts_out[2] = e.counters[2];
+    }
+  }
+  for (uint64_t i = b * kEmitTiles + tid; i < e.clear_words; i += (uint64_t)gridDim.x * kEmitTiles)
+    e.clear[i] = 0ull;
 
   unsigned todo = __ballot_sync(kFull, cnt != 0);
   while (todo) {

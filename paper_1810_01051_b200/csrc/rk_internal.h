@@ -32,7 +32,10 @@ struct EmitArgs {
   int64_t start_bias;   // written value = a-space end position + start_bias
   int64_t* out;
   uint64_t cap;
-  unsigned long long* counters;  // [0] <- total matches
+  unsigned long long* counters;    // [0] <- total matches ([1], [2] from the scan)
+  unsigned long long* counts_out;  // optional: {matches, hash_hits, collisions}
+  unsigned long long* clear;       // the other counter set, zeroed for the next scan
+  uint64_t clear_words;
 };
 cudaError_t launch_emit(const EmitArgs& e, cudaStream_t s);
 

@@ -195,23 +195,23 @@ __device__ __forceinline__ void exact_group(const ScanArgs& a, const Vec32& v,
       }
     }
     (void)L;
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int kk = 0; kk < 8; ++kk) {
-    const int k = G * 8 + kk;
-    L = 2u * L + b64(lb, v, 32 + k) - (b64(lb, v, 32 + k - M) << M);
-    if (L == T && a.g.valid_end(J + k)) {
-      bool hit = true;
-      if constexpr (M > 24) {  // low 32 bits agree; confirm the high half
-        uint64_t h = 0;
+    for (int kk = 0; kk < 8; ++kk) {
+      const int k = G * 8 + kk;
+      L = 2u * L + b64(lb, v, 32 + k) - (b64(lb, v, 32 + k - M) << M);
+      if (L == T && a.g.valid_end(J + k)) {
+        bool hit = true;
+        if constexpr (M > 24) {  // low 32 bits agree; confirm the high half
+          uint64_t h = 0;
 #pragma unroll
-        for (int i = 0; i < M; ++i) h = (h << 1) + b64(lb, v, 33 + k - M + i);
-        hit = (h == a.hx);
-      }
-      if (hit) {
-        ++hits;
-        if (window_eq<M>(lb, v, 33 + k - M, a.pw)) hm |= 1u << k;
+          for (int i = 0; i < M; ++i) h = (h << 1) + b64(lb, v, 33 + k - M + i);
+          hit = (h == a.hx);
+        }
+        if (hit) {
+          ++hits;
+          if (window_eq<M>(lb, v, 33 + k - M, a.pw)) hm |= 1u << k;
+        }
       }
     }
   }
