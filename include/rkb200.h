@@ -77,6 +77,17 @@ int rk_scan_result(rk_ctx_t* ctx, uint64_t* matches, uint64_t* collisions, uint6
                    void* stream);
 
 /*
+ * rk_scan_bitmap -- MatchResult.to_bitmap (matcher.py:36-42) produced on the device:
+ * d_bitmap (ceil((stop-start)/32) u32 words, caller-allocated) receives bit i (bit i%32
+ * of word i/32) = 1 iff window start+i matches.  1 bit per window instead of 8 bytes
+ * per match.  d_counts (device, 3 x u64, optional) receives
+ * {matches, hash_hits, collisions}.  Asynchronous on `stream`.
+ */
+int rk_scan_bitmap(rk_ctx_t* ctx, const uint8_t* d_text, uint64_t n, const uint8_t* h_pattern,
+                   uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, uint32_t* d_bitmap,
+                   uint64_t* d_counts, void* stream);
+
+/*
  * rk_scan_host -- the end-to-end path for a HOST text (search_sequential /
  * search_parallel called with bytes, matcher.py:101-122, parallel.py:124-177).  The text
  * is staged into HBM in chunks with cudaMemcpyAsync on a copy stream (through an

@@ -21,7 +21,8 @@ MULTI_MAX_PATTERNS = 4096
 # every symbol include/rkb200.h declares (checked by tests/test_capi.py)
 EXPORTS = (
     "rk_version", "rk_last_error", "rk_device_count", "rk_ctx_create", "rk_ctx_destroy",
-    "rk_scan", "rk_scan_async", "rk_scan_result", "rk_scan_host", "rk_scan_host_fetch",
+    "rk_scan", "rk_scan_async", "rk_scan_result", "rk_scan_bitmap", "rk_scan_host",
+    "rk_scan_host_fetch",
     "rk_multi_scan", "rk_window_hashes", "rk_generate", "rk_launch_count",
 )
 
@@ -51,6 +52,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.rk_scan.argtypes = [vp, u8p, u64, u8p, u32, u64, u64, u64, vp, u64, pu64, pu64, pu64, vp]
     lib.rk_scan_async.restype = ci
     lib.rk_scan_async.argtypes = [vp, u8p, u64, u8p, u32, u64, u64, u64, vp, u64, i64, vp, vp]
+    lib.rk_scan_bitmap.restype = ci
+    lib.rk_scan_bitmap.argtypes = [vp, u8p, u64, u8p, u32, u64, u64, u64, vp, vp, vp]
     lib.rk_scan_result.restype = ci
     lib.rk_scan_result.argtypes = [vp, pu64, pu64, pu64, vp]
     lib.rk_scan_host.restype = ci

@@ -148,6 +148,47 @@ def scan(text, pattern, hx: int, start: int, stop: int):
     return offsets, collisions
 
 
+def scan_bitmap(text, pattern, hx: int, start: int, stop: int, *, packed: bool = False):
+    """Match bitmap of windows [start, stop) computed on the device (rk_scan_bitmap):
+    element i is True iff window start+i matches -- MatchResult.to_bitmap
+    (matcher.py:36-42) without materialising offsets (1 bit per window instead of 8 bytes
+    per match).  Returns (bitmap, matches, collisions, hash_hits); the bitmap is a bool
+    CUDA tensor for CUDA text, a bool ndarray for host text, or the packed uint32 words
+    (bit i%32 of word i/32) with packed=True."""
+    torch = _torch()
+    L = _lib.lib()
+    p = _host_bytes(pattern)
+    m = int(p.size)
+    n = _size(text)
+    if m == 0:
+        raise ValueError("empty pattern")
+    count = max(stop - start, 0)
+    dev = _device_of(text)
+    on_host = dev is None
+    if on_host:
+        dev = _lib.default_device()
+        t = torch.from_numpy(np.array(_host_bytes(text), copy=True)).to(f"cuda:{dev}")
+    else:
+        t = text
+    ctx = _lib.context(dev)
+    words = torch.zeros(max((count + 31) // 32, 1), dtype=torch.int32, device=t.device)
+    counts = torch.zeros(3, dtype=torch.int64, device=t.device)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    with ctx.lock:
+        _lib.check(L.rk_scan_bitmap(ctx.handle, t.data_ptr() if n else 0, n, _ptr(p), m,
+                                    int(hx) & ((1 << 64) - 1), start, max(stop, start),
+                                    words.data_ptr(), counts.data_ptr(), stream))
+    mt, hh, co = (int(v) for v in counts.cpu().tolist())
+    if packed:
+        return (words.cpu().numpy().view(np.uint32) if on_host else words), mt, co, hh
+    if on_host:
+        bits = np.unpackbits(words.cpu().numpy().view(np.uint8), bitorder="little")[:count]
+        return bits.astype(bool), mt, co, hh
+    shifts = torch.arange(32, device=t.device, dtype=torch.int32)
+    bits = ((words.unsqueeze(1) >> shifts) & 1).reshape(-1)[:count].bool()
+    return bits, mt, co, hh
+
+
 def window_hashes(text, m: int, start: int, stop: int):
     """uint64 hashes of every window [x, x+m), x in [start, stop) (_scan.py:71-91)."""
     if m < 1:

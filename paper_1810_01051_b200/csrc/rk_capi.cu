@@ -187,7 +187,8 @@ int begin_scan(rk_ctx* c, uint64_t tiles, cudaStream_t s) {
 // starting at a-space tile `tile0`; copies {matches, hash_hits, collisions} to d_counts
 // if given, and zeroes the other counter set for the next scan.
 int emit(rk_ctx* c, uint64_t tiles, uint64_t tile0, int64_t start_bias, int64_t* d_out,
-         uint64_t cap, cudaStream_t s, uint64_t* d_counts = nullptr) {
+         uint64_t cap, cudaStream_t s, uint64_t* d_counts = nullptr,
+         uint32_t* d_bitmap = nullptr, int64_t bit_bias = 0) {
   EmitArgs e;
   e.tile_info = c->d_tile_info;
   e.masks = c->d_masks;
@@ -201,6 +202,12 @@ int emit(rk_ctx* c, uint64_t tiles, uint64_t tile0, int64_t start_bias, int64_t*
   e.counts_out = (unsigned long long*)d_counts;
   e.clear = c->d_sets + (uint64_t)(c->cur_set ^ 1) * set_words(c);
   e.clear_words = set_words(c);
+  e.bitmap = nullptr;
+  e.bit_bias = 0;
+  if (d_bitmap) {
+    e.bitmap = d_bitmap;
+    e.bit_bias = bit_bias;
+  }
   RK_CUDA(launch_emit(e, s));
   ++c->launches;
   return RK_OK;
@@ -402,6 +409,28 @@ int rk_scan_async(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
   cudaStream_t s = (cudaStream_t)stream;
   return enqueue_scan(c, d_text, n, h_pattern, m, hx, start, stop, d_out, cap, out_bias, s,
                       d_counts);
+}
+
+int rk_scan_bitmap(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_pattern,
+                   uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, uint32_t* d_bitmap,
+                   uint64_t* d_counts, void* stream) {
+  if (!c) return fail(RK_EINVAL, "context is NULL");
+  if (int r = check_scan_args(d_text, n, h_pattern, m, start, stop, nullptr, 0)) return r;
+  if (stop > start && !d_bitmap) return fail(RK_EINVAL, "bitmap pointer is NULL");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (stop > start)
+    RK_CUDA(cudaMemsetAsync(d_bitmap, 0, ((stop - start + 31) / 32) * sizeof(uint32_t), s));
+  if (stop <= start || hash_unreachable(m, hx)) return zero_result(c, d_counts, s);
+  if (int r = upload_pattern(c, h_pattern, m, s)) return r;
+  const Geometry gm = geometry(d_text, m, start, stop);
+  if (int r = begin_scan(c, gm.num_tiles, s)) return r;
+  if (int r = launch_one(c, d_text, n, m, hx, start, stop, 0, pack_pattern(h_pattern, m), s))
+    return r;
+  // bit of window start x = (end - m + 1 - amis) - start
+  const int64_t bit_bias = -(int64_t)gm.amis - (int64_t)m + 1 - (int64_t)start;
+  return emit(c, gm.num_tiles, gm.tile_first, 0, nullptr, 0, s, d_counts, d_bitmap, bit_bias);
 }
 
 int rk_scan_result(rk_ctx_t* c, uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits,

@@ -67,6 +67,32 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
     e.clear[i] = 0ull;
 
   unsigned todo = __ballot_sync(kFull, cnt != 0);
+  if (e.bitmap) {
+    // bitmap mode (MatchResult.to_bitmap): each lane ORs its 32 hit bits into place
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint64_t tseq = b * kEmitTiles + warp * 32 + j;
+      uint32_t flags = __shfl_sync(kFull, info, j) >> 16;
+      const int64_t tile_a = (int64_t)((e.tile0 + tseq) * (uint64_t)kTile);
+      const uint32_t* tm = e.masks + tseq * (kTileChunks * 32);
+      while (flags) {
+        const int c = __ffs(flags) - 1;
+        flags &= flags - 1;
+        const uint32_t hm = tm[c * 32 + lane];
+        if (hm) {
+          // hm only has bits of valid windows, so every nonzero part lands in the bitmap
+          const int64_t bit = tile_a + c * kChunk + lane * kR + e.bit_bias;
+          const int64_t word = bit >> 5;  // floor, also for the first (partial) word
+          const int sh = (int)(bit & 31);
+          const uint32_t lo = hm << sh, hi = sh ? hm >> (32 - sh) : 0u;
+          if (lo) atomicOr(&e.bitmap[word], lo);
+          if (hi) atomicOr(&e.bitmap[word + 1], hi);
+        }
+      }
+    }
+    return;
+  }
   while (todo) {
     const int j = __ffs(todo) - 1;
     todo &= todo - 1;

@@ -36,6 +36,8 @@ struct EmitArgs {
   unsigned long long* counts_out;  // optional: {matches, hash_hits, collisions}
   unsigned long long* clear;       // the other counter set, zeroed for the next scan
   uint64_t clear_words;
+  uint32_t* bitmap;                // bitmap mode: bit (end position + bit_bias) per match
+  int64_t bit_bias;
 };
 cudaError_t launch_emit(const EmitArgs& e, cudaStream_t s);
 

@@ -109,6 +109,27 @@ def search_sequential(text, pattern, stats: ScanStats | None = None) -> MatchRes
     return MatchResult(n, m, _to_list(offsets))
 
 
+def search_bitmap(text, pattern, stats: ScanStats | None = None):
+    """search_sequential(text, pattern).to_bitmap() computed on the device without the
+    offset list (matcher.py:36-42 + :101-122): a bool array/tensor with one entry per
+    window, True where a match starts (SURVEY s8f#3)."""
+    t = _scan.as_u8(text)
+    p = _scan.as_u8(pattern)
+    m = _scan._size(p)
+    if m == 0:
+        raise ValueError("empty pattern")
+    n = _scan._size(t)
+    n_windows = n - m + 1
+    if n_windows <= 0:
+        return np.zeros(0, dtype=bool)
+    bits, matches, collisions, hash_hits = _scan.scan_bitmap(t, p, hash_full(p), 0, n_windows)
+    if stats is not None:
+        stats.windows += n_windows
+        stats.hash_hits += hash_hits
+        stats.collisions += collisions
+    return bits
+
+
 def _device_text(t):
     """(device tensor, device index) for search_multi; host text is copied once."""
     import torch

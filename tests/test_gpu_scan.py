@@ -306,3 +306,37 @@ def test_multi_4096_patterns(gpu):
     assert len(out) == len(ps)
     for i, r in out:
         assert r.offsets == expect[i]
+
+
+def test_bitmap_output(gpu):
+    """rk_scan_bitmap == MatchResult.to_bitmap of the oracle offsets (ranges, alignments,
+    dense text)."""
+    torch = _torch()
+    rng = np.random.default_rng(91)
+    base = rng.integers(0, 3, 100000, dtype=np.uint8)
+    dev_base = torch.from_numpy(base).cuda()
+    for shift in (0, 3, 17):
+        host = base[shift:]
+        dev = dev_base[shift:]
+        for m in (1, 4, 9, 31, 32, 40, 70):
+            pat = host[5000 : 5000 + m]
+            hx = oracle.hash_full(pat.tobytes())
+            nw = host.size - m + 1
+            for start, stop in [(0, nw), (7, 70000), (33, 34), (nw - 5, nw)]:
+                eo, ec = oracle.c_scan(host, pat, start, stop)
+                expect = np.zeros(stop - start, dtype=bool)
+                expect[eo - start] = True
+                bits, k, coll, hits = _scan.scan_bitmap(dev, pat.tobytes(), hx, start, stop)
+                assert torch.equal(bits.cpu(), torch.from_numpy(expect)), (shift, m, start, stop)
+                assert k == len(eo) and coll == ec and hits == k + coll
+                hbits, k2, _, _ = _scan.scan_bitmap(host, pat.tobytes(), hx, start, stop)
+                assert (hbits == expect).all() and k2 == k
+    # dense: every window
+    n = 1 << 20
+    t = torch.full((n,), 97, dtype=torch.uint8, device="cuda")
+    bits, k, coll, _ = _scan.scan_bitmap(t, b"aaaa", rk.hash_full(b"aaaa"), 0, n - 3)
+    assert k == n - 3 and bool(bits.all()) and bits.numel() == n - 3
+    st = rk.ScanStats()
+    bm = rk.search_bitmap(b"abab", b"ab", stats=st)
+    assert bm.tolist() == rk.MatchResult(4, 2, [0, 2]).to_bitmap().tolist()
+    assert st == rk.ScanStats(3, 2, 0)
