@@ -51,6 +51,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    # test plumbing only: exercise the multi-rank path on a one-GPU box (all ranks on
+    # cuda:0, gloo instead of NCCL so no collective kernels wait on each other there)
+    ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"))
+    ap.add_argument("--same-device", action="store_true")
     return ap.parse_args()
 
 
@@ -214,10 +218,13 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    dev = local
+    dev = 0 if args.same_device else local
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        else:
+            dist.init_process_group("gloo")
     sweep = [int(x) for x in args.sweep.split(",")]
     per = args.bytes_per_gpu
     n_total = per * world
