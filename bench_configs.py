@@ -62,13 +62,14 @@ def c1(reps):
             "note": "includes the host round trip of the synchronous rk_scan (counts D2H)"}
 
 
-def c3(reps, n=4 << 30, P=1024, m=16):
+def c3(reps, n=4 << 30, P=1024, m=16, alphabet=None, tag="C3"):
     import torch
 
     import paper_1810_01051_b200 as rk
     from paper_1810_01051_b200 import _lib, datagen
 
-    spec = rk.DnaSpec(43, n, ASCII)
+    alphabet = ASCII if alphabet is None else alphabet
+    spec = rk.DnaSpec(43, n, alphabet)
     t = rk.generate_tensor(spec)
     pats = []
     state = 43
@@ -77,7 +78,7 @@ def c3(reps, n=4 << 30, P=1024, m=16):
         x = draw % (n - m + 1)
         pats.append(t[x: x + m].cpu().numpy().tobytes())
     for j in range(P - P // 2):
-        pats.append(rk.generate(rk.DnaSpec((43 ^ 0x5DEECE66D) + j, m, ASCII)))
+        pats.append(rk.generate(rk.DnaSpec((43 ^ 0x5DEECE66D) + j, m, alphabet)))
     ps = rk.PatternSet(pats)
     flat = np.frombuffer(b"".join(ps.patterns), dtype=np.uint8)
     hashes = np.array([rk.hash_full(p) for p in ps.patterns], dtype=np.uint64)
@@ -95,7 +96,7 @@ def c3(reps, n=4 << 30, P=1024, m=16):
                                    ctypes.byref(pairs), s.cuda_stream))
 
     ms = timed(run, reps, s)
-    return {"config": "C3", "bytes": n, "patterns": len(ps), "m": m, "ms": ms,
+    return {"config": tag, "bytes": n, "patterns": len(ps), "m": m, "ms": ms,
             "GBps": n / ms / 1e6, "pairs": int(pairs.value),
             "note": "rk_multi_scan incl. table build + host ordering of the pairs"}
 
@@ -154,7 +155,9 @@ def main():
     ap.add_argument("--only", default="C1,C3,C4,C5")
     ap.add_argument("--reps", type=int, default=5)
     args = ap.parse_args()
-    fns = {"C1": c1, "C3": c3, "C4": c4, "C5": c5}
+    fns = {"C1": c1, "C3": c3, "C4": c4, "C5": c5,
+           # not a BASELINE config: C3's shape over DNA (low-entropy q-grams)
+           "C3dna": lambda r: c3(r, m=32, alphabet=b"ACGT", tag="C3dna")}
     for name in args.only.split(","):
         t0 = time.time()
         r = fns[name](args.reps)

@@ -731,20 +731,37 @@ int rk_multi_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
   }
   if (!c->d_mfilter) RK_CUDA(cudaMalloc(&c->d_mfilter, kMultiFilterWords * sizeof(uint32_t)));
   if (!c->d_qfilter) RK_CUDA(cudaMalloc(&c->d_qfilter, kQFilterWords * sizeof(uint32_t)));
-  // q-gram sampling filter (see rk_multi_impl.cuh): step s, q-gram length q <= m - s + 1
-  const uint32_t qmode = m >= 16 ? 8u : (m >= 7 ? 4u : 0u);
+  // q-gram sampling filter (see rk_multi_impl.cuh): step s, q = 4 * qwords bytes,
+  // q + s - 1 <= m.  Rich alphabets (>= 20 distinct pattern bytes) filter well with
+  // 8-byte q-grams every 8 bytes; small ones (DNA) need longer q-grams.
+  bool seen[256] = {};
+  uint32_t distinct = 0;
+  for (uint64_t i = 0; i < (uint64_t)P * m; ++i)
+    if (!seen[h_patterns[i]]) {
+      seen[h_patterns[i]] = true;
+      ++distinct;
+    }
+  uint32_t qmode = 0, qwords = 0;
+  if (m >= 23 && distinct < 20) qmode = 8, qwords = 4;
+  else if (m >= 15 && distinct < 20) qmode = 4, qwords = 3;
+  else if (m >= 15) qmode = 8, qwords = 2;
+  else if (m >= 11) qmode = 4, qwords = 2;
+  else if (m >= 7) qmode = 4, qwords = 1;
   std::vector<uint32_t> qfilter;
   if (qmode) {
     qfilter.assign(kQFilterWords, 0u);
     for (uint32_t i = 0; i < P; ++i) {
       const uint8_t* p = h_patterns + (uint64_t)i * m;
       for (uint32_t j = 0; j < qmode; ++j) {
-        uint32_t w0 = 0, w1 = 0;
-        memcpy(&w0, p + j, 4);
-        if (qmode == 8) memcpy(&w1, p + j + 4, 4);
-        else w1 = kQ4Salt;
-        uint32_t i1, i2;
-        qgram_bits(w0, w1, i1, i2);
+        uint32_t w[4] = {0, 0, 0, 0};
+        memcpy(w, p + j, 4 * qwords);
+        uint32_t i1 = 0, i2 = 0;
+        switch (qwords) {
+          case 4: qgram_bits<4>(w, i1, i2); break;
+          case 3: qgram_bits<3>(w, i1, i2); break;
+          case 2: qgram_bits<2>(w, i1, i2); break;
+          default: qgram_bits<1>(w, i1, i2); break;
+        }
         qfilter[i1 >> 5] |= 1u << (i1 & 31);
         qfilter[i2 >> 5] |= 1u << (i2 & 31);
       }
@@ -766,15 +783,18 @@ int rk_multi_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
   p.ys_lo = gg.amis;
   p.ys_hi = gg.amis + nw;
   if (qmode) {
-    // tiles over aligned q-gram positions x in [first window start, last start + s)
-    gg.ja_lo = gg.amis;
-    gg.ja_hi = std::min<uint64_t>(gg.amis + nw - 1 + qmode, gg.amis + n);
+    // tiles over the anchors e (window ends of q-grams): [first start + q - 1,
+    // last start + q - 1 + s), clamped to the text
+    const uint64_t q = 4ull * qwords;
+    gg.ja_lo = gg.amis + q - 1;
+    gg.ja_hi = std::min<uint64_t>(gg.amis + nw - 1 + q - 1 + qmode, gg.amis + n);
     gg.tile_first = gg.ja_lo / kTile;
     gg.num_tiles = (gg.ja_hi - 1) / kTile - gg.tile_first + 1;
   }
   p.g = text_geom(gg, n, m, 0);
   p.qfilter = c->d_qfilter;
   p.qmode = qmode;
+  p.qwords = qwords;
   p.pats = c->d_mpats;
   p.phash = c->d_mphash;
   p.filter = c->d_mfilter;

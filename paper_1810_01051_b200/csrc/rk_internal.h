@@ -45,18 +45,17 @@ cudaError_t launch_emit(const EmitArgs& e, cudaStream_t s);
 constexpr int kMultiFilterWords = (1 << 16) / 32;
 constexpr int kQFilterWords = (1 << 19) / 32;  // q-gram Bloom filter, 64 KiB
 constexpr uint32_t kMultiEmpty = 0xffffffffu;
-constexpr uint32_t kQ4Salt = 0x5bd1e995u;      // second word of a 4-byte q-gram
 
-// The two Bloom-filter bit indices (19 bits each) of an 8-byte q-gram (w0, w1) -- the
-// same function on the host (filter build) and the device (text q-grams).
-__host__ __device__ __forceinline__ void qgram_bits(uint32_t w0, uint32_t w1, uint32_t& i1,
+// 2-probe Bloom filter (2^19 bits) of q-grams of QW = 1..4 little-endian words: the two
+// bit indices of a q-gram.  The same function runs on the host (filter build) and the
+// device (text q-grams).
+template <int QW>
+__host__ __device__ __forceinline__ void qgram_bits(const uint32_t* w, uint32_t& i1,
                                                     uint32_t& i2) {
-  uint32_t h = w0 * 0x9E3779B1u;
+  const uint32_t C[4] = {0x9E3779B1u, 0x85EBCA77u, 0xC2B2AE3Du, 0x165667B1u};
+  uint32_t h = w[0] * C[0];
+  for (int i = 1; i < QW; ++i) h += w[i] * C[i];
   h ^= h >> 15;
-  h ^= w1 * 0x85EBCA77u;
-  h ^= h >> 13;
-  h *= 0xC2B2AE3Du;
-  h ^= h >> 16;
   i1 = h >> 13;
   i2 = (h * 0x27D4EB2Fu) >> 13;
 }
@@ -65,6 +64,7 @@ struct MultiArgs {
   TextGeom g;                 // q-gram mode: tiles cover aligned q-gram positions
   const uint32_t* qfilter;    // kQFilterWords words (q-gram mode)
   uint32_t qmode;             // sampling step s (8 or 4), 0 = per-window filter
+  uint32_t qwords;            // q-gram length in words (q = 4 * qwords)
   uint64_t ys_lo, ys_hi;      // valid window starts, a-space
   const uint8_t* pats;        // P * m bytes, deduplicated, index order
   const uint64_t* phash;      // 64-bit hash per pattern

@@ -9,15 +9,16 @@
 // the 64-bit hash (m > 24) and the bytes confirm.
 //
 // Which windows get that test is decided by a filter that never rejects a match:
-//   * q-gram sampling (m >= 7): every occurrence of a pattern p at y covers the aligned
-//     position x = y rounded up to a multiple of s, and the q bytes at x are p[j:j+q] with
-//     j = x - y < s, j + q <= m.  All P*s such q-grams go into a 2^19-bit, 2-probe Bloom
-//     filter in shared memory; the fast pass tests only the aligned q-grams of the text
-//     (one test per s bytes, straight from the 8-byte-aligned words, no rolling hash).  A
-//     q-gram that hits makes the s windows whose aligned position it is candidates; s
-//     lanes of the warp check them at once (exact hash + table + bytes).  Each window has
-//     exactly one aligned position, so nothing is reported twice.
-//     (s, q) = (8, 8) for m >= 16, (4, 4) for 7 <= m < 16.
+//   * q-gram sampling (m >= 7): anchors are the positions e with e + 1 = 0 mod s.  Every
+//     occurrence of a pattern p at y contains exactly one anchored q-gram: the q bytes
+//     ending at the first anchor e >= y + q - 1, which are p[j:j+q] with j = e-q+1-y < s
+//     (so q + s - 1 <= m).  All P*s such pattern q-grams go into a 2^19-bit 2-probe
+//     Bloom filter (64 KiB) in shared memory; the fast pass tests one
+//     word-aligned q-gram per s bytes straight from the loaded words (no rolling hash).
+//     A q-gram that hits makes its s windows candidates; s lanes of the warp check them
+//     at once (exact hash + table + bytes), and since each window has one anchor nothing
+//     is reported twice.  (s, q) is chosen on the host from m and the pattern alphabet:
+//     q up to 16 bytes so that low-entropy texts (DNA: 4^q q-grams) still filter.
 //   * m < 7: every window's exact 32-bit rolling hash is tested against a 2^16-bit
 //     filter of the pattern hashes.
 // Hits are appended with warp ballot/popc and one atomic per warp; the host orders them
@@ -38,11 +39,32 @@ __device__ __forceinline__ bool filter_test(const uint32_t* __restrict__ f, uint
   return (f[b >> 5] >> (b & 31)) & 1u;
 }
 
-__device__ __forceinline__ bool qfilter_test(const uint32_t* __restrict__ f, uint32_t w0,
-                                             uint32_t w1) {
+template <int QW>
+__device__ __forceinline__ bool qfilter_test(const uint32_t* __restrict__ f, const uint32_t* w) {
   uint32_t i1, i2;
-  qgram_bits(w0, w1, i1, i2);
+  qgram_bits<QW>(w, i1, i2);
   return ((f[i1 >> 5] >> (i1 & 31)) & (f[i2 >> 5] >> (i2 & 31)) & 1u) != 0u;
+}
+
+// Anchored q-gram tests of one lane (window-end anchors e = J + s*t + s - 1, the q-gram
+// being the QW words ending at e inside lb ++ v); bit t set when anchor t passes.
+template <int S, int QW>
+__device__ __forceinline__ uint32_t qgram_tests(const uint32_t* f, const Vec32& v,
+                                                const uint32_t (&lb)[8]) {
+  uint32_t w[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    w[i] = lb[i];
+    w[8 + i] = v.w[i];
+  }
+  uint32_t qm = 0;
+#pragma unroll
+  for (int t = 0; t < 32 / S; ++t) {
+    constexpr int kw = S / 4;              // words per step
+    const int end_w = 8 + (t + 1) * kw;    // one past the q-gram's last word
+    qm |= (uint32_t)qfilter_test<QW>(f, &w[end_w - QW]) << t;
+  }
+  return qm;
 }
 
 static __device__ __noinline__ uint64_t multi_hash_global(const uint8_t* text, uint32_t m,
@@ -174,6 +196,33 @@ __device__ __forceinline__ void multi_check_window(const MultiArgs& a, int64_t y
   }
 }
 
+// One tile of anchored q-grams (one per SS bytes, ending at e = J + SS*t + SS - 1); a
+// q-gram that passes the filter makes its SS windows candidates, checked by SS lanes at once.
+template <int SS, int QW>
+__device__ __forceinline__ void qgram_tile(const MultiArgs& a, WarpRing* R, Stream& S,
+                                           uint32_t t, int lane, const uint32_t* sfilter) {
+  constexpr int q = 4 * QW;
+  stream_tile<31, false>(
+      a.g, R, S, t, lane,
+      [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J, int) {
+        const uint32_t qm = qgram_tests<SS, QW>(sfilter, v, lb);
+        unsigned lanes = __ballot_sync(kFull, qm != 0);
+        while (lanes) {
+          const int src = __ffs(lanes) - 1;
+          lanes &= lanes - 1;
+          uint32_t ms = __shfl_sync(kFull, qm, src);
+          const int64_t Js = __shfl_sync(kFull, J, src);
+          while (ms) {
+            const int tt = __ffs(ms) - 1;
+            ms &= ms - 1;
+            // the window whose anchor this is: its q-gram starts j = lane bytes in
+            const int64_t e = Js + (int64_t)SS * tt + SS - 1;
+            multi_check_window(a, e - q + 1 - lane, lane < SS, lane);
+          }
+        }
+      });
+}
+
 template <int M>
 __global__ void __launch_bounds__(kMultiBlock) rk_multi_kernel(const MultiArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -204,35 +253,13 @@ __global__ void __launch_bounds__(kMultiBlock) rk_multi_kernel(const MultiArgs a
         multi_exact<M>(a, ta + c * kChunk + lane * kR, lane, 0, 0);
       }
     } else {
-      // aligned q-grams of the lane's 32 bytes (positions x = J + s*q, J 32-aligned); a
-      // q-gram that passes the Bloom filter makes windows x-s+1 .. x candidates, checked
-      // right away by s lanes of the warp together
-      stream_tile<32, false>(
-          a.g, R, S, t, lane,
-          [&](const Vec32& v, const uint32_t (&)[8], uint32_t&, int64_t J, int) {
-            uint32_t qm = 0;
-            if (s == 8) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                qm |= (uint32_t)qfilter_test(sfilter, v.w[2 * q], v.w[2 * q + 1]) << q;
-            } else {
-#pragma unroll
-              for (int q = 0; q < 8; ++q)
-                qm |= (uint32_t)qfilter_test(sfilter, v.w[q], kQ4Salt) << q;
-            }
-            unsigned lanes = __ballot_sync(kFull, qm != 0);
-            while (lanes) {
-              const int src = __ffs(lanes) - 1;
-              lanes &= lanes - 1;
-              uint32_t ms = __shfl_sync(kFull, qm, src);
-              const int64_t Js = __shfl_sync(kFull, J, src);
-              while (ms) {
-                const int q = __ffs(ms) - 1;
-                ms &= ms - 1;
-                multi_check_window(a, Js + (int64_t)q * s - lane, lane < s, lane);
-              }
-            }
-          });
+      switch (s * 8 + (int)a.qwords) {
+        case 8 * 8 + 4: qgram_tile<8, 4>(a, R, S, t, lane, sfilter); break;
+        case 8 * 8 + 2: qgram_tile<8, 2>(a, R, S, t, lane, sfilter); break;
+        case 4 * 8 + 3: qgram_tile<4, 3>(a, R, S, t, lane, sfilter); break;
+        case 4 * 8 + 2: qgram_tile<4, 2>(a, R, S, t, lane, sfilter); break;
+        default: qgram_tile<4, 1>(a, R, S, t, lane, sfilter); break;
+      }
     }
   }
 }

@@ -277,16 +277,18 @@ def test_multi_qgram_modes_edges(gpu):
     device views at odd offsets, many patterns sharing q-grams."""
     torch = _torch()
     rng = np.random.default_rng(77)
-    for m in (7, 8, 11, 15, 16, 17, 24, 33, 64, 100):
+    cases = [(m, 4) for m in (7, 8, 10, 11, 14, 15, 16, 17, 22, 23, 24, 33, 64, 100)]
+    cases += [(m, 256) for m in (7, 10, 11, 14, 15, 16, 23, 40)]
+    for m, alpha in cases:
         n = 50000
-        base = rng.integers(0, 4, n + 40, dtype=np.uint8)
+        base = rng.integers(0, alpha, n + 40, dtype=np.uint8)
         for shift in (0, 1, 5, 13):
             host = base[shift : shift + n].copy()
             pats = []
             for x in (0, 1, 2, 3, 7, 8, 9, 4095, 4096, 8191, 8192, n // 2 + 3, n - m - 1, n - m):
                 pats.append(host[x : x + m].tobytes())
             for _ in range(40):
-                pats.append(rng.integers(0, 4, m, dtype=np.uint8).tobytes())
+                pats.append(rng.integers(0, alpha, m, dtype=np.uint8).tobytes())
             dev = torch.from_numpy(base).cuda()[shift : shift + n]
             out = rk.search_multi(dev, pats)
             ps, by_len, _ = oracle.pattern_set(pats)
