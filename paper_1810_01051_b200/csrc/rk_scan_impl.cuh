@@ -117,12 +117,10 @@ __device__ __forceinline__ SlowOut slow_chunk(const ScanArgs& a, int64_t J) {
 }
 
 // ---------------------------------------------------------------------------------
-// Short patterns (M < 32) have frequent exact-hash hits on small alphabets (m = 4 over
+// Short patterns (M <= 8) have frequent exact-hash hits on small alphabets (m = 4 over
 // printable ASCII: ~1.2e-3 per window, most 1 KiB chunks), so their candidates are
-// settled inside the fast pass while the bytes are still in registers: the 32 positions
-// roll in four groups of 8, each group ORs its compares into one predicate, and a lane
-// whose group fired re-rolls just those 8 positions exactly (64-bit hash for M > 24,
-// bytes against the pattern).  No chunk is re-read.
+// settled inside the fast pass while the bytes are still in registers (short_chunk).
+// No chunk is re-read.
 
 // Patterns shorter than this settle candidates inline (see short_chunk).
 constexpr int kShortInline = 9;
@@ -176,138 +174,98 @@ __host__ __device__ constexpr uint32_t win_weights(int q) {
   return w;
 }
 
-template <int M, int G>
-__device__ __forceinline__ void exact_group(const ScanArgs& a, const Vec32& v,
-                                            const uint32_t (&lb)[8], int64_t J, uint32_t L,
-                                            uint32_t& hm, uint32_t& hits) {
-  const uint32_t T = (uint32_t)a.hx;
-  if constexpr (M <= 8) {
-    // the whole hash is a dot product of the window's (at most two) words: no re-roll
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const int k = G * 8 + kk;
-      const int s0 = 33 + k - M;  // first byte of the window in lb ++ v
-      uint32_t h = __dp4a(w64(lb, v, s0), win_weights<M>(0), 0u);
-      if constexpr (M > 4) h = __dp4a(w64(lb, v, s0 + 4), win_weights<M>(1), h);
-      if (h == T && a.g.valid_end(J + k)) {
-        ++hits;
-        if (window_eq<M>(lb, v, s0, a.pw)) hm |= 1u << k;
-      }
-    }
-    (void)L;
-  } else {
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const int k = G * 8 + kk;
-      L = 2u * L + b64(lb, v, 32 + k) - (b64(lb, v, 32 + k - M) << M);
-      if (L == T && a.g.valid_end(J + k)) {
-        bool hit = true;
-        if constexpr (M > 24) {  // low 32 bits agree; confirm the high half
-          uint64_t h = 0;
-#pragma unroll
-          for (int i = 0; i < M; ++i) h = (h << 1) + b64(lb, v, 33 + k - M + i);
-          hit = (h == a.hx);
-        }
-        if (hit) {
-          ++hits;
-          if (window_eq<M>(lb, v, 33 + k - M, a.pw)) hm |= 1u << k;
-        }
-      }
-    }
-  }
+// Bit k set when window end J + k is in the launch's range [ja_lo, ja_hi).
+__device__ __forceinline__ uint32_t valid_mask(const TextGeom& g, int64_t J) {
+  const int64_t lo = min(max((int64_t)g.ja_lo - J, (int64_t)0), (int64_t)32);
+  const int64_t hi = min(max((int64_t)g.ja_hi - J, (int64_t)0), (int64_t)32);
+  const uint32_t above = lo >= 32 ? 0u : (0xffffffffu << lo);
+  const uint32_t below = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
+  return above & below;
 }
 
-// One step of the exact 32-bit roll at position k (alternating instruction mixes so the
-// ALU and FMA pipes share the work; see fast_chunk).
-template <int M>
-__device__ __forceinline__ uint32_t roll_step(uint32_t L, const uint32_t (&lb)[8], const Vec32& v,
-                                              int k, const RollConsts& K) {
-  const int io = 32 + k - M;
-  const uint32_t wout = io < 32 ? lb[io >> 2] : v.w[(io - 32) >> 2];
-  if (k & 1) {
-    L = L * K.k2 + bsel(v.w[k >> 2], k & 3);
-    return bsel(wout, io & 3) * K.negpow + L;
-  } else if constexpr (M <= 7) {
-    const uint32_t t = __dp4a(v.w[k >> 2], 1u << (8 * (k & 3)), L * K.k2);
-    return dp4a_us(wout, (uint32_t)(uint8_t)(-(1 << M)) << (8 * (io & 3)), t);
-  } else {
-    const uint32_t t = __dp4a(v.w[k >> 2], 1u << (8 * (k & 3)), L * K.k2);
-    return bsel(wout, io & 3) * K.negpow + t;
-  }
-}
-
-// The 32 positions are checked in four groups of 8; each group ORs its compares into
-// one predicate, and a lane whose group fired settles those 8 positions exactly.
-//  M <= 8: the whole hash is a dot product of the window's (at most two) words with the
-//    weights 2^(M-1-i): per window one funnel shift (shared between neighbours), one or
-//    two dp4a, one compare -- no serial roll chain at all.
-//  M > 8: the exact 32-bit roll.
+// M <= 8: the whole hash of a window is a dot product of its (at most two) words with
+// the weights 2^(M-1-i), so there is no serial roll chain: per window one funnel shift
+// (shared between neighbours), one or two dp4a, one compare.  The 32 positions go in
+// four groups of 8 whose compares OR into one predicate; a group that fired (m = 4 over
+// printable ASCII: ~26% of warp-groups) settles from the words and hashes it still holds
+// in registers -- hit and byte-equality masks, no re-roll, no per-window range test
+// (vmask covers the launch range once per chunk).
 template <int M>
 __device__ __forceinline__ void short_chunk(const ScanArgs& a, const Vec32& v,
-                                            const uint32_t (&lb)[8], int64_t J, uint32_t& hm,
-                                            uint32_t& hits) {
+                                            const uint32_t (&lb)[8], uint32_t vmask,
+                                            uint32_t& hm, uint32_t& hits) {
+  static_assert(M <= 8, "dot-product hashes need M <= 8");
   const uint32_t T = (uint32_t)a.hx;
-  if constexpr (M <= 8) {
-    constexpr uint32_t W0 = win_weights<M>(0), W1 = win_weights<M>(1);
+  constexpr uint32_t W0 = win_weights<M>(0), W1 = win_weights<M>(1);
+  constexpr uint32_t K0 = M >= 4 ? 0xffffffffu : ((1u << (8 * M)) - 1u);
+  constexpr uint32_t K1 = M >= 8 ? 0xffffffffu : M > 4 ? ((1u << (8 * (M - 4))) - 1u) : 0u;
 #pragma unroll
-    for (int grp = 0; grp < 4; ++grp) {
-      bool anyg = false;
+  for (int grp = 0; grp < 4; ++grp) {
+    uint32_t wA[8], wB[8], h[8];
+    bool anyg = false;
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const int s0 = 33 + grp * 8 + kk - M;
-        uint32_t h = __dp4a(w64(lb, v, s0), W0, 0u);
-        if constexpr (M > 4) h = __dp4a(w64(lb, v, s0 + 4), W1, h);
-        anyg |= (h == T);
+    for (int kk = 0; kk < 8; ++kk) {
+      const int s0 = 33 + grp * 8 + kk - M;
+      wA[kk] = w64(lb, v, s0);
+      h[kk] = __dp4a(wA[kk], W0, 0u);
+      if constexpr (M > 4) {
+        wB[kk] = w64(lb, v, s0 + 4);
+        h[kk] = __dp4a(wB[kk], W1, h[kk]);
       }
-      if (anyg) {
-        if (grp == 0) exact_group<M, 0>(a, v, lb, J, 0u, hm, hits);
-        if (grp == 1) exact_group<M, 1>(a, v, lb, J, 0u, hm, hits);
-        if (grp == 2) exact_group<M, 2>(a, v, lb, J, 0u, hm, hits);
-        if (grp == 3) exact_group<M, 3>(a, v, lb, J, 0u, hm, hits);
-      }
+      anyg |= (h[kk] == T);
     }
-  } else {
-    const RollConsts& K = a.g.K;
-    uint32_t L = fold_tail<M>(lb);
-#pragma unroll
-    for (int grp = 0; grp < 4; ++grp) {
-      const uint32_t L0 = L;
-      bool anyg = false;
+    if (anyg) {
+      uint32_t hmask = 0, emask = 0;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
-        L = roll_step<M>(L, lb, v, grp * 8 + kk, K);
-        anyg |= (L == T);
+        uint32_t d = (wA[kk] ^ a.pw.w[0]) & K0;
+        if constexpr (M > 4) d |= (wB[kk] ^ a.pw.w[1]) & K1;
+        if (h[kk] == T) hmask |= 1u << (grp * 8 + kk);
+        if (d == 0u) emask |= 1u << (grp * 8 + kk);
       }
-      if (anyg) {
-        if (grp == 0) exact_group<M, 0>(a, v, lb, J, L0, hm, hits);
-        if (grp == 1) exact_group<M, 1>(a, v, lb, J, L0, hm, hits);
-        if (grp == 2) exact_group<M, 2>(a, v, lb, J, L0, hm, hits);
-        if (grp == 3) exact_group<M, 3>(a, v, lb, J, L0, hm, hits);
-      }
+      hmask &= vmask;  // (hx is a parameter: equal bytes need not mean a hash hit)
+      hits += __popc(hmask);
+      hm |= emask & hmask;
     }
   }
 }
 
-// Records a tile's results for the ordered emission and adds the counters.
+// Per-warp totals of hash hits and matches, flushed to the global counters once per
+// warp at the end of the kernel (m = 4 hits most tiles: a per-tile atomic on one address
+// from every warp would serialise in its L2 slice).
+struct WarpTotals {
+  uint32_t hits = 0;     // this lane's hash hits (< 2^32: a lane sees 1/32 of a warp's windows)
+  uint64_t matches = 0;  // the warp's matches (warp-uniform)
+};
+
+// Records a tile's results for the ordered emission and adds to the warp's totals.
 __device__ __forceinline__ void record_tile(const ScanArgs& a, uint64_t seq, uint32_t my_matches,
-                                            uint32_t my_hits, uint32_t hitflags, int lane) {
+                                            uint32_t my_hits, uint32_t hitflags, int lane,
+                                            WarpTotals& tot) {
   const uint32_t agg = __reduce_add_sync(kFull, my_matches);
-  const uint32_t hits = __reduce_add_sync(kFull, my_hits);
+  tot.hits += my_hits;
+  tot.matches += agg;
   if (lane == 0) {
     a.tile_info[seq] = agg | (hitflags << 16);
     if (agg) atomicAdd(&a.block_sums[seq / kEmitTiles], (unsigned long long)agg);
-    if (hits) {
-      atomicAdd(&a.counters[1], (unsigned long long)hits);
-      atomicAdd(&a.counters[2], (unsigned long long)(hits - agg));
-    }
+  }
+}
+
+__device__ __forceinline__ void flush_totals(const ScanArgs& a, const WarpTotals& tot, int lane) {
+  uint64_t hits = tot.hits;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hits += __shfl_xor_sync(kFull, hits, o);
+  if (lane == 0 && hits) {
+    atomicAdd(&a.counters[1], (unsigned long long)hits);
+    atomicAdd(&a.counters[2], (unsigned long long)(hits - tot.matches));
   }
 }
 
 // Exact pass over the candidate chunks of tile t; records the tile's match count,
-// chunk bitmap and hit masks for the ordered emission and adds the counters.
+// chunk bitmap and hit masks for the ordered emission and adds to the warp's totals.
 template <int M>
 __device__ __forceinline__ void finish_tile(const ScanArgs& a, uint64_t t, uint32_t cand,
-                                            int lane) {
+                                            int lane, WarpTotals& tot) {
   const TextGeom& g = a.g;
   const int64_t ta = g.tile_a(t);
   const uint64_t seq = g.seq_base + t;
@@ -324,7 +282,7 @@ __device__ __forceinline__ void finish_tile(const ScanArgs& a, uint64_t t, uint3
       hitflags |= 1u << c;
     }
   }
-  record_tile(a, seq, my_matches, my_hits, hitflags, lane);
+  record_tile(a, seq, my_matches, my_hits, hitflags, lane, tot);
 }
 
 template <int M>
@@ -340,6 +298,7 @@ __global__ void __launch_bounds__(kBlock, 3) rk_scan_kernel(const ScanArgs a) {
   const auto pred = [T](uint32_t L) { return L == T; };
   Stream S;
   stream_init(a.g, R, S, (uint32_t)w, (uint32_t)W, lane);
+  WarpTotals tot;
   for (uint32_t t = (uint32_t)w; t < (uint32_t)a.g.num_tiles; t += (uint32_t)W) {
     if constexpr (M >= 32) {
       // candidates are ~2^-32 per window: one vote per tile, and a tile with any
@@ -349,21 +308,24 @@ __global__ void __launch_bounds__(kBlock, 3) rk_scan_kernel(const ScanArgs a) {
                      [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t& carryS, int64_t, int) {
                        any |= fast_chunk<M>(v, lb, lane, carryS, a.g.K, pred);
                      });
-      finish_tile<M>(a, t, __any_sync(kFull, any) ? (1u << kTileChunks) - 1 : 0u, lane);
+      finish_tile<M>(a, t, __any_sync(kFull, any) ? (1u << kTileChunks) - 1 : 0u, lane, tot);
     } else if constexpr (M >= kShortInline) {
       // exact hits are rare (m = 8 printable ASCII: ~2% of chunks): flag chunks, settle
       // them in the exact pass
       const uint32_t cand = fast_tile<M, false>(a.g, R, S, t, lane, pred);
-      finish_tile<M>(a, t, cand, lane);
+      finish_tile<M>(a, t, cand, lane, tot);
     } else {
       const uint64_t seq = a.g.seq_base + t;
       uint32_t* tmask = a.masks + seq * (kTileChunks * 32);
       uint32_t hitflags = 0, my_matches = 0, my_hits = 0;
+      const int64_t ta = a.g.tile_a(t);
+      const bool full = ta >= (int64_t)a.g.ja_lo && ta + kTile <= (int64_t)a.g.ja_hi;
       stream_tile<M, false>(a.g, R, S, t, lane,
                             [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J,
                                 int c) {
                        uint32_t hm = 0, hits = 0;
-                       short_chunk<M>(a, v, lb, J, hm, hits);
+                       short_chunk<M>(a, v, lb, full ? 0xffffffffu : valid_mask(a.g, J), hm,
+                                      hits);
                        my_hits += hits;
                        my_matches += __popc(hm);
                        if (__ballot_sync(kFull, hm != 0)) {
@@ -371,9 +333,10 @@ __global__ void __launch_bounds__(kBlock, 3) rk_scan_kernel(const ScanArgs a) {
                          hitflags |= 1u << c;
                        }
                      });
-      record_tile(a, seq, my_matches, my_hits, hitflags, lane);
+      record_tile(a, seq, my_matches, my_hits, hitflags, lane, tot);
     }
   }
+  flush_totals(a, tot, lane);
 }
 
 template <int M>

@@ -56,3 +56,50 @@ def test_gpu_engines_listing(tmp_path, capsys, gpu):
     out = tmp_path / "g.txt"
     assert cli.main(["gen", "--size", "4KB", "--out", str(out)]) == 0
     assert out.stat().st_size == 4096
+
+
+def test_bench_validation_and_formats(capsys):
+    from paper_1810_01051_b200 import bench
+
+    with pytest.raises(ValueError):
+        bench.sweep("nope", [1])
+    with pytest.raises(ValueError):
+        bench.sweep("workers", [])
+    with pytest.raises(ValueError):
+        bench.sweep("workers", [1], bench.SweepConfig(reps=2))
+    with pytest.raises(ValueError):
+        bench.speedup(0, 1)
+    assert bench.speedup(6.0, 2.0) == 3.0
+    rep = bench.BenchReport("pattern_length", [bench.BenchRow(25, 2.0, 1.0, 2.0)], {},
+                            [bench.DeviceRow(25, 0.5, 40.0, 3)])
+    assert bench.format_csv(rep) == "axis_value,t_seq_ms,t_par_ms,speedup\n25,2.0,1.0,2.0\n"
+    table = bench.format_table(rep).split("\n")
+    assert table[0].split() == ["pattern_length", "t_seq_ms", "t_par_ms", "speedup",
+                                "t_dev_ms", "dev_GB/s"]
+    assert table[2].split()[:4] == ["25", "2.000", "1.000", "2.0000"]
+    payload = bench.report_payload(rep)
+    assert payload["rows"] == [{"axis_value": 25, "t_seq_ms": 2.0, "t_par_ms": 1.0, "speedup": 2.0}]
+    assert payload["device_rows"][0]["gbps"] == 40.0
+    assert cli.main(["bench", "--axis", "bogus", "--values", "1"]) == 2
+    assert cli.main(["bench", "--axis", "workers", "--values", ","]) == 2
+    assert cli.main(["bench", "--axis", "workers", "--values", "x"]) == 2
+
+
+@pytest.mark.gpu
+def test_bench_sweep_gpu(tmp_path, capsys, gpu):
+    import json
+
+    from paper_1810_01051_b200 import bench
+
+    cfg = bench.SweepConfig(corpus=bench.DnaSpec(42, 1 << 20), pattern_length=7)
+    rep = bench.sweep("pattern_length", [5, 25], cfg)
+    assert [r.axis_value for r in rep.rows] == [5, 25]
+    assert all(r.speedup == r.t_seq_ms / r.t_par_ms for r in rep.rows)
+    assert [r.axis_value for r in rep.device_rows] == [5, 25]
+    assert all(r.matches >= 1 and r.t_dev_ms > 0 for r in rep.device_rows)
+    base = tmp_path / "rep"
+    assert cli.main(["bench", "--axis", "file_size", "--values", "300KB,1MB", "--size", "1MB",
+                     "--out", str(base), "--format", "json"]) == 0
+    data = json.loads((tmp_path / "rep.json").read_text())
+    assert [r["axis_value"] for r in data["rows"]] == [300 << 10, 1 << 20]
+    assert (tmp_path / "rep.csv").read_text().startswith("axis_value,t_seq_ms,t_par_ms,speedup\n")
