@@ -185,47 +185,71 @@ __device__ __forceinline__ uint32_t valid_mask(const TextGeom& g, int64_t J) {
 
 // M <= 8: the whole hash of a window is a dot product of its (at most two) words with
 // the weights 2^(M-1-i), so there is no serial roll chain: per window one funnel shift
-// (shared between neighbours), one or two dp4a, one compare.  The 32 positions go in
-// four groups of 8 whose compares OR into one predicate; a group that fired (m = 4 over
-// printable ASCII: ~26% of warp-groups) settles from the words and hashes it still holds
-// in registers -- hit and byte-equality masks, no re-roll, no per-window range test
-// (vmask covers the launch range once per chunk).
+// (shared between neighbours) and one or two dp4a that also subtract hx, giving
+// d = hash - hx directly.  The 32 positions go in four groups of 8 with one predicate
+// each: M <= 4 tests half the group as a product of the d's (zero iff some factor is
+// zero, or -- harmlessly -- when 2-adic factors pile up to 2^32: the group is then just
+// settled needlessly) so the FMA pipe carries what the ALU pipe would otherwise queue.
+// A group that fired (m = 4 over printable ASCII: ~26% of warp-groups) settles from the
+// d's and words still in registers: hash hits are counted, and only when some window's
+// bytes equal the pattern (or the tile is at the edge of the range) are the hit and
+// byte masks built.
 template <int M>
 __device__ __forceinline__ void short_chunk(const ScanArgs& a, const Vec32& v,
-                                            const uint32_t (&lb)[8], uint32_t vmask,
+                                            const uint32_t (&lb)[8], bool full, uint32_t vmask,
                                             uint32_t& hm, uint32_t& hits) {
   static_assert(M <= 8, "dot-product hashes need M <= 8");
-  const uint32_t T = (uint32_t)a.hx;
+  const uint32_t negT = 0u - (uint32_t)a.hx;
   constexpr uint32_t W0 = win_weights<M>(0), W1 = win_weights<M>(1);
   constexpr uint32_t K0 = M >= 4 ? 0xffffffffu : ((1u << (8 * M)) - 1u);
   constexpr uint32_t K1 = M >= 8 ? 0xffffffffu : M > 4 ? ((1u << (8 * (M - 4))) - 1u) : 0u;
 #pragma unroll
   for (int grp = 0; grp < 4; ++grp) {
-    uint32_t wA[8], wB[8], h[8];
-    bool anyg = false;
+    uint32_t wA[8], wB[8], d[8];
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
       const int s0 = 33 + grp * 8 + kk - M;
       wA[kk] = w64(lb, v, s0);
-      h[kk] = __dp4a(wA[kk], W0, 0u);
       if constexpr (M > 4) {
         wB[kk] = w64(lb, v, s0 + 4);
-        h[kk] = __dp4a(wB[kk], W1, h[kk]);
+        d[kk] = __dp4a(wA[kk], W0, __dp4a(wB[kk], W1, negT));
+      } else {
+        d[kk] = __dp4a(wA[kk], W0, negT);
       }
-      anyg |= (h[kk] == T);
+    }
+    bool anyg;
+    if constexpr (M <= 4) {
+      const uint32_t p = d[0] * d[1] * d[2] * d[3];
+      anyg = (p == 0u) | (d[4] == 0u) | (d[5] == 0u) | (d[6] == 0u) | (d[7] == 0u);
+    } else {
+      anyg = false;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) anyg |= (d[kk] == 0u);
     }
     if (anyg) {
-      uint32_t hmask = 0, emask = 0;
+      bool anyeq = false;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
-        uint32_t d = (wA[kk] ^ a.pw.w[0]) & K0;
-        if constexpr (M > 4) d |= (wB[kk] ^ a.pw.w[1]) & K1;
-        if (h[kk] == T) hmask |= 1u << (grp * 8 + kk);
-        if (d == 0u) emask |= 1u << (grp * 8 + kk);
+        uint32_t x = (wA[kk] ^ a.pw.w[0]) & K0;
+        if constexpr (M > 4) x |= (wB[kk] ^ a.pw.w[1]) & K1;
+        anyeq |= (x == 0u);
       }
-      hmask &= vmask;  // (hx is a parameter: equal bytes need not mean a hash hit)
-      hits += __popc(hmask);
-      hm |= emask & hmask;
+      if (full && !anyeq) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) hits += (d[kk] == 0u);
+      } else {
+        uint32_t hmask = 0, emask = 0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          uint32_t x = (wA[kk] ^ a.pw.w[0]) & K0;
+          if constexpr (M > 4) x |= (wB[kk] ^ a.pw.w[1]) & K1;
+          if (d[kk] == 0u) hmask |= 1u << (grp * 8 + kk);
+          if (x == 0u) emask |= 1u << (grp * 8 + kk);
+        }
+        hmask &= vmask;  // (hx is a parameter: equal bytes need not mean a hash hit)
+        hits += __popc(hmask);
+        hm |= emask & hmask;
+      }
     }
   }
 }
@@ -324,8 +348,8 @@ __global__ void __launch_bounds__(kBlock, 3) rk_scan_kernel(const ScanArgs a) {
                             [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J,
                                 int c) {
                        uint32_t hm = 0, hits = 0;
-                       short_chunk<M>(a, v, lb, full ? 0xffffffffu : valid_mask(a.g, J), hm,
-                                      hits);
+                       short_chunk<M>(a, v, lb, full, full ? 0xffffffffu : valid_mask(a.g, J),
+                                      hm, hits);
                        my_hits += hits;
                        my_matches += __popc(hm);
                        if (__ballot_sync(kFull, hm != 0)) {
