@@ -39,6 +39,15 @@ __device__ __forceinline__ bool warp_equal(const uint8_t* text, const uint8_t* p
   return __all_sync(kFull, eq);
 }
 
+// Bit k set when window end J + k is in the launch's range [ja_lo, ja_hi).
+__device__ __forceinline__ uint32_t valid_mask(const TextGeom& g, int64_t J) {
+  const int64_t lo = min(max((int64_t)g.ja_lo - J, (int64_t)0), (int64_t)32);
+  const int64_t hi = min(max((int64_t)g.ja_hi - J, (int64_t)0), (int64_t)32);
+  const uint32_t above = lo >= 32 ? 0u : (0xffffffffu << lo);
+  const uint32_t below = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
+  return above & below;
+}
+
 struct SlowOut {
   uint32_t hm;    // hit bits (window end = J + k)
   uint32_t hits;  // hash hits (matches + collisions)
@@ -54,18 +63,28 @@ __device__ __forceinline__ SlowOut slow_chunk(const ScanArgs& a, int64_t J) {
   const Vec32 lbv = load_edge(g, J - 32);
   const uint32_t T = (uint32_t)a.hx;
   if constexpr (M >= 32) {
-    // one candidate at a time, checked by the whole warp
+    // the lane's 32 low-32 hashes first (one dependent IMAD each, no vote inside the
+    // chain), then the candidates one at a time, each checked by the whole warp
     const uint8_t* text = g.abase + g.amis;
     const int lane = threadIdx.x & 31;
     uint32_t S = fold32(lbv.w);
-#pragma unroll 4
+    uint32_t cm = 0;
+#pragma unroll
     for (int k = 0; k < 32; ++k) {
       S = 2u * S + bsel(v.w[k >> 2], k & 3);
-      unsigned todo = __ballot_sync(kFull, S == T && g.valid_end(J + k));
-      while (todo) {
-        const int src = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const int64_t je = __shfl_sync(kFull, J, src) + k - (int64_t)g.amis;  // last byte
+      if (S == T) cm |= 1u << k;
+    }
+    cm &= valid_mask(g, J);
+    unsigned lanes = __ballot_sync(kFull, cm != 0);
+    while (lanes) {
+      const int src = __ffs(lanes) - 1;
+      lanes &= lanes - 1;
+      uint32_t bits = __shfl_sync(kFull, cm, src);
+      const int64_t Js = __shfl_sync(kFull, J, src) - (int64_t)g.amis;
+      while (bits) {
+        const int k = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int64_t je = Js + k;  // text index of the window's last byte
         if (warp_hash64(text, g.m, je, lane) == a.hx) {
           const bool eq = warp_equal(text + je - (int64_t)g.m + 1, a.pattern, g.m, lane);
           if (lane == src) {
@@ -172,15 +191,6 @@ __host__ __device__ constexpr uint32_t win_weights(int q) {
     if (i < M) w |= (uint32_t)(1u << (M - 1 - i)) << (8 * b);
   }
   return w;
-}
-
-// Bit k set when window end J + k is in the launch's range [ja_lo, ja_hi).
-__device__ __forceinline__ uint32_t valid_mask(const TextGeom& g, int64_t J) {
-  const int64_t lo = min(max((int64_t)g.ja_lo - J, (int64_t)0), (int64_t)32);
-  const int64_t hi = min(max((int64_t)g.ja_hi - J, (int64_t)0), (int64_t)32);
-  const uint32_t above = lo >= 32 ? 0u : (0xffffffffu << lo);
-  const uint32_t below = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
-  return above & below;
 }
 
 // M <= 8: the whole hash of a window is a dot product of its (at most two) words with

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--m", default="4")
     ap.add_argument("--bytes", type=int, default=1 << 30)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--source", default="sampled", choices=("sampled", "generated"))
     args = ap.parse_args()
     n = args.bytes
     spec = rk.DnaSpec(42, n, bytes(range(32, 127)))
@@ -34,7 +35,7 @@ def main():
     counts = torch.zeros(3, dtype=torch.int64, device="cuda")
     out = torch.empty(1 << 20, dtype=torch.int64, device="cuda")
     for m in [int(x) for x in args.m.split(",")]:
-        pat = np.frombuffer(rk.datagen.make_pattern(t, spec, m, "sampled"), dtype=np.uint8)
+        pat = np.frombuffer(rk.datagen.make_pattern(t, spec, m, args.source), dtype=np.uint8)
         hx = rk.hash_full(pat.tobytes())
         times = []
         for _ in range(args.reps):
