@@ -143,6 +143,10 @@ __device__ __forceinline__ SlowOut slow_chunk(const ScanArgs& a, int64_t J) {
 
 // Patterns shorter than this settle candidates inline (see short_chunk).
 constexpr int kShortInline = 9;
+// From this length on, M < 32 filters with the 32-byte fold (see rk_scan_kernel): one
+// false positive per 2^M windows sends ~1 KiB/2^(M-10) of chunks to the exact pass, which
+// beats the exact roll from M = 17 (measured: m = 20 4.78 vs 4.27 TB/s, m = 16 4.27 vs 4.35).
+constexpr int kFoldFilter = 17;
 
 // byte i of lb ++ v (i static after unrolling)
 __device__ __forceinline__ uint32_t b64(const uint32_t (&lb)[8], const Vec32& v, int i) {
@@ -343,6 +347,20 @@ __global__ void __launch_bounds__(kBlock, 3) rk_scan_kernel(const ScanArgs a) {
                        any |= fast_chunk<M>(v, lb, lane, carryS, a.g.K, pred);
                      });
       finish_tile<M>(a, t, __any_sync(kFull, any) ? (1u << kTileChunks) - 1 : 0u, lane, tot);
+    } else if constexpr (M >= kFoldFilter) {
+      // the 32-byte fold S(j) agrees with the window hash mod 2^M (the out-term is a
+      // multiple of 2^M), so the m >= 32 chain with a masked compare is an exact-hit
+      // filter (false positives ~2^-M per window); flagged chunks get the exact pass
+      const uint32_t mask = (1u << M) - 1u;  // (M = 16 would compile to PRMT extracts)
+      const auto fpred = [T, mask](uint32_t L) { return ((L ^ T) & mask) == 0u; };
+      uint32_t cand = 0;
+      stream_tile<32>(a.g, R, S, t, lane,
+                      [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t& carryS, int64_t,
+                          int c) {
+                        const bool any = fast_chunk<32>(v, lb, lane, carryS, a.g.K, fpred);
+                        if (__any_sync(kFull, any)) cand |= 1u << c;
+                      });
+      finish_tile<M>(a, t, cand, lane, tot);
     } else if constexpr (M >= kShortInline) {
       // exact hits are rare (m = 8 printable ASCII: ~2% of chunks): flag chunks, settle
       // them in the exact pass
