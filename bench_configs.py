@@ -101,6 +101,50 @@ def c3(reps, n=4 << 30, P=1024, m=16, alphabet=None, tag="C3"):
             "note": "rk_multi_scan incl. table build + host ordering of the pairs"}
 
 
+def c3_mixed(reps, n=4 << 30, P=1024):
+    """C3's corpus and shape with mixed lengths 8..71 (64 distinct -> 4 sweeps of 16
+    lengths) through rk_multi_scan_mixed (not a BASELINE config)."""
+    import torch
+
+    import paper_1810_01051_b200 as rk
+    from paper_1810_01051_b200 import _lib, datagen
+
+    spec = rk.DnaSpec(43, n, ASCII)
+    t = rk.generate_tensor(spec)
+    pats = []
+    state = 43
+    for i in range(P):
+        m = 8 + i % 64
+        draw, state = datagen.splitmix64(state)
+        x = draw % (n - m + 1)
+        pats.append(t[x: x + m].cpu().numpy().tobytes())
+    ps = rk.PatternSet(pats)
+    flat = np.frombuffer(b"".join(ps.patterns), dtype=np.uint8)
+    lengths = np.array([len(p) for p in ps.patterns], dtype=np.uint32)
+    hashes = np.array([rk.hash_full(p) for p in ps.patterns], dtype=np.uint64)
+    ctx = _lib.context()
+    L = _lib.lib()
+    cap = 1 << 20
+    off = torch.empty(cap, dtype=torch.int64, device="cuda")
+    idx = torch.empty(cap, dtype=torch.int32, device="cuda")
+    pairs = _lib.u64ref()
+    s = torch.cuda.current_stream()
+
+    def run():
+        _lib.check(L.rk_multi_scan_mixed(ctx.handle, t.data_ptr(), n, flat.ctypes.data,
+                                         lengths.ctypes.data, len(ps), hashes.ctypes.data,
+                                         off.data_ptr(), idx.data_ptr(), cap, ctypes.byref(pairs),
+                                         s.cuda_stream))
+
+    before = ctx.launches
+    run()
+    sweeps = ctx.launches - before
+    ms = timed(run, reps, s)
+    return {"config": "C3mixed", "bytes": n, "patterns": len(ps), "lengths": "8..71",
+            "sweeps": sweeps, "ms": ms, "GBps": n / ms / 1e6, "pairs": int(pairs.value),
+            "note": "rk_multi_scan_mixed incl. table build + host ordering of the pairs"}
+
+
 def c4(reps, n=16 << 30, m=32):
     import torch
 
@@ -157,7 +201,8 @@ def main():
     args = ap.parse_args()
     fns = {"C1": c1, "C3": c3, "C4": c4, "C5": c5,
            # not a BASELINE config: C3's shape over DNA (low-entropy q-grams)
-           "C3dna": lambda r: c3(r, m=32, alphabet=b"ACGT", tag="C3dna")}
+           "C3dna": lambda r: c3(r, m=32, alphabet=b"ACGT", tag="C3dna"),
+           "C3mixed": c3_mixed}
     for name in args.only.split(","):
         t0 = time.time()
         r = fns[name](args.reps)

@@ -115,6 +115,19 @@ int rk_multi_scan(rk_ctx_t* ctx, const uint8_t* d_text, uint64_t n, const uint8_
                   uint32_t* d_idx, uint64_t cap, uint64_t* pairs, void* stream);
 
 /*
+ * rk_multi_scan_mixed -- a whole PatternSet of mixed lengths (matcher.py:125-157).
+ * h_patterns holds the P deduplicated patterns back to back, pattern i being
+ * h_lengths[i] bytes; pair indices are positions in this list.  Lengths >= 7 share one
+ * sweep over the text per 16 distinct lengths (the reference runs one pass per length,
+ * matcher.py:139-153); each length < 7 gets its own sweep.  Patterns longer than the text
+ * have no windows.  Output and ordering as rk_multi_scan.
+ */
+int rk_multi_scan_mixed(rk_ctx_t* ctx, const uint8_t* d_text, uint64_t n,
+                        const uint8_t* h_patterns, const uint32_t* h_lengths, uint32_t P,
+                        const uint64_t* h_hashes, int64_t* d_off, uint32_t* d_idx, uint64_t cap,
+                        uint64_t* pairs, void* stream);
+
+/*
  * rk_window_hashes -- _scan.py:71-91: d_out[x - start] = hash of window x for
  * x in [start, stop).  Requires stop - 1 + m <= n.
  */

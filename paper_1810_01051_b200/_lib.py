@@ -23,7 +23,7 @@ EXPORTS = (
     "rk_version", "rk_last_error", "rk_device_count", "rk_ctx_create", "rk_ctx_destroy",
     "rk_scan", "rk_scan_async", "rk_scan_result", "rk_scan_bitmap", "rk_scan_host",
     "rk_scan_host_fetch",
-    "rk_multi_scan", "rk_window_hashes", "rk_generate", "rk_launch_count",
+    "rk_multi_scan", "rk_multi_scan_mixed", "rk_window_hashes", "rk_generate", "rk_launch_count",
 )
 
 _lib = None
@@ -62,6 +62,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.rk_scan_host_fetch.argtypes = [vp, vp, u64, u64]
     lib.rk_multi_scan.restype = ci
     lib.rk_multi_scan.argtypes = [vp, u8p, u64, u8p, u32, u32, vp, vp, vp, u64, pu64, vp]
+    lib.rk_multi_scan_mixed.restype = ci
+    lib.rk_multi_scan_mixed.argtypes = [vp, u8p, u64, u8p, vp, u32, vp, vp, vp, u64, pu64, vp]
     lib.rk_window_hashes.restype = ci
     lib.rk_window_hashes.argtypes = [vp, u8p, u64, u32, u64, u64, vp, vp]
     lib.rk_generate.restype = ci

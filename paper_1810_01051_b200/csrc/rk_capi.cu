@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -169,14 +170,9 @@ struct rk_ctx {
   cudaEvent_t ev_copied[kRing] = {};  // ring slot free again
   cudaEvent_t ev_ready = nullptr;                 // bytes of the current chunk landed
   // multi-pattern tables
-  uint8_t* d_mpats = nullptr;
-  uint64_t mpats_cap = 0;
-  uint64_t* d_mphash = nullptr;
-  uint32_t* d_morder = nullptr;
-  uint32_t* d_mfilter = nullptr;
+  uint8_t* d_mblob = nullptr;  // every length group's patterns, hashes and tables
+  uint64_t mblob_cap = 0;
   uint32_t* d_qfilter = nullptr;
-  uint2* d_mtable = nullptr;
-  uint64_t mslots_cap = 0;
   std::mutex mu;
 };
 
@@ -463,12 +459,8 @@ int rk_ctx_destroy(rk_ctx_t* c) {
   cudaEventDestroy(c->ev_ready);
   cudaStreamDestroy(c->s_copy);
   cudaStreamDestroy(c->s_comp);
-  cudaFree(c->d_mpats);
-  cudaFree(c->d_mphash);
-  cudaFree(c->d_morder);
-  cudaFree(c->d_mfilter);
+  cudaFree(c->d_mblob);
   cudaFree(c->d_qfilter);
-  cudaFree(c->d_mtable);
   delete c;
   return RK_OK;
 }
@@ -678,139 +670,207 @@ int rk_multi_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
                   uint32_t P, uint32_t m, const uint64_t* h_hashes, int64_t* d_off,
                   uint32_t* d_idx, uint64_t cap, uint64_t* pairs, void* stream) {
   if (!c) return fail(RK_EINVAL, "context is NULL");
+  if (m < 1) return fail(RK_EINVAL, "patterns must be non-empty");
   if (P < 1 || P > RK_MULTI_MAX_PATTERNS)
     return fail(RK_EINVAL, "pattern count %u outside [1, %d]", P, RK_MULTI_MAX_PATTERNS);
-  if (m < 1 || !h_patterns || !h_hashes) return fail(RK_EINVAL, "patterns must be non-empty");
+  std::vector<uint32_t> lengths(P, m);
+  return rk_multi_scan_mixed(c, d_text, n, h_patterns, lengths.data(), P, h_hashes, d_off, d_idx,
+                             cap, pairs, stream);
+}
+
+int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_patterns,
+                        const uint32_t* h_lengths, uint32_t P, const uint64_t* h_hashes,
+                        int64_t* d_off, uint32_t* d_idx, uint64_t cap, uint64_t* pairs,
+                        void* stream) {
+  if (!c) return fail(RK_EINVAL, "context is NULL");
+  if (P < 1 || P > RK_MULTI_MAX_PATTERNS)
+    return fail(RK_EINVAL, "pattern count %u outside [1, %d]", P, RK_MULTI_MAX_PATTERNS);
+  if (!h_patterns || !h_lengths || !h_hashes) return fail(RK_EINVAL, "NULL pattern arrays");
+  for (uint32_t i = 0; i < P; ++i)
+    if (h_lengths[i] < 1) return fail(RK_EINVAL, "pattern %u is empty", i);
   if (cap && (!d_off || !d_idx)) return fail(RK_EINVAL, "NULL output with cap > 0");
   std::lock_guard<std::mutex> lk(c->mu);
-  DeviceGuard g(c->device);
+  DeviceGuard dg(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   *pairs = 0;
-  if (n < m) return RK_OK;
+
+  // ---- length groups (ascending m) of the patterns that have windows in the text
+  std::vector<uint64_t> first_byte(P + 1, 0);
+  for (uint32_t i = 0; i < P; ++i) first_byte[i + 1] = first_byte[i] + h_lengths[i];
+  std::map<uint32_t, std::vector<uint32_t>> by_len;
+  for (uint32_t i = 0; i < P; ++i)
+    if (h_lengths[i] <= n) by_len[h_lengths[i]].push_back(i);
+  if (by_len.empty()) return RK_OK;
   if (!d_text) return fail(RK_EINVAL, "text pointer is NULL");
 
-  // ---- host build: filter bits, open-addressing table of distinct low32 keys
-  std::vector<std::pair<uint32_t, uint32_t>> keyed(P);
-  for (uint32_t i = 0; i < P; ++i) keyed[i] = {(uint32_t)h_hashes[i], i};
-  std::stable_sort(keyed.begin(), keyed.end(),
-                   [](const auto& x, const auto& y) { return x.first < y.first; });
-  std::vector<uint32_t> order(P);
-  std::vector<std::pair<uint32_t, uint32_t>> runs;  // (key, first<<13 | cnt)
-  for (uint32_t i = 0; i < P;) {
-    uint32_t j = i;
-    while (j < P && keyed[j].first == keyed[i].first) {
-      order[j] = keyed[j].second;
-      ++j;
-    }
-    runs.push_back({keyed[i].first, (i << 13) | (j - i)});
-    i = j;
-  }
-  uint32_t tsize = 64;
-  while (tsize < 2 * runs.size()) tsize <<= 1;
-  std::vector<uint2> table(tsize, make_uint2(0u, kMultiEmpty));
-  std::vector<uint32_t> filter(kMultiFilterWords, 0u);
-  // reachable keys only: m <= 24 windows have hash < 2^32
-  for (const auto& r : runs) {
-    uint32_t slot = (r.first * 0x9E3779B1u) & (tsize - 1);
-    while (table[slot].y != kMultiEmpty) slot = (slot + 1) & (tsize - 1);
-    table[slot] = make_uint2(r.first, r.second);
-    const uint32_t b = (r.first * 0x9E3779B1u) >> 16;
-    filter[b >> 5] |= 1u << (b & 31);
-  }
-  if (int r = grow(&c->d_mpats, &c->mpats_cap, (uint64_t)P * m, false, s)) return r;
-  uint64_t pcap = c->mslots_cap;
-  if (pcap < std::max<uint64_t>(P, tsize)) {
-    cudaFree(c->d_mphash);
-    cudaFree(c->d_morder);
-    cudaFree(c->d_mtable);
-    pcap = std::max<uint64_t>(P, tsize);
-    RK_CUDA(cudaMalloc(&c->d_mphash, pcap * sizeof(uint64_t)));
-    RK_CUDA(cudaMalloc(&c->d_morder, pcap * sizeof(uint32_t)));
-    RK_CUDA(cudaMalloc(&c->d_mtable, pcap * sizeof(uint2)));
-    c->mslots_cap = pcap;
-  }
-  if (!c->d_mfilter) RK_CUDA(cudaMalloc(&c->d_mfilter, kMultiFilterWords * sizeof(uint32_t)));
-  if (!c->d_qfilter) RK_CUDA(cudaMalloc(&c->d_qfilter, kQFilterWords * sizeof(uint32_t)));
-  // q-gram sampling filter (see rk_multi_impl.cuh): step s, q = 4 * qwords bytes,
-  // q + s - 1 <= m.  Rich alphabets (>= 20 distinct pattern bytes) filter well with
-  // 8-byte q-grams every 8 bytes; small ones (DNA) need longer q-grams.
-  bool seen[256] = {};
-  uint32_t distinct = 0;
-  for (uint64_t i = 0; i < (uint64_t)P * m; ++i)
-    if (!seen[h_patterns[i]]) {
-      seen[h_patterns[i]] = true;
-      ++distinct;
-    }
-  uint32_t qmode = 0, qwords = 0;
-  if (m >= 23 && distinct < 20) qmode = 8, qwords = 4;
-  else if (m >= 15 && distinct < 20) qmode = 4, qwords = 3;
-  else if (m >= 15) qmode = 8, qwords = 2;
-  else if (m >= 11) qmode = 4, qwords = 2;
-  else if (m >= 7) qmode = 4, qwords = 1;
-  std::vector<uint32_t> qfilter;
-  if (qmode) {
-    qfilter.assign(kQFilterWords, 0u);
-    for (uint32_t i = 0; i < P; ++i) {
-      const uint8_t* p = h_patterns + (uint64_t)i * m;
-      for (uint32_t j = 0; j < qmode; ++j) {
-        uint32_t w[4] = {0, 0, 0, 0};
-        memcpy(w, p + j, 4 * qwords);
-        uint32_t i1 = 0, i2 = 0;
-        switch (qwords) {
-          case 4: qgram_bits<4>(w, i1, i2); break;
-          case 3: qgram_bits<3>(w, i1, i2); break;
-          case 2: qgram_bits<2>(w, i1, i2); break;
-          default: qgram_bits<1>(w, i1, i2); break;
-        }
-        qfilter[i1 >> 5] |= 1u << (i1 & 31);
-        qfilter[i2 >> 5] |= 1u << (i2 & 31);
+  // ---- host build of every group's tables in one blob (one upload):
+  //      pats | phash | order | gidx | table | filter, 16-byte aligned sections
+  struct Built {
+    uint32_t m, P, tsize;
+    uint64_t pats, phash, order, gidx, table, filter;  // blob offsets
+  };
+  std::vector<Built> built;
+  std::vector<uint8_t> blob;
+  auto reserve = [&blob](uint64_t bytes) {
+    const uint64_t off = (blob.size() + 15) & ~(uint64_t)15;
+    blob.resize(off + bytes, 0);
+    return off;
+  };
+  for (const auto& [m, members] : by_len) {
+    Built b{};
+    b.m = m;
+    b.P = (uint32_t)members.size();
+    std::vector<std::pair<uint32_t, uint32_t>> keyed(b.P);
+    for (uint32_t i = 0; i < b.P; ++i) keyed[i] = {(uint32_t)h_hashes[members[i]], i};
+    std::stable_sort(keyed.begin(), keyed.end(),
+                     [](const auto& x, const auto& y) { return x.first < y.first; });
+    std::vector<uint32_t> order(b.P);
+    std::vector<std::pair<uint32_t, uint32_t>> runs;  // (key, first << 13 | count)
+    for (uint32_t i = 0; i < b.P;) {
+      uint32_t j = i;
+      while (j < b.P && keyed[j].first == keyed[i].first) {
+        order[j] = keyed[j].second;
+        ++j;
       }
+      runs.push_back({keyed[i].first, (i << 13) | (j - i)});
+      i = j;
     }
-    RK_CUDA(cudaMemcpyAsync(c->d_qfilter, qfilter.data(), kQFilterWords * sizeof(uint32_t),
-                            cudaMemcpyHostToDevice, s));
+    b.tsize = 64;
+    while (b.tsize < 2 * runs.size()) b.tsize <<= 1;
+    b.pats = reserve((uint64_t)b.P * m);
+    b.phash = reserve((uint64_t)b.P * sizeof(uint64_t));
+    b.order = reserve((uint64_t)b.P * sizeof(uint32_t));
+    b.gidx = reserve((uint64_t)b.P * sizeof(uint32_t));
+    b.table = reserve((uint64_t)b.tsize * sizeof(uint2));
+    b.filter = reserve(kMultiFilterWords * sizeof(uint32_t));
+    uint8_t* base = blob.data();
+    for (uint32_t i = 0; i < b.P; ++i) {
+      memcpy(base + b.pats + (uint64_t)i * m, h_patterns + first_byte[members[i]], m);
+      memcpy(base + b.phash + 8ull * i, &h_hashes[members[i]], 8);
+      memcpy(base + b.gidx + 4ull * i, &members[i], 4);
+    }
+    memcpy(base + b.order, order.data(), 4ull * b.P);
+    uint2* table = reinterpret_cast<uint2*>(base + b.table);
+    uint32_t* filter = reinterpret_cast<uint32_t*>(base + b.filter);
+    for (uint32_t t = 0; t < b.tsize; ++t) table[t] = make_uint2(0u, kMultiEmpty);
+    for (const auto& r : runs) {
+      uint32_t slot = (r.first * 0x9E3779B1u) & (b.tsize - 1);
+      while (table[slot].y != kMultiEmpty) slot = (slot + 1) & (b.tsize - 1);
+      table[slot] = make_uint2(r.first, r.second);
+      const uint32_t bit = (r.first * 0x9E3779B1u) >> 16;
+      filter[bit >> 5] |= 1u << (bit & 31);
+    }
+    built.push_back(b);
   }
-  RK_CUDA(cudaMemcpyAsync(c->d_mpats, h_patterns, (uint64_t)P * m, cudaMemcpyHostToDevice, s));
-  RK_CUDA(cudaMemcpyAsync(c->d_mphash, h_hashes, P * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-  RK_CUDA(cudaMemcpyAsync(c->d_morder, order.data(), P * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-  RK_CUDA(cudaMemcpyAsync(c->d_mtable, table.data(), tsize * sizeof(uint2), cudaMemcpyHostToDevice, s));
-  RK_CUDA(cudaMemcpyAsync(c->d_mfilter, filter.data(), kMultiFilterWords * sizeof(uint32_t),
-                          cudaMemcpyHostToDevice, s));
+  if (int r = grow(&c->d_mblob, &c->mblob_cap, (uint64_t)blob.size(), false, s)) return r;
+  if (!c->d_qfilter) RK_CUDA(cudaMalloc(&c->d_qfilter, kQFilterWords * sizeof(uint32_t)));
+  RK_CUDA(cudaMemcpyAsync(c->d_mblob, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
   RK_CUDA(cudaMemsetAsync(c->d_mcount, 0, sizeof(unsigned long long), s));
 
-  const uint64_t nw = n - m + 1;
-  Geometry gg = geometry(d_text, m, 0, nw);
-  MultiArgs p{};
-  p.ys_lo = gg.amis;
-  p.ys_hi = gg.amis + nw;
-  if (qmode) {
-    // tiles over the anchors e (window ends of q-grams): [first start + q - 1,
-    // last start + q - 1 + s), clamped to the text
+  const uint8_t* dev = c->d_mblob;
+  auto group_of = [&](const Built& b, uint64_t amis) {
+    MultiGroup G{};
+    G.pats = dev + b.pats;
+    G.phash = reinterpret_cast<const uint64_t*>(dev + b.phash);
+    G.order = reinterpret_cast<const uint32_t*>(dev + b.order);
+    G.gidx = reinterpret_cast<const uint32_t*>(dev + b.gidx);
+    G.table = reinterpret_cast<const uint2*>(dev + b.table);
+    G.filter = reinterpret_cast<const uint32_t*>(dev + b.filter);
+    G.ys_hi = amis + (n - b.m + 1);
+    G.m = b.m;
+    G.tsize = b.tsize;
+    return G;
+  };
+  auto launch = [&](MultiArgs& p, const Geometry& gg, uint32_t m) -> int {
+    p.g = text_geom(gg, n, m, 0);
+    p.ys_lo = gg.amis;
+    p.out_off = d_off;
+    p.out_idx = d_idx;
+    p.cap = cap;
+    p.counters = c->d_mcount;
+    const uint64_t grid = std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)c->num_sms * multi_blocks_per_sm(p.qmode, m),
+                              (gg.num_tiles + kMultiWarps - 1) / kMultiWarps));
+    RK_CUDA(launch_multi(p, (int)grid, s));
+    ++c->launches;
+    return RK_OK;
+  };
+
+  // ---- m < 7: one launch per length, every window's hash against the group's filter
+  size_t gi = 0;
+  for (; gi < built.size() && built[gi].m < 7; ++gi) {
+    const Built& b = built[gi];
+    Geometry gg = geometry(d_text, b.m, 0, n - b.m + 1);
+    MultiArgs p{};
+    p.qmode = 0;
+    p.G = 1;
+    p.grp[0] = group_of(b, gg.amis);
+    if (int r = launch(p, gg, b.m)) return r;
+  }
+  // ---- m >= 7: up to kMultiMaxGroups lengths per sweep, one shared q-gram filter
+  std::vector<uint32_t> qfilter(kQFilterWords);
+  for (; gi < built.size(); gi += kMultiMaxGroups) {
+    const size_t g_end = std::min(built.size(), gi + kMultiMaxGroups);
+    const uint32_t m_min = built[gi].m;
+    // (s, q = 4 * qwords) from the shortest length (q + s - 1 <= m_min) and the
+    // alphabet: rich alphabets (>= 20 distinct pattern bytes) filter well with 8-byte
+    // q-grams every 8 bytes; small ones (DNA) need longer q-grams
+    bool seen[256] = {};
+    uint32_t distinct = 0;
+    for (size_t k = gi; k < g_end; ++k)
+      for (uint64_t i = 0; i < (uint64_t)built[k].P * built[k].m; ++i) {
+        const uint8_t byte = blob[built[k].pats + i];
+        if (!seen[byte]) {
+          seen[byte] = true;
+          ++distinct;
+        }
+      }
+    uint32_t qmode, qwords;
+    if (m_min >= 23 && distinct < 20) qmode = 8, qwords = 4;
+    else if (m_min >= 15 && distinct < 20) qmode = 4, qwords = 3;
+    else if (m_min >= 15) qmode = 8, qwords = 2;
+    else if (m_min >= 11) qmode = 4, qwords = 2;
+    else qmode = 4, qwords = 1;
+    std::fill(qfilter.begin(), qfilter.end(), 0u);
+    for (size_t k = gi; k < g_end; ++k)
+      for (uint32_t i = 0; i < built[k].P; ++i) {
+        const uint8_t* p = blob.data() + built[k].pats + (uint64_t)i * built[k].m;
+        for (uint32_t j = 0; j < qmode; ++j) {
+          uint32_t w[4] = {0, 0, 0, 0};
+          memcpy(w, p + j, 4 * qwords);
+          uint32_t i1 = 0, i2 = 0;
+          switch (qwords) {
+            case 4: qgram_bits<4>(w, i1, i2); break;
+            case 3: qgram_bits<3>(w, i1, i2); break;
+            case 2: qgram_bits<2>(w, i1, i2); break;
+            default: qgram_bits<1>(w, i1, i2); break;
+          }
+          qfilter[i1 >> 5] |= 1u << (i1 & 31);
+          qfilter[i2 >> 5] |= 1u << (i2 & 31);
+        }
+      }
+    // pageable source: the call returns once the bytes are staged, so the vector may be
+    // refilled for the next sweep (which is ordered after this one on the stream)
+    RK_CUDA(cudaMemcpyAsync(c->d_qfilter, qfilter.data(), kQFilterWords * sizeof(uint32_t),
+                            cudaMemcpyHostToDevice, s));
+    // tiles over the anchors e (q-gram ends): [first start + q - 1, last start of the
+    // shortest length + q - 1 + s), clamped to the text
+    const uint64_t nw = n - m_min + 1;
+    Geometry gg = geometry(d_text, m_min, 0, nw);
     const uint64_t q = 4ull * qwords;
     gg.ja_lo = gg.amis + q - 1;
     gg.ja_hi = std::min<uint64_t>(gg.amis + nw - 1 + q - 1 + qmode, gg.amis + n);
     gg.tile_first = gg.ja_lo / kTile;
     gg.num_tiles = (gg.ja_hi - 1) / kTile - gg.tile_first + 1;
+    MultiArgs p{};
+    p.qfilter = c->d_qfilter;
+    p.qmode = qmode;
+    p.qwords = qwords;
+    p.G = (uint32_t)(g_end - gi);
+    for (size_t k = gi; k < g_end; ++k) p.grp[k - gi] = group_of(built[k], gg.amis);
+    if (int r = launch(p, gg, m_min)) return r;
   }
-  p.g = text_geom(gg, n, m, 0);
-  p.qfilter = c->d_qfilter;
-  p.qmode = qmode;
-  p.qwords = qwords;
-  p.pats = c->d_mpats;
-  p.phash = c->d_mphash;
-  p.filter = c->d_mfilter;
-  p.table = c->d_mtable;
-  p.order = c->d_morder;
-  p.out_off = d_off;
-  p.out_idx = d_idx;
-  p.cap = cap;
-  p.counters = c->d_mcount;
-  p.P = P;
-  p.tsize = tsize;
-  const uint64_t mgrid = std::max<uint64_t>(
-      1, std::min<uint64_t>((uint64_t)c->num_sms * multi_blocks_per_sm(m, tsize),
-                            (gg.num_tiles + 15) / 16));
-  RK_CUDA(launch_multi(p, (int)mgrid, s));
-  ++c->launches;
+
   RK_CUDA(cudaMemcpyAsync(c->h_counters, c->d_mcount, sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, s));
   RK_CUDA(cudaStreamSynchronize(s));

@@ -60,25 +60,35 @@ __host__ __device__ __forceinline__ void qgram_bits(const uint32_t* w, uint32_t&
   i2 = (h * 0x27D4EB2Fu) >> 13;
 }
 
+// One length group of a multi-pattern launch (all arrays device-resident).
+struct MultiGroup {
+  const uint8_t* pats;     // P_g * m bytes, the group's patterns back to back
+  const uint64_t* phash;   // 64-bit hash per pattern
+  const uint32_t* order;   // group-local pattern indices, grouped by low-32 key
+  const uint32_t* gidx;    // group-local index -> the caller's pattern index
+  const uint2* table;      // tsize entries: {key, (first << 13) | count}, y = empty marker
+  const uint32_t* filter;  // kMultiFilterWords words over the low-32 keys
+  uint64_t ys_hi;          // one past the last window start with room for m bytes (a-space)
+  uint32_t m, tsize;
+};
+constexpr int kMultiMaxGroups = 16;
+constexpr int kMultiWarps = 16;  // one 16-warp CTA per SM shares the 64 KiB q-gram filter  // length groups per sweep (kernel parameter space)
+
 struct MultiArgs {
-  TextGeom g;                 // q-gram mode: tiles cover aligned q-gram positions
+  TextGeom g;                 // q-gram mode: tiles cover the anchors (q-gram ends)
   const uint32_t* qfilter;    // kQFilterWords words (q-gram mode)
-  uint32_t qmode;             // sampling step s (8 or 4), 0 = per-window filter
+  uint32_t qmode;             // sampling step s (8 or 4), 0 = per-window filter (m < 7)
   uint32_t qwords;            // q-gram length in words (q = 4 * qwords)
-  uint64_t ys_lo, ys_hi;      // valid window starts, a-space
-  const uint8_t* pats;        // P * m bytes, deduplicated, index order
-  const uint64_t* phash;      // 64-bit hash per pattern
-  const uint32_t* filter;     // kMultiFilterWords words
-  const uint2* table;         // tsize entries: {key, (first << 13) | count}, y = empty marker
-  const uint32_t* order;      // pattern indices grouped by key
+  uint64_t ys_lo;             // first valid window start, a-space
   int64_t* out_off;
   uint32_t* out_idx;
   uint64_t cap;
   unsigned long long* counters;  // [0] = pairs found
-  uint32_t P, tsize;
+  uint32_t G;                    // length groups in grp (1 when qmode == 0)
+  MultiGroup grp[kMultiMaxGroups];
 };
-size_t multi_smem_bytes(uint32_t tsize);
-int multi_blocks_per_sm(uint32_t m, uint32_t tsize);
+size_t multi_smem_bytes();
+int multi_blocks_per_sm(uint32_t qmode, uint32_t m);
 cudaError_t launch_multi(const MultiArgs& a, int grid, cudaStream_t s);
 
 // auxiliaries (rk_aux.cu)

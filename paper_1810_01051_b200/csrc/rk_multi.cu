@@ -1,35 +1,65 @@
-// rk_multi.cu -- dispatch of the multi-pattern scan variants (instantiated in
-// rk_multi_g0..3.cu, kernels in rk_multi_impl.cuh).
-#include "rk_device.cuh"
-#include "rk_internal.h"
+// rk_multi.cu -- dispatch of the multi-pattern scan kernels (m < 7 variants instantiated
+// in rk_multi_g0.cu; kernels in rk_multi_impl.cuh).
+#include "rk_multi_impl.cuh"
 
 namespace rkb {
 
-template <int M>
-cudaError_t launch_multi_m(const MultiArgs& a, int grid, cudaStream_t s);
-template <int M>
-int multi_occupancy_m(uint32_t tsize);
+// Every length >= 7 of the set in one sweep: anchored q-grams against the shared filter.
+__global__ void __launch_bounds__(kMultiBlock) rk_multi_qgram_kernel(const MultiArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  WarpRing* rings = reinterpret_cast<WarpRing*>(smem);
+  uint32_t* sfilter = reinterpret_cast<uint32_t*>(smem + sizeof(WarpRing) * kMultiWarps);
+  for (int i = threadIdx.x; i < kQFilterWords; i += blockDim.x) sfilter[i] = a.qfilter[i];
+  __syncthreads();
 
-using MultiLaunchFn = cudaError_t (*)(const MultiArgs&, int, cudaStream_t);
-using MultiOccFn = int (*)(uint32_t);
-template <int... Ms>
-struct MultiTable {
-  static constexpr MultiLaunchFn launch[sizeof...(Ms)] = {&launch_multi_m<Ms>...};
-  static constexpr MultiOccFn occ[sizeof...(Ms)] = {&multi_occupancy_m<Ms>...};
-};
-using MTable = MultiTable<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20,
-                          21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32>;
-
-static int mvariant(uint32_t m) { return m >= 32 ? 31 : (int)m - 1; }
-
-size_t multi_smem_bytes(uint32_t) {
-  return sizeof(WarpRing) * 16 + kQFilterWords * sizeof(uint32_t);
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  WarpRing* R = rings + warp;
+  ring_init(R, lane);
+  const uint64_t W = (uint64_t)gridDim.x * kMultiWarps;
+  const uint64_t w = (uint64_t)blockIdx.x * kMultiWarps + warp;
+  Stream S;
+  stream_init(a.g, R, S, (uint32_t)w, (uint32_t)W, lane);
+  const int s = (int)a.qmode;
+  for (uint32_t t = (uint32_t)w; t < (uint32_t)a.g.num_tiles; t += (uint32_t)W) {
+    switch (s * 8 + (int)a.qwords) {
+      case 8 * 8 + 4: qgram_tile<8, 4>(a, R, S, t, lane, sfilter); break;
+      case 8 * 8 + 2: qgram_tile<8, 2>(a, R, S, t, lane, sfilter); break;
+      case 4 * 8 + 3: qgram_tile<4, 3>(a, R, S, t, lane, sfilter); break;
+      case 4 * 8 + 2: qgram_tile<4, 2>(a, R, S, t, lane, sfilter); break;
+      default: qgram_tile<4, 1>(a, R, S, t, lane, sfilter); break;
+    }
+  }
 }
 
-int multi_blocks_per_sm(uint32_t m, uint32_t tsize) { return MTable::occ[mvariant(m)](tsize); }
+template <int M>
+cudaError_t launch_multi_short(const MultiArgs& a, int grid, cudaStream_t s);
+template <int M>
+int multi_short_occupancy();
+
+using MultiLaunchFn = cudaError_t (*)(const MultiArgs&, int, cudaStream_t);
+using MultiOccFn = int (*)();
+static constexpr MultiLaunchFn kShortLaunch[6] = {
+    &launch_multi_short<1>, &launch_multi_short<2>, &launch_multi_short<3>,
+    &launch_multi_short<4>, &launch_multi_short<5>, &launch_multi_short<6>};
+static constexpr MultiOccFn kShortOcc[6] = {
+    &multi_short_occupancy<1>, &multi_short_occupancy<2>, &multi_short_occupancy<3>,
+    &multi_short_occupancy<4>, &multi_short_occupancy<5>, &multi_short_occupancy<6>};
+
+size_t multi_smem_bytes() {
+  return sizeof(WarpRing) * kMultiWarps + kQFilterWords * sizeof(uint32_t);
+}
+
+int multi_blocks_per_sm(uint32_t qmode, uint32_t m) {
+  if (qmode == 0) return kShortOcc[m - 1]();
+  static int occ = 0;  // same on every B200
+  if (!occ) occ = multi_occupancy(rk_multi_qgram_kernel);
+  return occ;
+}
 
 cudaError_t launch_multi(const MultiArgs& a, int grid, cudaStream_t s) {
-  return MTable::launch[mvariant(a.g.m)](a, grid, s);
+  if (a.qmode == 0) return kShortLaunch[a.g.m - 1](a, grid, s);
+  return multi_launch_kernel(rk_multi_qgram_kernel, a, grid, s);
 }
 
 }  // namespace rkb

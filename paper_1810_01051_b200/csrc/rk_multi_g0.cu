@@ -1,22 +1,29 @@
-// rk_multi_g0.cu -- explicit instantiations of the multi-pattern scan for m in
-// {1, 2, 3, 4, 5, 6, 7, 8} (m = 32 stands for every m >= 32).
+// rk_multi_g0.cu -- explicit instantiations of the m < 7 multi-pattern kernels.
 #include "rk_multi_impl.cuh"
 
 namespace rkb {
-template cudaError_t launch_multi_m<1>(const MultiArgs&, int, cudaStream_t);
-template int multi_occupancy_m<1>(uint32_t);
-template cudaError_t launch_multi_m<2>(const MultiArgs&, int, cudaStream_t);
-template int multi_occupancy_m<2>(uint32_t);
-template cudaError_t launch_multi_m<3>(const MultiArgs&, int, cudaStream_t);
-template int multi_occupancy_m<3>(uint32_t);
-template cudaError_t launch_multi_m<4>(const MultiArgs&, int, cudaStream_t);
-template int multi_occupancy_m<4>(uint32_t);
-template cudaError_t launch_multi_m<5>(const MultiArgs&, int, cudaStream_t);
-template int multi_occupancy_m<5>(uint32_t);
-template cudaError_t launch_multi_m<6>(const MultiArgs&, int, cudaStream_t);
-template int multi_occupancy_m<6>(uint32_t);
-template cudaError_t launch_multi_m<7>(const MultiArgs&, int, cudaStream_t);
-template int multi_occupancy_m<7>(uint32_t);
-template cudaError_t launch_multi_m<8>(const MultiArgs&, int, cudaStream_t);
-template int multi_occupancy_m<8>(uint32_t);
+
+template <int M>
+cudaError_t launch_multi_short(const MultiArgs& a, int grid, cudaStream_t s) {
+  return multi_launch_kernel(rk_multi_short_kernel<M>, a, grid, s);
+}
+
+template <int M>
+int multi_short_occupancy() {
+  return multi_occupancy(rk_multi_short_kernel<M>);
+}
+
+template cudaError_t launch_multi_short<1>(const MultiArgs&, int, cudaStream_t);
+template cudaError_t launch_multi_short<2>(const MultiArgs&, int, cudaStream_t);
+template cudaError_t launch_multi_short<3>(const MultiArgs&, int, cudaStream_t);
+template cudaError_t launch_multi_short<4>(const MultiArgs&, int, cudaStream_t);
+template cudaError_t launch_multi_short<5>(const MultiArgs&, int, cudaStream_t);
+template cudaError_t launch_multi_short<6>(const MultiArgs&, int, cudaStream_t);
+template int multi_short_occupancy<1>();
+template int multi_short_occupancy<2>();
+template int multi_short_occupancy<3>();
+template int multi_short_occupancy<4>();
+template int multi_short_occupancy<5>();
+template int multi_short_occupancy<6>();
+
 }  // namespace rkb

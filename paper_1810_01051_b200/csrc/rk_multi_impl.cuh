@@ -1,26 +1,29 @@
-// rk_multi_impl.cuh -- multi-pattern scan over one equal-length group of a PatternSet
-// (/root/reference/pkg/src/rkmatch/matcher.py:139-153: per length, hash every window,
-// look the hash up in the set's hash index, byte-verify every pattern carrying it).
+// rk_multi_impl.cuh -- multi-pattern scan of a PatternSet (/root/reference/pkg/src/rkmatch/
+// matcher.py:125-157: per length, hash every window, look the hash up in the set's hash
+// index, byte-verify every pattern carrying it) -- here all lengths >= 7 of a set share
+// ONE sweep over the text, the reference's per-length passes being the
+// special case of one length group.
 //
 // The exact test is the reference's: a window matches pattern i iff its Rabin hash
-// equals hash_full(pattern i) and its bytes equal the pattern.  Hashes are looked up in a
-// table of the distinct low-32 keys whose entries point at the run of patterns sharing the
-// key (several patterns may share a hash, e.g. "ac"/"ba", tests/test_matcher.py:139-146);
-// the 64-bit hash (m > 24) and the bytes confirm.
+// equals hash_full(pattern i) and its bytes equal the pattern.  Per length group, hashes
+// are looked up in a table of the distinct low-32 keys whose entries point at the run of
+// patterns sharing the key (several patterns may share a hash, e.g. "ac"/"ba",
+// tests/test_matcher.py:139-146); the 64-bit hash (m > 24) and the bytes confirm.
 //
 // Which windows get that test is decided by a filter that never rejects a match:
-//   * q-gram sampling (m >= 7): anchors are the positions e with e + 1 = 0 mod s.  Every
-//     occurrence of a pattern p at y contains exactly one anchored q-gram: the q bytes
-//     ending at the first anchor e >= y + q - 1, which are p[j:j+q] with j = e-q+1-y < s
-//     (so q + s - 1 <= m).  All P*s such pattern q-grams go into a 2^19-bit 2-probe
-//     Bloom filter (64 KiB) in shared memory; the fast pass tests one
-//     word-aligned q-gram per s bytes straight from the loaded words (no rolling hash).
-//     A q-gram that hits makes its s windows candidates; s lanes of the warp check them
-//     at once (exact hash + table + bytes), and since each window has one anchor nothing
-//     is reported twice.  (s, q) is chosen on the host from m and the pattern alphabet:
-//     q up to 16 bytes so that low-entropy texts (DNA: 4^q q-grams) still filter.
-//   * m < 7: every window's exact 32-bit rolling hash is tested against a 2^16-bit
-//     filter of the pattern hashes.
+//   * q-gram sampling (every length >= 7): anchors are the positions e with
+//     e + 1 = 0 mod s.  Every occurrence of a pattern p at y contains exactly one anchored
+//     q-gram: the q bytes ending at the first anchor e >= y + q - 1, which are p[j:j+q]
+//     with j = e-q+1-y < s (so q + s - 1 <= m; (s, q) follow the group's shortest
+//     length).  All such pattern q-grams go into a 2^19-bit 2-probe Bloom filter (64 KiB)
+//     in shared memory; the fast pass tests one word-aligned q-gram per s bytes straight
+//     from the loaded words (no rolling hash).  A q-gram that hits makes its s window
+//     starts candidates; s lanes of the warp check them at once against every length
+//     group (exact hash + table + bytes), and since each window has one anchor nothing
+//     is reported twice.  (s, q) is chosen on the host from the lengths and the pattern
+//     alphabet: q up to 16 bytes so that low-entropy texts (DNA: 4^q q-grams) still filter.
+//   * m < 7 (one length per launch): every window's exact 32-bit rolling hash is tested
+//     against a 2^16-bit filter of the pattern hashes.
 // Hits are appended with warp ballot/popc and one atomic per warp; the host orders them
 // by (pattern index, offset), which is exactly the reference's per-pattern ascending lists.
 #pragma once
@@ -29,7 +32,6 @@
 
 namespace rkb {
 
-constexpr int kMultiWarps = 16;  // one 16-warp CTA per SM shares the 64 KiB q-gram filter
 constexpr int kMultiBlock = 32 * kMultiWarps;
 
 __device__ __forceinline__ uint32_t mhash(uint32_t key) { return key * 0x9E3779B1u; }
@@ -75,10 +77,13 @@ static __device__ __noinline__ uint64_t multi_hash_global(const uint8_t* text, u
   return h;
 }
 
-// Index of the pattern the window ending at text index je (low32 hash L) matches, or -1.
-// Deduplicated patterns of one length are distinct, so at most one can byte-match.
+// Caller's index of the pattern of group G that the window ending at text index je (low32
+// hash L) matches, or -1.  Deduplicated patterns of one length are distinct, so at most
+// one can byte-match.  (Fields by value: a reference into the kernel parameters would
+// force them into local memory.)
 static __device__ __noinline__ int multi_resolve(const uint8_t* text, const uint8_t* pats,
                                                  const uint64_t* phash, const uint32_t* order,
+                                                 const uint32_t* gidx,
                                                  const uint2* __restrict__ tbl, uint32_t tsize,
                                                  uint32_t m, uint32_t L, int64_t je) {
   uint32_t slot = mhash(L) & (tsize - 1);
@@ -106,7 +111,7 @@ static __device__ __noinline__ int multi_resolve(const uint8_t* text, const uint
             eq = false;
             break;
           }
-        if (eq) return (int)idx;
+        if (eq) return (int)gidx[idx];
       }
       return -1;
     }
@@ -114,73 +119,13 @@ static __device__ __noinline__ int multi_resolve(const uint8_t* text, const uint
   }
 }
 
-// Exact pass over the 32 windows ending at [J, J+32) of this lane (a-space).  With
-// q-gram sampling on (s > 0) a window is taken only if its aligned position
-// x = roundup(start, s) lies in [X0, X0 + kChunk).
-template <int M>
-__device__ __forceinline__ void multi_exact(const MultiArgs& a, int64_t J, int lane, int s,
-                                            int64_t X0) {
-  const TextGeom& g = a.g;
-  const Vec32 v = load_edge(g, J);
-  const Vec32 lbv = load_edge(g, J - 32);
-  const uint8_t* text = g.abase + g.amis;
-  uint32_t L;
-  if constexpr (M >= 32) L = fold32(lbv.w);
-  else L = fold_tail<M>(lbv.w);
-#pragma unroll 4
-  for (int k = 0; k < 32; ++k) {
-    if constexpr (M >= 32) {
-      L = 2u * L + bsel(v.w[k >> 2], k & 3);
-    } else {
-      const int io = 32 + k - M;
-      const uint32_t in = bsel(v.w[k >> 2], k & 3);
-      const uint32_t out =
-          io < 32 ? bsel(lbv.w[io >> 2], io & 3) : bsel(v.w[(io - 32) >> 2], io & 3);
-      L = 2u * L + in - (out << M);
-    }
-    const int64_t ja = J + k;                  // window end (a-space)
-    const int64_t ya = ja - (int64_t)g.m + 1;  // window start (a-space)
-    bool take = ya >= (int64_t)a.ys_lo && ya < (int64_t)a.ys_hi;
-    if (s > 0) {  // s is a power of two
-      const int64_t xa = (ya + s - 1) & ~(int64_t)(s - 1);
-      take = take && xa >= X0 && xa < X0 + kChunk;
-    }
-    int idx = -1;
-    if (take && filter_test(a.filter, L))
-      idx = multi_resolve(text, a.pats, a.phash, a.order, a.table, a.tsize, g.m, L,
-                          ja - (int64_t)g.amis);
-    const unsigned hit = __ballot_sync(kFull, idx >= 0);
-    if (hit) {
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(&a.counters[0], (unsigned long long)__popc(hit));
-      base = __shfl_sync(kFull, base, 0);
-      if (idx >= 0) {
-        const uint64_t pos = base + __popc(hit & ((1u << lane) - 1u));
-        if (pos < a.cap) {
-          a.out_off[pos] = ya - (int64_t)g.amis;
-          a.out_idx[pos] = (uint32_t)idx;
-        }
-      }
-    }
-  }
+__device__ __forceinline__ int group_resolve(const MultiGroup& G, const uint8_t* text, uint32_t L,
+                                             int64_t je) {
+  return multi_resolve(text, G.pats, G.phash, G.order, G.gidx, G.table, G.tsize, G.m, L, je);
 }
 
-// Exact check of the window starting at a-position ya (lanes with active == false only
-// take part in the warp collectives).  Appends (offset, pattern) on a match.
-__device__ __forceinline__ void multi_check_window(const MultiArgs& a, int64_t ya, bool active,
-                                                   int lane) {
-  const TextGeom& g = a.g;
-  int idx = -1;
-  if (active && ya >= (int64_t)a.ys_lo && ya < (int64_t)a.ys_hi) {
-    const uint8_t* text = g.abase + g.amis;
-    const int64_t y = ya - (int64_t)g.amis;     // text index of the first byte
-    const int64_t je = y + (int64_t)g.m - 1;    // ... and of the last
-    const uint32_t span = g.m < 32 ? g.m : 32;  // low 32 bits of the hash: last <= 32 bytes
-    uint32_t L = 0;
-    for (uint32_t i = 0; i < span; ++i) L = 2u * L + text[je - span + 1 + i];
-    if (filter_test(a.filter, L))
-      idx = multi_resolve(text, a.pats, a.phash, a.order, a.table, a.tsize, g.m, L, je);
-  }
+// Appends (window start, pattern) for the lanes with idx >= 0: one atomic per warp.
+__device__ __forceinline__ void multi_append(const MultiArgs& a, int idx, int64_t y, int lane) {
   const unsigned hit = __ballot_sync(kFull, idx >= 0);
   if (hit) {
     unsigned long long base = 0;
@@ -189,10 +134,56 @@ __device__ __forceinline__ void multi_check_window(const MultiArgs& a, int64_t y
     if (idx >= 0) {
       const uint64_t pos = base + __popc(hit & ((1u << lane) - 1u));
       if (pos < a.cap) {
-        a.out_off[pos] = ya - (int64_t)g.amis;
+        a.out_off[pos] = y;
         a.out_idx[pos] = (uint32_t)idx;
       }
     }
+  }
+}
+
+// Exact pass over the 32 windows ending at [J, J+32) of this lane (a-space), for the
+// single length group of an m < 7 launch.
+template <int M>
+__device__ __forceinline__ void multi_exact(const MultiArgs& a, int64_t J, int lane) {
+  const TextGeom& g = a.g;
+  const Vec32 v = load_edge(g, J);
+  const Vec32 lbv = load_edge(g, J - 32);
+  const uint8_t* text = g.abase + g.amis;
+  uint32_t L = fold_tail<M>(lbv.w);
+#pragma unroll 4
+  for (int k = 0; k < 32; ++k) {
+    const int io = 32 + k - M;
+    const uint32_t in = bsel(v.w[k >> 2], k & 3);
+    const uint32_t out =
+        io < 32 ? bsel(lbv.w[io >> 2], io & 3) : bsel(v.w[(io - 32) >> 2], io & 3);
+    L = 2u * L + in - (out << M);
+    const int64_t ja = J + k;             // window end (a-space)
+    const int64_t ya = ja - (int64_t)M + 1;  // window start (a-space)
+    int idx = -1;
+    if (ya >= (int64_t)a.ys_lo && ya < (int64_t)a.grp[0].ys_hi && filter_test(a.grp[0].filter, L))
+      idx = group_resolve(a.grp[0], text, L, ja - (int64_t)g.amis);
+    multi_append(a, idx, ya - (int64_t)g.amis, lane);
+  }
+}
+
+// Exact check of the window(s) starting at a-position ya against every length group
+// (lanes with active == false only take part in the warp collectives).
+__device__ __forceinline__ void multi_check_window(const MultiArgs& a, int64_t ya, bool active,
+                                                   int lane) {
+  const TextGeom& g = a.g;
+  const uint8_t* text = g.abase + g.amis;
+  const int64_t y = ya - (int64_t)g.amis;  // text index of the first byte
+  for (uint32_t gi = 0; gi < a.G; ++gi) {
+    const uint32_t m = a.grp[gi].m;
+    int idx = -1;
+    if (active && ya >= (int64_t)a.ys_lo && ya < (int64_t)a.grp[gi].ys_hi) {
+      const int64_t je = y + (int64_t)m - 1;  // text index of the last byte
+      const uint32_t span = m < 32 ? m : 32;  // low 32 bits of the hash: last <= 32 bytes
+      uint32_t L = 0;
+      for (uint32_t i = 0; i < span; ++i) L = 2u * L + text[je - span + 1 + i];
+      if (filter_test(a.grp[gi].filter, L)) idx = group_resolve(a.grp[gi], text, L, je);
+    }
+    multi_append(a, idx, y, lane);
   }
 }
 
@@ -223,14 +214,13 @@ __device__ __forceinline__ void qgram_tile(const MultiArgs& a, WarpRing* R, Stre
       });
 }
 
+// m < 7: one length group, every window's exact rolling hash against a 2^16-bit filter.
 template <int M>
-__global__ void __launch_bounds__(kMultiBlock) rk_multi_kernel(const MultiArgs a) {
+__global__ void __launch_bounds__(kMultiBlock) rk_multi_short_kernel(const MultiArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   WarpRing* rings = reinterpret_cast<WarpRing*>(smem);
   uint32_t* sfilter = reinterpret_cast<uint32_t*>(smem + sizeof(WarpRing) * kMultiWarps);
-  const int nwords = a.qmode ? kQFilterWords : kMultiFilterWords;
-  const uint32_t* gsrc = a.qmode ? a.qfilter : a.filter;
-  for (int i = threadIdx.x; i < nwords; i += blockDim.x) sfilter[i] = gsrc[i];
+  for (int i = threadIdx.x; i < kMultiFilterWords; i += blockDim.x) sfilter[i] = a.grp[0].filter[i];
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
@@ -241,46 +231,35 @@ __global__ void __launch_bounds__(kMultiBlock) rk_multi_kernel(const MultiArgs a
   const uint64_t w = (uint64_t)blockIdx.x * kMultiWarps + warp;
   Stream S;
   stream_init(a.g, R, S, (uint32_t)w, (uint32_t)W, lane);
-  const int s = (int)a.qmode;
+  const auto pred = [sfilter](uint32_t L) { return filter_test(sfilter, L); };
   for (uint32_t t = (uint32_t)w; t < (uint32_t)a.g.num_tiles; t += (uint32_t)W) {
     const int64_t ta = a.g.tile_a(t);
-    if (s == 0) {
-      const auto pred = [sfilter](uint32_t L) { return filter_test(sfilter, L); };
-      uint32_t cand = fast_tile<M, false>(a.g, R, S, t, lane, pred);
-      while (cand) {
-        const int c = __ffs(cand) - 1;
-        cand &= cand - 1;
-        multi_exact<M>(a, ta + c * kChunk + lane * kR, lane, 0, 0);
-      }
-    } else {
-      switch (s * 8 + (int)a.qwords) {
-        case 8 * 8 + 4: qgram_tile<8, 4>(a, R, S, t, lane, sfilter); break;
-        case 8 * 8 + 2: qgram_tile<8, 2>(a, R, S, t, lane, sfilter); break;
-        case 4 * 8 + 3: qgram_tile<4, 3>(a, R, S, t, lane, sfilter); break;
-        case 4 * 8 + 2: qgram_tile<4, 2>(a, R, S, t, lane, sfilter); break;
-        default: qgram_tile<4, 1>(a, R, S, t, lane, sfilter); break;
-      }
+    uint32_t cand = fast_tile<M, false>(a.g, R, S, t, lane, pred);
+    while (cand) {
+      const int c = __ffs(cand) - 1;
+      cand &= cand - 1;
+      multi_exact<M>(a, ta + c * kChunk + lane * kR, lane);
     }
   }
 }
 
-template <int M>
-cudaError_t launch_multi_m(const MultiArgs& a, int grid, cudaStream_t s) {
-  const size_t smem = multi_smem_bytes(a.tsize);
-  cudaError_t e = cudaFuncSetAttribute(rk_multi_kernel<M>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  rk_multi_kernel<M><<<grid, kMultiBlock, smem, s>>>(a);
-  return cudaGetLastError();
+template <class K>
+int multi_occupancy(K kernel) {
+  const size_t smem = multi_smem_bytes();
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kMultiBlock, smem);
+  return b > 0 ? b : 1;
 }
 
-template <int M>
-int multi_occupancy_m(uint32_t tsize) {
-  const size_t smem = multi_smem_bytes(tsize);
-  cudaFuncSetAttribute(rk_multi_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rk_multi_kernel<M>, kMultiBlock, smem);
-  return b > 0 ? b : 1;
+template <class K>
+cudaError_t multi_launch_kernel(K kernel, const MultiArgs& a, int grid, cudaStream_t s) {
+  const size_t smem = multi_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  kernel<<<grid, kMultiBlock, smem, s>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace rkb

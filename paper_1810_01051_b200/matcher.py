@@ -143,15 +143,16 @@ def _device_text(t):
     return host.to(f"cuda:{dev}", non_blocking=True), dev
 
 
-def multi_group(t_dev, dev: int, pats: list[bytes]):
-    """One equal-length group through rk_multi_scan -> [offsets ndarray per pattern]."""
+def multi_scan(t_dev, dev: int, pats: list[bytes]):
+    """Patterns of any lengths through rk_multi_scan_mixed (one device sweep for all lengths
+    >= 7) -> [offsets ndarray per pattern]."""
     import torch
 
     L = _lib.lib()
-    m = len(pats[0])
     P = len(pats)
     n = int(t_dev.numel())
     flat = np.frombuffer(b"".join(pats), dtype=np.uint8)
+    lengths = np.array([len(p) for p in pats], dtype=np.uint32)
     hashes = np.array([hash_full(p) for p in pats], dtype=np.uint64)
     ctx = _lib.context(dev)
     stream = torch.cuda.current_stream(dev).cuda_stream
@@ -161,9 +162,10 @@ def multi_group(t_dev, dev: int, pats: list[bytes]):
         off = torch.empty(cap, dtype=torch.int64, device=t_dev.device)
         idx = torch.empty(cap, dtype=torch.int32, device=t_dev.device)
         with ctx.lock:
-            _lib.check(L.rk_multi_scan(ctx.handle, t_dev.data_ptr(), n, flat.ctypes.data, P, m,
-                                       hashes.ctypes.data, off.data_ptr(), idx.data_ptr(), cap,
-                                       ctypes.byref(pairs), stream))
+            _lib.check(L.rk_multi_scan_mixed(ctx.handle, t_dev.data_ptr(), n, flat.ctypes.data,
+                                             lengths.ctypes.data, P, hashes.ctypes.data,
+                                             off.data_ptr(), idx.data_ptr(), cap,
+                                             ctypes.byref(pairs), stream))
         k = int(pairs.value)
         if k <= cap:
             break
@@ -175,7 +177,8 @@ def multi_group(t_dev, dev: int, pats: list[bytes]):
 
 
 def search_multi(text, patterns) -> list[tuple[int, MatchResult]]:
-    """Every pattern of a PatternSet, one device sweep per length (matcher.py:125-157).
+    """Every pattern of a PatternSet (matcher.py:125-157): all lengths >= 7 in one device
+    sweep, each shorter length in its own.
 
     Returns one (pattern index, MatchResult) per distinct pattern, in index order; each
     result equals search_naive for that pattern."""
@@ -184,16 +187,14 @@ def search_multi(text, patterns) -> list[tuple[int, MatchResult]]:
     t = _scan.as_u8(text)
     n = _scan._size(t)
     found: dict[int, list[int]] = {i: [] for i in range(len(patterns))}
-    lengths = [m for m in sorted(patterns.by_length) if n - m + 1 > 0]
-    if lengths:
+    idxs = [i for i, p in enumerate(patterns.patterns) if len(p) <= n]
+    if idxs:
         t_dev, dev = _device_text(t)
-        for m in lengths:
-            idxs = patterns.by_length[m]
-            for a in range(0, len(idxs), _lib.MULTI_MAX_PATTERNS):
-                batch = idxs[a : a + _lib.MULTI_MAX_PATTERNS]
-                per = multi_group(t_dev, dev, [patterns.patterns[i] for i in batch])
-                for i, offs in zip(batch, per):
-                    found[i] = offs.tolist()
+        for a in range(0, len(idxs), _lib.MULTI_MAX_PATTERNS):
+            batch = idxs[a : a + _lib.MULTI_MAX_PATTERNS]
+            per = multi_scan(t_dev, dev, [patterns.patterns[i] for i in batch])
+            for i, offs in zip(batch, per):
+                found[i] = offs.tolist()
     return [
         (i, MatchResult(n, len(patterns.patterns[i]), found[i]))
         for i in range(len(patterns))

@@ -297,6 +297,39 @@ def test_multi_qgram_modes_edges(gpu):
                 assert r.offsets == expect[i], (m, shift, i)
 
 
+def test_multi_mixed_lengths_one_sweep(gpu):
+    """Every length >= 7 of a set shares a sweep (16 lengths per launch); lengths < 7 get
+    their own; results equal the per-length oracle, at both text ends and any alignment."""
+    torch = _torch()
+    from paper_1810_01051_b200 import _lib
+
+    rng = np.random.default_rng(81)
+    for alpha in (4, 95):
+        n = 150000
+        base = (rng.integers(0, alpha, n + 16, dtype=np.uint8) + (0 if alpha == 4 else 32)).astype(np.uint8)
+        for shift in (0, 3):
+            host = base[shift : shift + n].copy()
+            lengths = list(range(7, 27)) + [3, 5, 40, 64, 100]
+            pats = []
+            for m in lengths:
+                for x in (0, 1, 4095, 4096, n // 3, n - m):
+                    pats.append(host[x : x + m].tobytes())
+                pats.append((rng.integers(0, alpha, m) + (0 if alpha == 4 else 32)).astype(np.uint8).tobytes())
+            dev = torch.from_numpy(base).cuda()[shift : shift + n]
+            ctx = _lib.context()
+            before = ctx.launches
+            out = rk.search_multi(dev, pats)
+            sweeps = ctx.launches - before
+            assert sweeps == 2 + 2, sweeps  # m = 3 and 5 alone, 23 lengths >= 7 in 2 sweeps
+            ps, by_len, _ = oracle.pattern_set(pats)
+            expect = {}
+            for m, idxs in by_len.items():
+                for j, offs in oracle.c_search_multi_group(host, [ps[i] for i in idxs]):
+                    expect[idxs[j]] = offs.tolist()
+            for i, r in out:
+                assert r.offsets == expect[i], (alpha, shift, i, len(ps[i]))
+
+
 def test_multi_4096_patterns(gpu):
     rng = np.random.default_rng(78)
     text = rng.integers(0, 256, 1 << 20, dtype=np.uint8)
