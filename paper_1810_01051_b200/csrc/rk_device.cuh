@@ -159,25 +159,6 @@ __device__ __forceinline__ uint32_t fold_tail(const uint32_t (&lb)[8]) {
   return s;
 }
 
-// fold of bytes [E-M, E) of the 64-byte array lb ++ v, exact mod 2^32 (E, M static).
-template <int M, int E>
-__device__ __forceinline__ uint32_t fold_at(const uint32_t (&lb)[8], const uint32_t (&v)[8]) {
-  static_assert(M >= 1 && M < 32 && E >= M && E <= 64, "fold_at");
-  constexpr int first = E - M;
-  constexpr int a4 = (first + 3) & ~3;  // first word-aligned byte
-  uint32_t s = 0;
-#pragma unroll
-  for (int i = first; i < (a4 < E ? a4 : E); ++i)
-    s = 2u * s + (i < 32 ? bsel(lb[i >> 2], i & 3) : bsel(v[(i - 32) >> 2], i & 3));
-#pragma unroll
-  for (int i = a4; i + 4 <= E; i += 4)
-    s = __dp4a(i < 32 ? lb[i >> 2] : v[(i - 32) >> 2], kFoldW, s << 4);
-#pragma unroll
-  for (int i = (E & ~3) > a4 ? (E & ~3) : a4; i < E; ++i)
-    s = 2u * s + (i < 32 ? bsel(lb[i >> 2], i & 3) : bsel(v[(i - 32) >> 2], i & 3));
-  return s;
-}
-
 // dp4a with unsigned text bytes and signed weights (PTX dp4a.u32.s32).
 __device__ __forceinline__ uint32_t dp4a_us(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;

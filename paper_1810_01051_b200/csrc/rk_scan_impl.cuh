@@ -96,6 +96,7 @@ __device__ __forceinline__ SlowOut slow_chunk(const ScanArgs& a, int64_t J) {
     }
   } else {
     uint32_t L = fold_tail<M>(lbv.w);
+    uint32_t cm = 0;
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
       const int io = 32 + k - M;
@@ -103,32 +104,26 @@ __device__ __forceinline__ SlowOut slow_chunk(const ScanArgs& a, int64_t J) {
       const uint32_t out =
           io < 32 ? bsel(lbv.w[io >> 2], io & 3) : bsel(v.w[(io - 32) >> 2], io & 3);
       L = 2u * L + in - (out << M);
-      if (L == T && g.valid_end(J + k)) {
-        // window bytes are positions [33+k-M, 32+k] of lbv ++ v
-        bool hit = true;
-        if constexpr (M > 24) {
-          uint64_t h = 0;
-#pragma unroll
-          for (int i = 0; i < M; ++i) {
-            const int p = 33 + k - M + i;
-            const uint32_t b =
-                p < 32 ? bsel(lbv.w[p >> 2], p & 3) : bsel(v.w[(p - 32) >> 2], p & 3);
-            h = (h << 1) + b;
-          }
-          hit = (h == a.hx);
-        }
-        if (hit) {
-          ++r.hits;
-          bool eq = true;
-#pragma unroll
-          for (int i = 0; i < M; ++i) {
-            const int p = 33 + k - M + i;
-            const uint32_t b =
-                p < 32 ? bsel(lbv.w[p >> 2], p & 3) : bsel(v.w[(p - 32) >> 2], p & 3);
-            eq &= (b == bsel(a.pw.w[i >> 2], i & 3));
-          }
-          if (eq) r.hm |= 1u << k;
-        }
+      if (L == T) cm |= 1u << k;
+    }
+    cm &= valid_mask(g, J);
+    // the lane's candidates, one at a time from L1/L2 (rare: kept out of the unrolled code)
+    const uint8_t* text = g.abase + g.amis;
+    while (cm) {
+      const int k = __ffs(cm) - 1;
+      cm &= cm - 1;
+      const uint8_t* w = text + (J + k - (int64_t)g.amis) - M + 1;  // window start
+      bool hit = true;
+      if constexpr (M > 24) {  // low 32 bits agree; confirm the whole hash
+        uint64_t h = 0;
+        for (int i = 0; i < M; ++i) h = (h << 1) + w[i];
+        hit = (h == a.hx);
+      }
+      if (hit) {
+        ++r.hits;
+        bool eq = true;
+        for (int i = 0; i < M; ++i) eq &= (w[i] == a.pattern[i]);
+        if (eq) r.hm |= 1u << k;
       }
     }
   }
@@ -148,11 +143,6 @@ constexpr int kShortInline = 9;
 // beats the exact roll from M = 17 (measured: m = 20 4.78 vs 4.27 TB/s, m = 16 4.27 vs 4.35).
 constexpr int kFoldFilter = 17;
 
-// byte i of lb ++ v (i static after unrolling)
-__device__ __forceinline__ uint32_t b64(const uint32_t (&lb)[8], const Vec32& v, int i) {
-  return i < 32 ? bsel(lb[i >> 2], i & 3) : bsel(v.w[(i - 32) >> 2], i & 3);
-}
-
 // word (4 bytes) of lb ++ v starting at byte p (static after unrolling; p + 4 <= 64)
 __device__ __forceinline__ uint32_t w64(const uint32_t (&lb)[8], const Vec32& v, int p) {
   const int q = p >> 2, r = p & 3;
@@ -160,29 +150,6 @@ __device__ __forceinline__ uint32_t w64(const uint32_t (&lb)[8], const Vec32& v,
   if (r == 0) return lo;
   const uint32_t hi = (q + 1) < 8 ? lb[q + 1] : ((q + 1) < 16 ? v.w[q + 1 - 8] : 0u);
   return __funnelshift_r(lo, hi, 8 * r);
-}
-
-// bytes [s, s+M) of lb ++ v equal the pattern (word compares via funnel shifts)
-template <int M>
-__device__ __forceinline__ bool window_eq(const uint32_t (&lb)[8], const Vec32& v, int s,
-                                          const PatWords& pw) {
-  bool eq = true;
-#pragma unroll
-  for (int q = 0; q < (M + 3) / 4; ++q) {
-    const int rem = M - 4 * q;
-    const uint32_t mask = rem >= 4 ? 0xffffffffu : ((1u << (8 * rem)) - 1u);
-    uint32_t w;
-    if (s + 4 * q + 4 <= 64) {
-      w = w64(lb, v, s + 4 * q);
-    } else {  // last partial word at the end of the array
-      w = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-        if (s + 4 * q + b < 64) w |= b64(lb, v, s + 4 * q + b) << (8 * b);
-    }
-    eq &= ((w ^ pw.w[q]) & mask) == 0u;
-  }
-  return eq;
 }
 
 // dp4a weights of window bytes [4q, 4q+4) in the hash of an M-byte window (M <= 8):
