@@ -140,8 +140,9 @@ __device__ __forceinline__ SlowOut slow_chunk(const ScanArgs& a, int64_t J) {
 constexpr int kShortInline = 9;
 // From this length on, M < 32 filters with the 32-byte fold (see rk_scan_kernel): one
 // false positive per 2^M windows sends ~1 KiB/2^(M-10) of chunks to the exact pass, which
-// beats the exact roll from M = 17 (measured: m = 20 4.78 vs 4.27 TB/s, m = 16 4.27 vs 4.35).
-constexpr int kFoldFilter = 17;
+// beats the exact roll from M = 15 (measured: m = 20 4.74 vs 4.27 TB/s, m = 15 4.54 vs 4.3,
+// m = 14 4.27 vs 4.3).
+constexpr int kFoldFilter = 15;
 
 // word (4 bytes) of lb ++ v starting at byte p (static after unrolling; p + 4 <= 64)
 __device__ __forceinline__ uint32_t w64(const uint32_t (&lb)[8], const Vec32& v, int p) {
@@ -318,7 +319,9 @@ __global__ void __launch_bounds__(kBlock, 3) rk_scan_kernel(const ScanArgs a) {
       // the 32-byte fold S(j) agrees with the window hash mod 2^M (the out-term is a
       // multiple of 2^M), so the m >= 32 chain with a masked compare is an exact-hit
       // filter (false positives ~2^-M per window); flagged chunks get the exact pass
-      const uint32_t mask = (1u << M) - 1u;  // (M = 16 would compile to PRMT extracts)
+      // (a literal 0xffff would be matched to PRMT half-word extracts instead of one
+      // predicate-producing LOP3, so M = 16 takes it from a kernel argument)
+      const uint32_t mask = M == 16 ? ~a.g.K.negpow : (1u << M) - 1u;
       const auto fpred = [T, mask](uint32_t L) { return ((L ^ T) & mask) == 0u; };
       uint32_t cand = 0;
       stream_tile<32>(a.g, R, S, t, lane,
