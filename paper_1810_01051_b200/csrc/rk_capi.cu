@@ -130,6 +130,23 @@ class CopyPool {
 
 }  // namespace
 
+// A pattern set's device layout (offsets into the context's blob) and its sweeps.
+struct MultiPlan {
+  struct Group {
+    uint32_t m, P, tsize;
+    uint64_t pats, phash, order, gidx, table, filter;
+  };
+  struct Sweep {
+    std::vector<uint32_t> groups;  // ascending lengths
+    uint32_t qmode = 0, qwords = 0;
+    uint64_t qfilter = 0;  // blob offset of the sweep's q-gram filter (qmode > 0)
+  };
+  std::vector<uint8_t> key;  // P, lengths, hashes, pattern bytes
+  std::vector<Group> groups;
+  std::vector<Sweep> sweeps;
+};
+constexpr uint64_t kMultiPrefix = 4096;  // pairs fetched with the count in one round trip
+
 struct rk_ctx {
   int device = 0;
   int num_sms = 0;
@@ -172,7 +189,10 @@ struct rk_ctx {
   // multi-pattern tables
   uint8_t* d_mblob = nullptr;  // every length group's patterns, hashes and tables
   uint64_t mblob_cap = 0;
-  uint32_t* d_qfilter = nullptr;
+  uint8_t* h_mstage = nullptr;  // pinned staging of the blob
+  uint64_t h_mstage_cap = 0;
+  unsigned long long* h_mresult = nullptr;  // pinned: count, kMultiPrefix offsets, indices
+  MultiPlan mplan;              // the last pattern set's plan (cache key + layout)
   std::mutex mu;
 };
 
@@ -400,6 +420,150 @@ int read_counters(rk_ctx* c, uint64_t* matches, uint64_t* collisions, uint64_t* 
 
 }  // namespace
 
+// Builds (or reuses) the device tables of a pattern set: every length group's patterns,
+// hashes, key table and filter, plus one q-gram filter per sweep, in one device blob.
+// The plan is cached per context: repeating a search with the same set uploads nothing.
+int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, uint32_t P,
+               const uint64_t* h_hashes, cudaStream_t s) {
+  std::vector<uint8_t> key(sizeof(uint32_t) + P * (sizeof(uint32_t) + sizeof(uint64_t)));
+  uint64_t total = 0;
+  for (uint32_t i = 0; i < P; ++i) total += h_lengths[i];
+  memcpy(key.data(), &P, 4);
+  memcpy(key.data() + 4, h_lengths, 4ull * P);
+  memcpy(key.data() + 4 + 4ull * P, h_hashes, 8ull * P);
+  key.insert(key.end(), h_patterns, h_patterns + total);
+  if (c->d_mblob && key == c->mplan.key) return RK_OK;
+
+  MultiPlan plan;
+  std::vector<uint64_t> first_byte(P + 1, 0);
+  for (uint32_t i = 0; i < P; ++i) first_byte[i + 1] = first_byte[i] + h_lengths[i];
+  std::map<uint32_t, std::vector<uint32_t>> by_len;
+  for (uint32_t i = 0; i < P; ++i) by_len[h_lengths[i]].push_back(i);
+
+  std::vector<uint8_t> blob;
+  auto reserve = [&blob](uint64_t bytes) {
+    const uint64_t off = (blob.size() + 15) & ~(uint64_t)15;
+    blob.resize(off + bytes, 0);
+    return off;
+  };
+  for (const auto& [m, members] : by_len) {
+    MultiPlan::Group b{};
+    b.m = m;
+    b.P = (uint32_t)members.size();
+    std::vector<std::pair<uint32_t, uint32_t>> keyed(b.P);
+    for (uint32_t i = 0; i < b.P; ++i) keyed[i] = {(uint32_t)h_hashes[members[i]], i};
+    std::stable_sort(keyed.begin(), keyed.end(),
+                     [](const auto& x, const auto& y) { return x.first < y.first; });
+    std::vector<uint32_t> order(b.P);
+    std::vector<std::pair<uint32_t, uint32_t>> runs;  // (key, first << 13 | count)
+    for (uint32_t i = 0; i < b.P;) {
+      uint32_t j = i;
+      while (j < b.P && keyed[j].first == keyed[i].first) {
+        order[j] = keyed[j].second;
+        ++j;
+      }
+      runs.push_back({keyed[i].first, (i << 13) | (j - i)});
+      i = j;
+    }
+    b.tsize = 64;
+    while (b.tsize < 2 * runs.size()) b.tsize <<= 1;
+    b.pats = reserve((uint64_t)b.P * m);
+    b.phash = reserve((uint64_t)b.P * sizeof(uint64_t));
+    b.order = reserve((uint64_t)b.P * sizeof(uint32_t));
+    b.gidx = reserve((uint64_t)b.P * sizeof(uint32_t));
+    b.table = reserve((uint64_t)b.tsize * sizeof(uint2));
+    b.filter = reserve(kMultiFilterWords * sizeof(uint32_t));
+    uint8_t* base = blob.data();
+    for (uint32_t i = 0; i < b.P; ++i) {
+      memcpy(base + b.pats + (uint64_t)i * m, h_patterns + first_byte[members[i]], m);
+      memcpy(base + b.phash + 8ull * i, &h_hashes[members[i]], 8);
+      memcpy(base + b.gidx + 4ull * i, &members[i], 4);
+    }
+    memcpy(base + b.order, order.data(), 4ull * b.P);
+    uint2* table = reinterpret_cast<uint2*>(base + b.table);
+    uint32_t* filter = reinterpret_cast<uint32_t*>(base + b.filter);
+    for (uint32_t t = 0; t < b.tsize; ++t) table[t] = make_uint2(0u, kMultiEmpty);
+    for (const auto& r : runs) {
+      uint32_t slot = (r.first * 0x9E3779B1u) & (b.tsize - 1);
+      while (table[slot].y != kMultiEmpty) slot = (slot + 1) & (b.tsize - 1);
+      table[slot] = make_uint2(r.first, r.second);
+      const uint32_t bit = (r.first * 0x9E3779B1u) >> 16;
+      filter[bit >> 5] |= 1u << (bit & 31);
+    }
+    plan.groups.push_back(b);
+  }
+
+  // sweeps: each length < 7 alone (per-window filter); lengths >= 7 in runs of
+  // kMultiMaxGroups sharing one q-gram filter
+  size_t gi = 0;
+  for (; gi < plan.groups.size() && plan.groups[gi].m < 7; ++gi) {
+    MultiPlan::Sweep sw{};
+    sw.groups = {(uint32_t)gi};
+    plan.sweeps.push_back(sw);
+  }
+  for (; gi < plan.groups.size(); gi += kMultiMaxGroups) {
+    const size_t g_end = std::min(plan.groups.size(), gi + kMultiMaxGroups);
+    MultiPlan::Sweep sw{};
+    for (size_t k = gi; k < g_end; ++k) sw.groups.push_back((uint32_t)k);
+    const uint32_t m_min = plan.groups[gi].m;
+    // (s, q = 4 * qwords) from the shortest length (q + s - 1 <= m_min) and the
+    // alphabet: rich alphabets (>= 20 distinct pattern bytes) filter well with 8-byte
+    // q-grams every 8 bytes; small ones (DNA) need longer q-grams
+    bool seen[256] = {};
+    uint32_t distinct = 0;
+    for (size_t k = gi; k < g_end; ++k)
+      for (uint64_t i = 0; i < (uint64_t)plan.groups[k].P * plan.groups[k].m; ++i) {
+        const uint8_t byte = blob[plan.groups[k].pats + i];
+        if (!seen[byte]) {
+          seen[byte] = true;
+          ++distinct;
+        }
+      }
+    if (m_min >= 23 && distinct < 20) sw.qmode = 8, sw.qwords = 4;
+    else if (m_min >= 15 && distinct < 20) sw.qmode = 4, sw.qwords = 3;
+    else if (m_min >= 15) sw.qmode = 8, sw.qwords = 2;
+    else if (m_min >= 11) sw.qmode = 4, sw.qwords = 2;
+    else sw.qmode = 4, sw.qwords = 1;
+    sw.qfilter = reserve(kQFilterWords * sizeof(uint32_t));
+    uint32_t* qf = reinterpret_cast<uint32_t*>(blob.data() + sw.qfilter);
+    for (size_t k = gi; k < g_end; ++k)
+      for (uint32_t i = 0; i < plan.groups[k].P; ++i) {
+        const uint8_t* p = blob.data() + plan.groups[k].pats + (uint64_t)i * plan.groups[k].m;
+        for (uint32_t j = 0; j < sw.qmode; ++j) {
+          uint32_t w[4] = {0, 0, 0, 0};
+          memcpy(w, p + j, 4 * sw.qwords);
+          uint32_t i1 = 0, i2 = 0;
+          switch (sw.qwords) {
+            case 4: qgram_bits<4>(w, i1, i2); break;
+            case 3: qgram_bits<3>(w, i1, i2); break;
+            case 2: qgram_bits<2>(w, i1, i2); break;
+            default: qgram_bits<1>(w, i1, i2); break;
+          }
+          qf[i1 >> 5] |= 1u << (i1 & 31);
+          qf[i2 >> 5] |= 1u << (i2 & 31);
+        }
+      }
+    plan.sweeps.push_back(sw);
+  }
+
+  // one pinned-staged upload of the whole blob
+  if (int r = grow(&c->d_mblob, &c->mblob_cap, (uint64_t)blob.size(), false, s)) return r;
+  if (c->h_mstage_cap < blob.size()) {
+    RK_CUDA(cudaStreamSynchronize(s));
+    if (c->h_mstage) cudaFreeHost(c->h_mstage);
+    c->h_mstage = nullptr;
+    RK_CUDA(cudaMallocHost(&c->h_mstage, blob.size()));
+    c->h_mstage_cap = blob.size();
+  } else {
+    RK_CUDA(cudaStreamSynchronize(s));  // the staging buffer may still feed a previous upload
+  }
+  memcpy(c->h_mstage, blob.data(), blob.size());
+  RK_CUDA(cudaMemcpyAsync(c->d_mblob, c->h_mstage, blob.size(), cudaMemcpyHostToDevice, s));
+  plan.key = std::move(key);
+  c->mplan = std::move(plan);
+  return RK_OK;
+}
+
 extern "C" {
 
 const char* rk_version(void) { return "rkb200 0.1.0 sm_100a"; }
@@ -433,6 +597,8 @@ int rk_ctx_create(int device, rk_ctx_t** out) {
   c->num_sms = prop.multiProcessorCount;
   RK_CUDA(cudaMalloc(&c->d_mcount, sizeof(unsigned long long)));
   RK_CUDA(cudaMallocHost(&c->h_counters, 4 * sizeof(unsigned long long)));
+  RK_CUDA(cudaMallocHost(&c->h_mresult, (1 + kMultiPrefix) * sizeof(unsigned long long) +
+                                            kMultiPrefix * sizeof(uint32_t)));
   RK_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
   RK_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
   for (auto& e : c->ev_copied) RK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -460,7 +626,8 @@ int rk_ctx_destroy(rk_ctx_t* c) {
   cudaStreamDestroy(c->s_copy);
   cudaStreamDestroy(c->s_comp);
   cudaFree(c->d_mblob);
-  cudaFree(c->d_qfilter);
+  cudaFreeHost(c->h_mstage);
+  cudaFreeHost(c->h_mresult);
   delete c;
   return RK_OK;
 }
@@ -693,82 +860,19 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
   DeviceGuard dg(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   *pairs = 0;
-
-  // ---- length groups (ascending m) of the patterns that have windows in the text
-  std::vector<uint64_t> first_byte(P + 1, 0);
-  for (uint32_t i = 0; i < P; ++i) first_byte[i + 1] = first_byte[i] + h_lengths[i];
-  std::map<uint32_t, std::vector<uint32_t>> by_len;
-  for (uint32_t i = 0; i < P; ++i)
-    if (h_lengths[i] <= n) by_len[h_lengths[i]].push_back(i);
-  if (by_len.empty()) return RK_OK;
-  if (!d_text) return fail(RK_EINVAL, "text pointer is NULL");
-
-  // ---- host build of every group's tables in one blob (one upload):
-  //      pats | phash | order | gidx | table | filter, 16-byte aligned sections
-  struct Built {
-    uint32_t m, P, tsize;
-    uint64_t pats, phash, order, gidx, table, filter;  // blob offsets
-  };
-  std::vector<Built> built;
-  std::vector<uint8_t> blob;
-  auto reserve = [&blob](uint64_t bytes) {
-    const uint64_t off = (blob.size() + 15) & ~(uint64_t)15;
-    blob.resize(off + bytes, 0);
-    return off;
-  };
-  for (const auto& [m, members] : by_len) {
-    Built b{};
-    b.m = m;
-    b.P = (uint32_t)members.size();
-    std::vector<std::pair<uint32_t, uint32_t>> keyed(b.P);
-    for (uint32_t i = 0; i < b.P; ++i) keyed[i] = {(uint32_t)h_hashes[members[i]], i};
-    std::stable_sort(keyed.begin(), keyed.end(),
-                     [](const auto& x, const auto& y) { return x.first < y.first; });
-    std::vector<uint32_t> order(b.P);
-    std::vector<std::pair<uint32_t, uint32_t>> runs;  // (key, first << 13 | count)
-    for (uint32_t i = 0; i < b.P;) {
-      uint32_t j = i;
-      while (j < b.P && keyed[j].first == keyed[i].first) {
-        order[j] = keyed[j].second;
-        ++j;
-      }
-      runs.push_back({keyed[i].first, (i << 13) | (j - i)});
-      i = j;
-    }
-    b.tsize = 64;
-    while (b.tsize < 2 * runs.size()) b.tsize <<= 1;
-    b.pats = reserve((uint64_t)b.P * m);
-    b.phash = reserve((uint64_t)b.P * sizeof(uint64_t));
-    b.order = reserve((uint64_t)b.P * sizeof(uint32_t));
-    b.gidx = reserve((uint64_t)b.P * sizeof(uint32_t));
-    b.table = reserve((uint64_t)b.tsize * sizeof(uint2));
-    b.filter = reserve(kMultiFilterWords * sizeof(uint32_t));
-    uint8_t* base = blob.data();
-    for (uint32_t i = 0; i < b.P; ++i) {
-      memcpy(base + b.pats + (uint64_t)i * m, h_patterns + first_byte[members[i]], m);
-      memcpy(base + b.phash + 8ull * i, &h_hashes[members[i]], 8);
-      memcpy(base + b.gidx + 4ull * i, &members[i], 4);
-    }
-    memcpy(base + b.order, order.data(), 4ull * b.P);
-    uint2* table = reinterpret_cast<uint2*>(base + b.table);
-    uint32_t* filter = reinterpret_cast<uint32_t*>(base + b.filter);
-    for (uint32_t t = 0; t < b.tsize; ++t) table[t] = make_uint2(0u, kMultiEmpty);
-    for (const auto& r : runs) {
-      uint32_t slot = (r.first * 0x9E3779B1u) & (b.tsize - 1);
-      while (table[slot].y != kMultiEmpty) slot = (slot + 1) & (b.tsize - 1);
-      table[slot] = make_uint2(r.first, r.second);
-      const uint32_t bit = (r.first * 0x9E3779B1u) >> 16;
-      filter[bit >> 5] |= 1u << (bit & 31);
-    }
-    built.push_back(b);
+  uint64_t max_len = 0, min_len = ~0ull;
+  for (uint32_t i = 0; i < P; ++i) {
+    max_len = std::max<uint64_t>(max_len, h_lengths[i]);
+    min_len = std::min<uint64_t>(min_len, h_lengths[i]);
   }
-  if (int r = grow(&c->d_mblob, &c->mblob_cap, (uint64_t)blob.size(), false, s)) return r;
-  if (!c->d_qfilter) RK_CUDA(cudaMalloc(&c->d_qfilter, kQFilterWords * sizeof(uint32_t)));
-  RK_CUDA(cudaMemcpyAsync(c->d_mblob, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
+  if (min_len > n) return RK_OK;  // no pattern has a window
+  if (!d_text) return fail(RK_EINVAL, "text pointer is NULL");
+  if (int r = multi_plan(c, h_patterns, h_lengths, P, h_hashes, s)) return r;
+  const MultiPlan& plan = c->mplan;
   RK_CUDA(cudaMemsetAsync(c->d_mcount, 0, sizeof(unsigned long long), s));
 
   const uint8_t* dev = c->d_mblob;
-  auto group_of = [&](const Built& b, uint64_t amis) {
+  auto group_of = [&](const MultiPlan::Group& b, uint64_t amis) {
     MultiGroup G{};
     G.pats = dev + b.pats;
     G.phash = reinterpret_cast<const uint64_t*>(dev + b.phash);
@@ -781,123 +885,88 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
     G.tsize = b.tsize;
     return G;
   };
-  auto launch = [&](MultiArgs& p, const Geometry& gg, uint32_t m) -> int {
-    p.g = text_geom(gg, n, m, 0);
+  for (const MultiPlan::Sweep& sw : plan.sweeps) {
+    // lengths longer than the text have no windows: drop them from the sweep
+    std::vector<const MultiPlan::Group*> live;
+    for (uint32_t gi : sw.groups)
+      if (plan.groups[gi].m <= n) live.push_back(&plan.groups[gi]);
+    if (live.empty()) continue;
+    const uint32_t m_min = live.front()->m;
+    const uint64_t nw = n - m_min + 1;
+    Geometry gg = geometry(d_text, m_min, 0, nw);
+    MultiArgs p{};
+    p.qmode = sw.qmode;
+    p.qwords = sw.qwords;
+    if (sw.qmode) {
+      // tiles over the anchors e (q-gram ends): [first start + q - 1, last start of the
+      // shortest length + q - 1 + s), clamped to the text
+      const uint64_t q = 4ull * sw.qwords;
+      gg.ja_lo = gg.amis + q - 1;
+      gg.ja_hi = std::min<uint64_t>(gg.amis + nw - 1 + q - 1 + sw.qmode, gg.amis + n);
+      gg.tile_first = gg.ja_lo / kTile;
+      gg.num_tiles = (gg.ja_hi - 1) / kTile - gg.tile_first + 1;
+      p.qfilter = reinterpret_cast<const uint32_t*>(dev + sw.qfilter);
+    }
+    p.G = (uint32_t)live.size();
+    for (size_t k = 0; k < live.size(); ++k) p.grp[k] = group_of(*live[k], gg.amis);
+    p.g = text_geom(gg, n, m_min, 0);
     p.ys_lo = gg.amis;
     p.out_off = d_off;
     p.out_idx = d_idx;
     p.cap = cap;
     p.counters = c->d_mcount;
     const uint64_t grid = std::max<uint64_t>(
-        1, std::min<uint64_t>((uint64_t)c->num_sms * multi_blocks_per_sm(p.qmode, m),
+        1, std::min<uint64_t>((uint64_t)c->num_sms * multi_blocks_per_sm(p.qmode, m_min),
                               (gg.num_tiles + kMultiWarps - 1) / kMultiWarps));
     RK_CUDA(launch_multi(p, (int)grid, s));
     ++c->launches;
-    return RK_OK;
-  };
-
-  // ---- m < 7: one launch per length, every window's hash against the group's filter
-  size_t gi = 0;
-  for (; gi < built.size() && built[gi].m < 7; ++gi) {
-    const Built& b = built[gi];
-    Geometry gg = geometry(d_text, b.m, 0, n - b.m + 1);
-    MultiArgs p{};
-    p.qmode = 0;
-    p.G = 1;
-    p.grp[0] = group_of(b, gg.amis);
-    if (int r = launch(p, gg, b.m)) return r;
-  }
-  // ---- m >= 7: up to kMultiMaxGroups lengths per sweep, one shared q-gram filter
-  std::vector<uint32_t> qfilter(kQFilterWords);
-  for (; gi < built.size(); gi += kMultiMaxGroups) {
-    const size_t g_end = std::min(built.size(), gi + kMultiMaxGroups);
-    const uint32_t m_min = built[gi].m;
-    // (s, q = 4 * qwords) from the shortest length (q + s - 1 <= m_min) and the
-    // alphabet: rich alphabets (>= 20 distinct pattern bytes) filter well with 8-byte
-    // q-grams every 8 bytes; small ones (DNA) need longer q-grams
-    bool seen[256] = {};
-    uint32_t distinct = 0;
-    for (size_t k = gi; k < g_end; ++k)
-      for (uint64_t i = 0; i < (uint64_t)built[k].P * built[k].m; ++i) {
-        const uint8_t byte = blob[built[k].pats + i];
-        if (!seen[byte]) {
-          seen[byte] = true;
-          ++distinct;
-        }
-      }
-    uint32_t qmode, qwords;
-    if (m_min >= 23 && distinct < 20) qmode = 8, qwords = 4;
-    else if (m_min >= 15 && distinct < 20) qmode = 4, qwords = 3;
-    else if (m_min >= 15) qmode = 8, qwords = 2;
-    else if (m_min >= 11) qmode = 4, qwords = 2;
-    else qmode = 4, qwords = 1;
-    std::fill(qfilter.begin(), qfilter.end(), 0u);
-    for (size_t k = gi; k < g_end; ++k)
-      for (uint32_t i = 0; i < built[k].P; ++i) {
-        const uint8_t* p = blob.data() + built[k].pats + (uint64_t)i * built[k].m;
-        for (uint32_t j = 0; j < qmode; ++j) {
-          uint32_t w[4] = {0, 0, 0, 0};
-          memcpy(w, p + j, 4 * qwords);
-          uint32_t i1 = 0, i2 = 0;
-          switch (qwords) {
-            case 4: qgram_bits<4>(w, i1, i2); break;
-            case 3: qgram_bits<3>(w, i1, i2); break;
-            case 2: qgram_bits<2>(w, i1, i2); break;
-            default: qgram_bits<1>(w, i1, i2); break;
-          }
-          qfilter[i1 >> 5] |= 1u << (i1 & 31);
-          qfilter[i2 >> 5] |= 1u << (i2 & 31);
-        }
-      }
-    // pageable source: the call returns once the bytes are staged, so the vector may be
-    // refilled for the next sweep (which is ordered after this one on the stream)
-    RK_CUDA(cudaMemcpyAsync(c->d_qfilter, qfilter.data(), kQFilterWords * sizeof(uint32_t),
-                            cudaMemcpyHostToDevice, s));
-    // tiles over the anchors e (q-gram ends): [first start + q - 1, last start of the
-    // shortest length + q - 1 + s), clamped to the text
-    const uint64_t nw = n - m_min + 1;
-    Geometry gg = geometry(d_text, m_min, 0, nw);
-    const uint64_t q = 4ull * qwords;
-    gg.ja_lo = gg.amis + q - 1;
-    gg.ja_hi = std::min<uint64_t>(gg.amis + nw - 1 + q - 1 + qmode, gg.amis + n);
-    gg.tile_first = gg.ja_lo / kTile;
-    gg.num_tiles = (gg.ja_hi - 1) / kTile - gg.tile_first + 1;
-    MultiArgs p{};
-    p.qfilter = c->d_qfilter;
-    p.qmode = qmode;
-    p.qwords = qwords;
-    p.G = (uint32_t)(g_end - gi);
-    for (size_t k = gi; k < g_end; ++k) p.grp[k - gi] = group_of(built[k], gg.amis);
-    if (int r = launch(p, gg, m_min)) return r;
   }
 
-  RK_CUDA(cudaMemcpyAsync(c->h_counters, c->d_mcount, sizeof(unsigned long long),
+  // the count and a prefix of the pairs come back in one round trip; the host orders
+  // them by (pattern index, offset) -- the reference's per-pattern ascending lists -- and
+  // writes them back (stream-ordered, so the caller sees them in its next operation)
+  const uint64_t pre = std::min<uint64_t>(cap, kMultiPrefix);
+  RK_CUDA(cudaMemcpyAsync(c->h_mresult, c->d_mcount, sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, s));
+  if (pre) {
+    RK_CUDA(cudaMemcpyAsync(c->h_mresult + 1, d_off, pre * sizeof(int64_t),
+                            cudaMemcpyDeviceToHost, s));
+    RK_CUDA(cudaMemcpyAsync(c->h_mresult + 1 + kMultiPrefix, d_idx, pre * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, s));
+  }
   RK_CUDA(cudaStreamSynchronize(s));
-  const uint64_t total = c->h_counters[0];
+  const uint64_t total = c->h_mresult[0];
   *pairs = total;
-  // order by (pattern index, offset): the reference's per-pattern ascending lists
   const uint64_t k = std::min(total, cap);
   if (k > 1) {
     std::vector<int64_t> off(k);
     std::vector<uint32_t> idx(k);
-    RK_CUDA(cudaMemcpyAsync(off.data(), d_off, k * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    RK_CUDA(cudaMemcpyAsync(idx.data(), d_idx, k * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    RK_CUDA(cudaStreamSynchronize(s));
+    if (k <= pre) {
+      memcpy(off.data(), c->h_mresult + 1, k * sizeof(int64_t));
+      memcpy(idx.data(), c->h_mresult + 1 + kMultiPrefix, k * sizeof(uint32_t));
+    } else {
+      RK_CUDA(cudaMemcpyAsync(off.data(), d_off, k * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      RK_CUDA(cudaMemcpyAsync(idx.data(), d_idx, k * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      RK_CUDA(cudaStreamSynchronize(s));
+    }
     std::vector<uint64_t> perm(k);
     for (uint64_t i = 0; i < k; ++i) perm[i] = i;
     std::sort(perm.begin(), perm.end(), [&](uint64_t x, uint64_t y) {
       return idx[x] != idx[y] ? idx[x] < idx[y] : off[x] < off[y];
     });
-    std::vector<int64_t> off2(k);
-    std::vector<uint32_t> idx2(k);
-    for (uint64_t i = 0; i < k; ++i) {
-      off2[i] = off[perm[i]];
-      idx2[i] = idx[perm[i]];
+    bool sorted = true;
+    for (uint64_t i = 0; i < k && sorted; ++i) sorted = perm[i] == i;
+    if (!sorted) {
+      std::vector<int64_t> off2(k);
+      std::vector<uint32_t> idx2(k);
+      for (uint64_t i = 0; i < k; ++i) {
+        off2[i] = off[perm[i]];
+        idx2[i] = idx[perm[i]];
+      }
+      // pageable sources: each call returns once its bytes are staged
+      RK_CUDA(cudaMemcpyAsync(d_off, off2.data(), k * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      RK_CUDA(cudaMemcpyAsync(d_idx, idx2.data(), k * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
     }
-    RK_CUDA(cudaMemcpyAsync(d_off, off2.data(), k * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    RK_CUDA(cudaMemcpyAsync(d_idx, idx2.data(), k * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-    RK_CUDA(cudaStreamSynchronize(s));
   }
   return RK_OK;
 }

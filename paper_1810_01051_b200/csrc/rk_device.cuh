@@ -39,8 +39,6 @@ constexpr int kMaxDevices = 64;
 // before its first chunk (the lookback the first lane needs).
 constexpr int kStageChunks = 4;
 constexpr int kStages = 2;
-constexpr int kStageBytes = kStageChunks * kChunk + 32;  // 4128 (multiple of 16)
-constexpr int kStagesPerTile = kTileChunks / kStageChunks;
 static_assert(kTileChunks % kStageChunks == 0, "stage/tile");
 
 struct Vec32 {
@@ -234,16 +232,23 @@ __device__ __forceinline__ bool fast_chunk(const Vec32& v, const uint32_t (&lb)[
 }
 
 // ------------------------------------------------------------------------- TMA ring
-struct __align__(16) WarpRing {
-  uint8_t buf[kStages][kStageBytes];
+// SC = chunks per stage (the scan kernels use kStageChunks; the multi-pattern kernel,
+// which runs twice the warps per SM, half that).
+template <int SC>
+struct __align__(16) WarpRingT {
+  static constexpr int kChunks = SC;
+  static constexpr int kBytes = SC * kChunk + 32;  // stage + its 32-byte lookback
+  uint8_t buf[kStages][kBytes];
   unsigned long long bar[kStages];
 };
+using WarpRing = WarpRingT<kStageChunks>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-__device__ __forceinline__ void ring_init(WarpRing* R, int lane) {
+template <int SC>
+__device__ __forceinline__ void ring_init(WarpRingT<SC>* R, int lane) {
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s)
@@ -300,21 +305,24 @@ __device__ __forceinline__ void stream_seek(const TextGeom& g, Stream& S) {
   S.psrc = g.abase + g.tile_a(S.pt) - 32;
 }
 
-__device__ __forceinline__ void stream_issue(WarpRing* R, Stream& S, int lane) {
+template <int SC>
+__device__ __forceinline__ void stream_issue(WarpRingT<SC>* R, Stream& S, int lane) {
   if (S.pt >= S.ntiles || S.pt >= S.int_hi) return;
-  if (lane == 0) bulk_g2s(R->buf[S.pslot], S.psrc, kStageBytes, &R->bar[S.pslot]);
+  if (lane == 0) bulk_g2s(R->buf[S.pslot], S.psrc, WarpRingT<SC>::kBytes, &R->bar[S.pslot]);
   S.pslot = (S.pslot + 1) & (kStages - 1);
   ++S.pending;
-  S.psrc += kStageChunks * kChunk;
-  if (++S.ps == kStagesPerTile) {
+  S.psrc += SC * kChunk;
+  if (++S.ps == kTileChunks / SC) {
     S.ps = 0;
     S.pt += S.W;
     S.psrc += S.tile_jump;
   }
 }
 
-__device__ __forceinline__ void stream_init(const TextGeom& g, WarpRing* R, Stream& S, uint32_t w,
-                                            uint32_t W, int lane) {
+template <int SC>
+__device__ __forceinline__ void stream_init(const TextGeom& g, WarpRingT<SC>* R, Stream& S,
+                                            uint32_t w, uint32_t W, int lane) {
+  static_assert(kTileChunks % SC == 0, "stage/tile");
   static_assert((kStages & (kStages - 1)) == 0, "ring size must be a power of two");
   // interior tiles are exactly [int_lo, int_hi): tile_a - 32 >= amis and
   // tile_a + kTile <= amis + n, with tile_a = (tile0 + t) * kTile
@@ -339,8 +347,8 @@ __device__ __forceinline__ void stream_init(const TextGeom& g, WarpRing* R, Stre
 // (window ends [J, J+32)), lb = the 32 bytes before J (M < 32 only), carryS = the fold
 // seed for M >= 32 (see fast_chunk), c = chunk index in the tile.  Interior tiles come
 // from the TMA ring; edge tiles go through the bounds-checked loader.
-template <int M, bool UNROLL = true, class Op>
-__device__ __forceinline__ void stream_tile(const TextGeom& g, WarpRing* R, Stream& S,
+template <int M, bool UNROLL = true, int SC, class Op>
+__device__ __forceinline__ void stream_tile(const TextGeom& g, WarpRingT<SC>* R, Stream& S,
                                             uint32_t t, int lane, Op&& op) {
   const int64_t ta = g.tile_a(t);
   uint32_t carryS = 0;
@@ -349,21 +357,21 @@ __device__ __forceinline__ void stream_tile(const TextGeom& g, WarpRing* R, Stre
   for (int i = 0; i < 8; ++i) lb[i] = 0;
   if (t >= S.int_lo && t < S.int_hi) {
 #pragma unroll 1
-    for (int s = 0; s < kStagesPerTile; ++s) {
+    for (int s = 0; s < kTileChunks / SC; ++s) {
       mbar_wait(&R->bar[S.cslot], S.cphase);
       const uint8_t* st = R->buf[S.cslot];
       if constexpr (M >= 32) {
         if (s == 0) carryS = fold32(lds32(st).w);  // tile lookback, broadcast read
       }
-#pragma unroll(UNROLL ? kStageChunks : 1)
-      for (int j = 0; j < kStageChunks; ++j) {
+#pragma unroll(UNROLL ? SC : 1)
+      for (int j = 0; j < SC; ++j) {
         const Vec32 v = lds32(st + 32 + j * kChunk + lane * kR);
         if constexpr (M < 32) {
           const Vec32 l = lds32(st + j * kChunk + lane * kR);
 #pragma unroll
           for (int i = 0; i < 8; ++i) lb[i] = l.w[i];
         }
-        const int c = s * kStageChunks + j;
+        const int c = s * SC + j;
         op(v, lb, carryS, ta + c * kChunk + lane * kR, c);
       }
       // the slot's bytes are consumed: hand it back to the producer
@@ -390,8 +398,8 @@ __device__ __forceinline__ void stream_tile(const TextGeom& g, WarpRing* R, Stre
 }
 
 // Fast pass over tile t: bitmask of its chunks in which some lane saw pred() hold.
-template <int M, bool UNROLL = true, class Pred>
-__device__ __forceinline__ uint32_t fast_tile(const TextGeom& g, WarpRing* R, Stream& S,
+template <int M, bool UNROLL = true, int SC, class Pred>
+__device__ __forceinline__ uint32_t fast_tile(const TextGeom& g, WarpRingT<SC>* R, Stream& S,
                                               uint32_t t, int lane, Pred pred) {
   uint32_t cand = 0;
   stream_tile<M, UNROLL>(g, R, S, t, lane,

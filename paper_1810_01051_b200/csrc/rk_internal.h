@@ -72,7 +72,8 @@ struct MultiGroup {
   uint32_t m, tsize;
 };
 constexpr int kMultiMaxGroups = 16;
-constexpr int kMultiWarps = 16;  // one 16-warp CTA per SM shares the 64 KiB q-gram filter  // length groups per sweep (kernel parameter space)
+constexpr int kMultiWarps = 32;      // one 32-warp CTA per SM shares the 64 KiB q-gram filter
+constexpr int kMultiStageChunks = 2;  // 2 KiB TMA stages, so 32 rings fit beside the filter  // length groups per sweep (kernel parameter space)
 
 struct MultiArgs {
   TextGeom g;                 // q-gram mode: tiles cover the anchors (q-gram ends)

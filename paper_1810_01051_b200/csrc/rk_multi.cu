@@ -7,14 +7,14 @@ namespace rkb {
 // Every length >= 7 of the set in one sweep: anchored q-grams against the shared filter.
 __global__ void __launch_bounds__(kMultiBlock) rk_multi_qgram_kernel(const MultiArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  WarpRing* rings = reinterpret_cast<WarpRing*>(smem);
-  uint32_t* sfilter = reinterpret_cast<uint32_t*>(smem + sizeof(WarpRing) * kMultiWarps);
+  MultiRing* rings = reinterpret_cast<MultiRing*>(smem);
+  uint32_t* sfilter = reinterpret_cast<uint32_t*>(smem + sizeof(MultiRing) * kMultiWarps);
   for (int i = threadIdx.x; i < kQFilterWords; i += blockDim.x) sfilter[i] = a.qfilter[i];
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  WarpRing* R = rings + warp;
+  MultiRing* R = rings + warp;
   ring_init(R, lane);
   const uint64_t W = (uint64_t)gridDim.x * kMultiWarps;
   const uint64_t w = (uint64_t)blockIdx.x * kMultiWarps + warp;
@@ -47,7 +47,7 @@ static constexpr MultiOccFn kShortOcc[6] = {
     &multi_short_occupancy<4>, &multi_short_occupancy<5>, &multi_short_occupancy<6>};
 
 size_t multi_smem_bytes() {
-  return sizeof(WarpRing) * kMultiWarps + kQFilterWords * sizeof(uint32_t);
+  return sizeof(MultiRing) * kMultiWarps + kQFilterWords * sizeof(uint32_t);
 }
 
 int multi_blocks_per_sm(uint32_t qmode, uint32_t m) {
@@ -59,7 +59,7 @@ int multi_blocks_per_sm(uint32_t qmode, uint32_t m) {
 
 cudaError_t launch_multi(const MultiArgs& a, int grid, cudaStream_t s) {
   if (a.qmode == 0) return kShortLaunch[a.g.m - 1](a, grid, s);
-  return multi_launch_kernel(rk_multi_qgram_kernel, a, grid, s);
+  return multi_launch_kernel<struct QgramAttr>(rk_multi_qgram_kernel, a, grid, s);
 }
 
 }  // namespace rkb

@@ -4,8 +4,11 @@
 namespace rkb {
 
 template <int M>
+struct rk_multi_short_tag {};
+
+template <int M>
 cudaError_t launch_multi_short(const MultiArgs& a, int grid, cudaStream_t s) {
-  return multi_launch_kernel(rk_multi_short_kernel<M>, a, grid, s);
+  return multi_launch_kernel<rk_multi_short_tag<M>>(rk_multi_short_kernel<M>, a, grid, s);
 }
 
 template <int M>

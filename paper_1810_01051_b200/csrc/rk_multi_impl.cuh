@@ -33,6 +33,7 @@
 namespace rkb {
 
 constexpr int kMultiBlock = 32 * kMultiWarps;
+using MultiRing = WarpRingT<kMultiStageChunks>;
 
 __device__ __forceinline__ uint32_t mhash(uint32_t key) { return key * 0x9E3779B1u; }
 
@@ -190,7 +191,7 @@ __device__ __forceinline__ void multi_check_window(const MultiArgs& a, int64_t y
 // One tile of anchored q-grams (one per SS bytes, ending at e = J + SS*t + SS - 1); a
 // q-gram that passes the filter makes its SS windows candidates, checked by SS lanes at once.
 template <int SS, int QW>
-__device__ __forceinline__ void qgram_tile(const MultiArgs& a, WarpRing* R, Stream& S,
+__device__ __forceinline__ void qgram_tile(const MultiArgs& a, MultiRing* R, Stream& S,
                                            uint32_t t, int lane, const uint32_t* sfilter) {
   constexpr int q = 4 * QW;
   stream_tile<31, false>(
@@ -218,14 +219,14 @@ __device__ __forceinline__ void qgram_tile(const MultiArgs& a, WarpRing* R, Stre
 template <int M>
 __global__ void __launch_bounds__(kMultiBlock) rk_multi_short_kernel(const MultiArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  WarpRing* rings = reinterpret_cast<WarpRing*>(smem);
-  uint32_t* sfilter = reinterpret_cast<uint32_t*>(smem + sizeof(WarpRing) * kMultiWarps);
+  MultiRing* rings = reinterpret_cast<MultiRing*>(smem);
+  uint32_t* sfilter = reinterpret_cast<uint32_t*>(smem + sizeof(MultiRing) * kMultiWarps);
   for (int i = threadIdx.x; i < kMultiFilterWords; i += blockDim.x) sfilter[i] = a.grp[0].filter[i];
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  WarpRing* R = rings + warp;
+  MultiRing* R = rings + warp;
   ring_init(R, lane);
   const uint64_t W = (uint64_t)gridDim.x * kMultiWarps;
   const uint64_t w = (uint64_t)blockIdx.x * kMultiWarps + warp;
@@ -252,12 +253,19 @@ int multi_occupancy(K kernel) {
   return b > 0 ? b : 1;
 }
 
-template <class K>
+// (Attr is a per-kernel tag so each kernel opts in to > 48 KiB of smem once per device.)
+template <class Attr, class K>
 cudaError_t multi_launch_kernel(K kernel, const MultiArgs& a, int grid, cudaStream_t s) {
   const size_t smem = multi_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
+  static bool attr[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= kMaxDevices || !attr[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    if (dev < kMaxDevices) attr[dev] = true;
+  }
   kernel<<<grid, kMultiBlock, smem, s>>>(a);
   return cudaGetLastError();
 }

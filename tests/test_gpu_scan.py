@@ -330,6 +330,16 @@ def test_multi_mixed_lengths_one_sweep(gpu):
                 assert r.offsets == expect[i], (alpha, shift, i, len(ps[i]))
 
 
+def test_multi_plan_cache_keys_on_bytes(gpu):
+    """The per-context plan cache must not confuse sets that differ only in pattern bytes
+    (equal lengths and hashes: "ac" / "ba", tests/test_matcher.py:139-146 of the reference)."""
+    text = b"xacbaacxbaba" * 50
+    for pats in (["ac"], ["ba"], ["ac"], ["acbaacxb", "baacxbab"], ["baacxbab", "acbaacxb"]):
+        out = rk.search_multi(text, [p.encode() if isinstance(p, str) else p for p in pats])
+        for i, r in out:
+            assert r == rk.search_naive(text, pats[i].encode()), (pats, i)
+
+
 def test_multi_4096_patterns(gpu):
     rng = np.random.default_rng(78)
     text = rng.integers(0, 256, 1 << 20, dtype=np.uint8)
