@@ -532,15 +532,16 @@ int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, 
         for (uint32_t j = 0; j < sw.qmode; ++j) {
           uint32_t w[4] = {0, 0, 0, 0};
           memcpy(w, p + j, 4 * sw.qwords);
-          uint32_t i1 = 0, i2 = 0;
+          uint32_t h = 0;
           switch (sw.qwords) {
-            case 4: qgram_bits<4>(w, i1, i2); break;
-            case 3: qgram_bits<3>(w, i1, i2); break;
-            case 2: qgram_bits<2>(w, i1, i2); break;
-            default: qgram_bits<1>(w, i1, i2); break;
+            case 4: h = qgram_hash<4>(w); break;
+            case 3: h = qgram_hash<3>(w); break;
+            case 2: h = qgram_hash<2>(w); break;
+            default: h = qgram_hash<1>(w); break;
           }
-          qf[i1 >> 5] |= 1u << (i1 & 31);
-          qf[i2 >> 5] |= 1u << (i2 & 31);
+          uint32_t* blk = qf + 2 * (h >> 19);
+          blk[0] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31));
+          blk[1] |= (1u << ((h >> 10) & 31)) | (1u << ((h >> 15) & 31));
         }
       }
     plan.sweeps.push_back(sw);

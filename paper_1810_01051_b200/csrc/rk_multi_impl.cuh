@@ -15,8 +15,8 @@
 //     e + 1 = 0 mod s.  Every occurrence of a pattern p at y contains exactly one anchored
 //     q-gram: the q bytes ending at the first anchor e >= y + q - 1, which are p[j:j+q]
 //     with j = e-q+1-y < s (so q + s - 1 <= m; (s, q) follow the group's shortest
-//     length).  All such pattern q-grams go into a 2^19-bit 2-probe Bloom filter (64 KiB)
-//     in shared memory; the fast pass tests one word-aligned q-gram per s bytes straight
+//     length).  All such pattern q-grams go into a 64 KiB blocked Bloom filter (one
+//     64-bit block, 4 bits, per q-gram) in shared memory; the fast pass tests one word-aligned q-gram per s bytes straight
 //     from the loaded words (no rolling hash).  A q-gram that hits makes its s window
 //     starts candidates; s lanes of the warp check them at once against every length
 //     group (exact hash + table + bytes), and since each window has one anchor nothing
@@ -44,9 +44,12 @@ __device__ __forceinline__ bool filter_test(const uint32_t* __restrict__ f, uint
 
 template <int QW>
 __device__ __forceinline__ bool qfilter_test(const uint32_t* __restrict__ f, const uint32_t* w) {
-  uint32_t i1, i2;
-  qgram_bits<QW>(w, i1, i2);
-  return ((f[i1 >> 5] >> (i1 & 31)) & (f[i2 >> 5] >> (i2 & 31)) & 1u) != 0u;
+  const uint32_t h = qgram_hash<QW>(w);
+  const uint2 x = reinterpret_cast<const uint2*>(f)[h >> 19];
+  // rotates take the position mod 32: four SHF and two LOP3, no masking
+  const uint32_t r = __funnelshift_r(x.x, x.x, h) & __funnelshift_r(x.x, x.x, h >> 5) &
+                     __funnelshift_r(x.y, x.y, h >> 10) & __funnelshift_r(x.y, x.y, h >> 15);
+  return (r & 1u) != 0u;
 }
 
 // Anchored q-gram tests of one lane (window-end anchors e = J + s*t + s - 1, the q-gram
