@@ -140,6 +140,8 @@ struct MultiPlan {
     std::vector<uint32_t> groups;  // ascending lengths
     uint32_t qmode = 0, qwords = 0;
     uint64_t qfilter = 0;  // blob offset of the sweep's q-gram filter (qmode > 0)
+    uint64_t qmap = 0;     // blob offset of its q-gram -> group-mask table
+    uint32_t qmap_size = 0;
   };
   std::vector<uint8_t> key;  // P, lengths, hashes, pattern bytes
   std::vector<Group> groups;
@@ -525,7 +527,7 @@ int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, 
     else if (m_min >= 11) sw.qmode = 4, sw.qwords = 2;
     else sw.qmode = 4, sw.qwords = 1;
     sw.qfilter = reserve(kQFilterWords * sizeof(uint32_t));
-    uint32_t* qf = reinterpret_cast<uint32_t*>(blob.data() + sw.qfilter);
+    std::unordered_map<uint32_t, uint64_t> groups_of;  // q-gram hash -> group mask
     for (size_t k = gi; k < g_end; ++k)
       for (uint32_t i = 0; i < plan.groups[k].P; ++i) {
         const uint8_t* p = blob.data() + plan.groups[k].pats + (uint64_t)i * plan.groups[k].m;
@@ -539,11 +541,21 @@ int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, 
             case 2: h = qgram_hash<2>(w); break;
             default: h = qgram_hash<1>(w); break;
           }
-          uint32_t* blk = qf + 2 * (h >> 19);
+          uint32_t* blk = reinterpret_cast<uint32_t*>(blob.data() + sw.qfilter) + 2 * (h >> 19);
           blk[0] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31));
           blk[1] |= (1u << ((h >> 10) & 31)) | (1u << ((h >> 15) & 31));
+          groups_of[h] |= 1ull << (k - gi);
         }
       }
+    sw.qmap_size = 64;
+    while (sw.qmap_size < 2 * groups_of.size()) sw.qmap_size <<= 1;
+    sw.qmap = reserve((uint64_t)sw.qmap_size * sizeof(uint4));
+    uint4* qmap = reinterpret_cast<uint4*>(blob.data() + sw.qmap);
+    for (const auto& [h, mask] : groups_of) {
+      uint32_t slot = (h * 0x9E3779B1u) & (sw.qmap_size - 1);
+      while (qmap[slot].z | qmap[slot].w) slot = (slot + 1) & (sw.qmap_size - 1);
+      qmap[slot] = make_uint4(h, 0u, (uint32_t)mask, (uint32_t)(mask >> 32));
+    }
     plan.sweeps.push_back(sw);
   }
 
@@ -881,18 +893,16 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
     G.gidx = reinterpret_cast<const uint32_t*>(dev + b.gidx);
     G.table = reinterpret_cast<const uint2*>(dev + b.table);
     G.filter = reinterpret_cast<const uint32_t*>(dev + b.filter);
-    G.ys_hi = amis + (n - b.m + 1);
+    G.ys_hi = b.m <= n ? amis + (n - b.m + 1) : amis;  // longer than the text: no windows
     G.m = b.m;
     G.tsize = b.tsize;
     return G;
   };
   for (const MultiPlan::Sweep& sw : plan.sweeps) {
-    // lengths longer than the text have no windows: drop them from the sweep
-    std::vector<const MultiPlan::Group*> live;
-    for (uint32_t gi : sw.groups)
-      if (plan.groups[gi].m <= n) live.push_back(&plan.groups[gi]);
-    if (live.empty()) continue;
-    const uint32_t m_min = live.front()->m;
+    // (lengths longer than the text stay in the sweep -- group bits are positions in
+    // it -- with an empty window range)
+    const uint32_t m_min = plan.groups[sw.groups.front()].m;
+    if (m_min > n) continue;
     const uint64_t nw = n - m_min + 1;
     Geometry gg = geometry(d_text, m_min, 0, nw);
     MultiArgs p{};
@@ -907,9 +917,12 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
       gg.tile_first = gg.ja_lo / kTile;
       gg.num_tiles = (gg.ja_hi - 1) / kTile - gg.tile_first + 1;
       p.qfilter = reinterpret_cast<const uint32_t*>(dev + sw.qfilter);
+      p.qmap = reinterpret_cast<const uint4*>(dev + sw.qmap);
+      p.qmap_size = sw.qmap_size;
     }
-    p.G = (uint32_t)live.size();
-    for (size_t k = 0; k < live.size(); ++k) p.grp[k] = group_of(*live[k], gg.amis);
+    p.G = (uint32_t)sw.groups.size();
+    for (size_t k = 0; k < sw.groups.size(); ++k)
+      p.grp[k] = group_of(plan.groups[sw.groups[k]], gg.amis);
     p.g = text_geom(gg, n, m_min, 0);
     p.ys_lo = gg.amis;
     p.out_off = d_off;

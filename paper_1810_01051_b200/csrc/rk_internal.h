@@ -71,9 +71,9 @@ struct MultiGroup {
   uint64_t ys_hi;          // one past the last window start with room for m bytes (a-space)
   uint32_t m, tsize;
 };
-constexpr int kMultiMaxGroups = 16;
-constexpr int kMultiWarps = 32;      // one 32-warp CTA per SM shares the 64 KiB q-gram filter
-constexpr int kMultiStageChunks = 2;  // 2 KiB TMA stages, so 32 rings fit beside the filter  // length groups per sweep (kernel parameter space)
+constexpr int kMultiMaxGroups = 64;  // length groups per sweep (kernel parameter space)
+constexpr int kMultiWarps = 16;      // one 16-warp CTA per SM shares the 64 KiB q-gram filter
+constexpr int kMultiStageChunks = 4;  // 4 KiB TMA stages  // length groups per sweep (kernel parameter space)
 
 struct MultiArgs {
   TextGeom g;                 // q-gram mode: tiles cover the anchors (q-gram ends)
@@ -85,6 +85,8 @@ struct MultiArgs {
   uint32_t* out_idx;
   uint64_t cap;
   unsigned long long* counters;  // [0] = pairs found
+  const uint4* qmap;             // q-gram hash -> length-group mask (qmode > 0)
+  uint32_t qmap_size;            // entries, a power of two
   uint32_t G;                    // length groups in grp (1 when qmode == 0)
   MultiGroup grp[kMultiMaxGroups];
 };

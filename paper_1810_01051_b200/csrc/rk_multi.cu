@@ -5,7 +5,7 @@
 namespace rkb {
 
 // Every length >= 7 of the set in one sweep: anchored q-grams against the shared filter.
-__global__ void __launch_bounds__(kMultiBlock) rk_multi_qgram_kernel(const MultiArgs a) {
+__global__ void __launch_bounds__(kMultiBlock) rk_multi_qgram_kernel(const __grid_constant__ MultiArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   MultiRing* rings = reinterpret_cast<MultiRing*>(smem);
   uint32_t* sfilter = reinterpret_cast<uint32_t*>(smem + sizeof(MultiRing) * kMultiWarps);

@@ -170,14 +170,27 @@ __device__ __forceinline__ void multi_exact(const MultiArgs& a, int64_t J, int l
   }
 }
 
-// Exact check of the window(s) starting at a-position ya against every length group
-// (lanes with active == false only take part in the warp collectives).
+// Length groups (bit i = grp[i]) with a pattern whose sampled q-grams include the one
+// hashing to h: an open-addressing table {key, -, mask lo, mask hi} built with the filter.
+__device__ __forceinline__ uint64_t qgram_groups(const MultiArgs& a, uint32_t h) {
+  uint32_t slot = mhash(h) & (a.qmap_size - 1);
+  for (;;) {
+    const uint4 e = a.qmap[slot];
+    if ((e.z | e.w) == 0u) return 0;  // empty: no pattern has this q-gram
+    if (e.x == h) return ((uint64_t)e.w << 32) | e.z;
+    slot = (slot + 1) & (a.qmap_size - 1);
+  }
+}
+
+// Exact check of the window(s) starting at a-position ya against the length groups in
+// gmask (lanes with active == false only take part in the warp collectives).
 __device__ __forceinline__ void multi_check_window(const MultiArgs& a, int64_t ya, bool active,
-                                                   int lane) {
+                                                   int lane, uint64_t gmask) {
   const TextGeom& g = a.g;
   const uint8_t* text = g.abase + g.amis;
   const int64_t y = ya - (int64_t)g.amis;  // text index of the first byte
-  for (uint32_t gi = 0; gi < a.G; ++gi) {
+  for (; gmask; gmask &= gmask - 1) {
+    const uint32_t gi = __ffsll((long long)gmask) - 1;
     const uint32_t m = a.grp[gi].m;
     int idx = -1;
     if (active && ya >= (int64_t)a.ys_lo && ya < (int64_t)a.grp[gi].ys_hi) {
@@ -189,6 +202,25 @@ __device__ __forceinline__ void multi_check_window(const MultiArgs& a, int64_t y
     }
     multi_append(a, idx, y, lane);
   }
+}
+
+// The SS windows of anchor e (their q-gram ends at e and passed the filter), checked by
+// lanes 0..SS-1 against the length groups holding that q-gram.
+template <int SS, int QW>
+__device__ __forceinline__ void qgram_candidate(const MultiArgs& a, int64_t e, int lane) {
+  constexpr int q = 4 * QW;
+  if (e < (int64_t)a.g.ja_lo || e >= (int64_t)a.g.ja_hi) return;  // no window (uniform)
+  // which length groups hold this q-gram (the filter only says "some pattern")
+  uint64_t gmask = 1;
+  if (a.G > 1) {
+    const uint32_t* qw = reinterpret_cast<const uint32_t*>(a.g.abase + e - q + 1);
+    uint32_t w[QW];
+#pragma unroll
+    for (int i = 0; i < QW; ++i) w[i] = qw[i];
+    gmask = qgram_groups(a, qgram_hash<QW>(w));
+  }
+  // the window whose q-gram starts j = lane bytes in
+  if (gmask) multi_check_window(a, e - q + 1 - lane, lane < SS, lane, gmask);
 }
 
 // One tile of anchored q-grams (one per SS bytes, ending at e = J + SS*t + SS - 1); a
@@ -211,8 +243,7 @@ __device__ __forceinline__ void qgram_tile(const MultiArgs& a, MultiRing* R, Str
             const int tt = __ffs(ms) - 1;
             ms &= ms - 1;
             // the window whose anchor this is: its q-gram starts j = lane bytes in
-            const int64_t e = Js + (int64_t)SS * tt + SS - 1;
-            multi_check_window(a, e - q + 1 - lane, lane < SS, lane);
+            qgram_candidate<SS, QW>(a, Js + (int64_t)SS * tt + SS - 1, lane);
           }
         }
       });
@@ -220,7 +251,7 @@ __device__ __forceinline__ void qgram_tile(const MultiArgs& a, MultiRing* R, Str
 
 // m < 7: one length group, every window's exact rolling hash against a 2^16-bit filter.
 template <int M>
-__global__ void __launch_bounds__(kMultiBlock) rk_multi_short_kernel(const MultiArgs a) {
+__global__ void __launch_bounds__(kMultiBlock) rk_multi_short_kernel(const __grid_constant__ MultiArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   MultiRing* rings = reinterpret_cast<MultiRing*>(smem);
   uint32_t* sfilter = reinterpret_cast<uint32_t*>(smem + sizeof(MultiRing) * kMultiWarps);

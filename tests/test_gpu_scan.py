@@ -330,6 +330,19 @@ def test_multi_mixed_lengths_one_sweep(gpu):
                 assert r.offsets == expect[i], (alpha, shift, i, len(ps[i]))
 
 
+def test_multi_mixed_lengths_longer_than_text(gpu):
+    """Lengths longer than the text share the sweep with an empty window range."""
+    rng = np.random.default_rng(82)
+    for n in (7, 40, 100, 5000):
+        text = rng.integers(0, 3, n, dtype=np.uint8).tobytes()
+        pats = [text[: min(n, m)] if m <= n else bytes(m) for m in range(7, 130, 3)]
+        pats += [text[n // 2 : n // 2 + 9], text[-8:]]
+        out = rk.search_multi(text, pats)
+        ps, _, _ = oracle.pattern_set(pats)
+        for i, r in out:
+            assert r == rk.search_naive(text, ps[i]), (n, i, len(ps[i]))
+
+
 def test_multi_plan_cache_keys_on_bytes(gpu):
     """The per-context plan cache must not confuse sets that differ only in pattern bytes
     (equal lengths and hashes: "ac" / "ba", tests/test_matcher.py:139-146 of the reference)."""
