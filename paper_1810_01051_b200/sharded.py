@@ -98,3 +98,65 @@ def search_sharded(shard, pattern, win_lo: int, win_hi: int, byte_lo: int, group
     allo, _ = gather_offsets(offs, group)
     tot = sum_counters(torch.tensor([k, hits, coll], dtype=torch.int64, device=offs.device), group)
     return allo, [int(v) for v in tot.tolist()]
+
+
+def multi_shard(rank: int, world: int, n_total: int, lengths, per_rank: int | None = None):
+    """Shard map of a multi-pattern search (matcher.py:125-157) over window STARTS: rank r
+    owns starts [a_r, b_r) of the shortest length's start range and holds bytes
+    [a_r, b_r + max(m) - 1) -- enough for the longest pattern starting in its range.
+    ``per_rank`` given: weak scaling (fixed starts per rank), else strong."""
+    m_min, m_max = min(lengths), max(lengths)
+    if per_rank is None:
+        a, b, _, _ = strong_shard(rank, world, n_total, m_min)
+    else:
+        a, b, _, _ = weak_shard(rank, per_rank, n_total, m_min)
+    return a, b, a, min(b + m_max - 1, n_total) if b > a else a
+
+
+def gather_pairs(idx, off, group=None):
+    """All ranks' (pattern index, offset) pairs, ordered by (index, offset) on every rank.
+
+    Each rank's pairs must already be in (index, offset) order and the ranks' start
+    ranges ascending, so a stable sort by index of the rank-order concatenation is the
+    global order (the reference's per-pattern ascending lists)."""
+    import torch
+
+    key = (idx.to(torch.int64) << 40) | off.to(torch.int64)  # offsets < 2^40
+    allk, _ = gather_offsets(key, group)
+    order = torch.sort(allk >> 40, stable=True).indices
+    allk = allk[order]
+    return (allk >> 40).to(torch.int32), allk & ((1 << 40) - 1)
+
+
+def search_multi_sharded(shard, patterns, start_lo: int, start_hi: int, byte_lo: int,
+                         group=None, multi_fn=None):
+    """Multi-pattern search of this rank's shard (global starts [start_lo, start_hi),
+    bytes from byte_lo), gathered on every rank.
+
+    Returns (index int32 tensor, offset int64 tensor) ordered by (index, offset): pattern
+    i's matches are the offsets of its run.  ``multi_fn(shard, patterns) -> [offsets per
+    pattern]`` (shard-local) defaults to the B200 multi-pattern sweep."""
+    import numpy as np
+    import torch
+
+    if multi_fn is None:
+        from . import _scan
+        from .matcher import _device_text, multi_scan
+
+        def multi_fn(t, pats):
+            t_dev, dev = _device_text(_scan.as_u8(t))
+            return multi_scan(t_dev, dev, pats)
+
+    dev = shard.device if isinstance(shard, torch.Tensor) else "cpu"
+    idx_parts, off_parts = [], []
+    if start_hi > start_lo:
+        per = multi_fn(shard, list(patterns))
+        lo, hi = start_lo - byte_lo, start_hi - byte_lo
+        for i, offs in enumerate(per):
+            offs = torch.as_tensor(np.asarray(offs, dtype=np.int64))
+            offs = offs[(offs >= lo) & (offs < hi)]  # halo starts belong to the next rank
+            idx_parts.append(torch.full((offs.numel(),), i, dtype=torch.int32))
+            off_parts.append(offs + byte_lo)
+    idx = torch.cat(idx_parts) if idx_parts else torch.empty(0, dtype=torch.int32)
+    off = torch.cat(off_parts) if off_parts else torch.empty(0, dtype=torch.int64)
+    return gather_pairs(idx.to(dev), off.to(dev), group)

@@ -113,3 +113,84 @@ def test_shard_maps_cover_windows_once():
                     a, b, blo, bhi = sharded.weak_shard(r, per, n, m)
                     cov += list(range(a, b))
                 assert cov == list(range(nw))
+
+
+def _oracle_multi(shard, pats):
+    t = shard.numpy() if isinstance(shard, torch.Tensor) else np.asarray(shard)
+    ps, by_len, _ = oracle.pattern_set(pats)
+    out = [None] * len(ps)
+    for m, idxs in by_len.items():
+        for j, offs in oracle.c_search_multi_group(t, [ps[i] for i in idxs]):
+            out[idxs[j]] = offs
+    return out
+
+
+def _multi_worker(rank, world, port, text, pats, weak, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = len(text)
+        lengths = [len(p) for p in pats]
+        per = -(-n // world) if weak else None
+        a, b, blo, bhi = sharded.multi_shard(rank, world, n, lengths, per)
+        shard = torch.from_numpy(np.frombuffer(text, dtype=np.uint8)[blo:bhi].copy())
+        idx, off = sharded.search_multi_sharded(shard, pats, a, b, blo, multi_fn=_oracle_multi)
+        q.put((rank, idx.tolist(), off.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,weak", [(2, False), (3, True)])
+def test_sharded_multi_pairs_match_oracle(world, weak):
+    """Mixed lengths, copies straddling every shard boundary: each rank keeps the starts
+    it owns (the (max m - 1)-byte halo serves the longest pattern), and the gathered
+    pairs are the reference's per-pattern ascending lists."""
+    rng = np.random.default_rng(40 + world)
+    n = 12000
+    text = bytearray(rng.integers(0, 3, n, dtype=np.uint8).tobytes())
+    pats = [bytes(text[50 : 50 + m]) for m in (3, 9, 17, 40)] + [b"\x00\x01\x02" * 5]
+    for cut in (n // 2, n // 3, 2 * n // 3, -(-n // world), 2 * -(-n // world)):
+        for p in pats[1:4]:
+            x = cut - len(p) // 2
+            text[x : x + len(p)] = p
+    text = bytes(text)
+    expect = _oracle_multi(np.frombuffer(text, dtype=np.uint8), pats)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_multi_worker, args=(r, world, port, text, pats, weak, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, idx, off in out:
+        got = [[o for i, o in zip(idx, off) if i == j] for j in range(len(pats))]
+        assert got == [e.tolist() for e in expect], rank
+
+
+@pytest.mark.gpu
+def test_sharded_multi_gpu_single_rank(gpu):
+    """The default multi_fn (the B200 sweep) and the NCCL gather, one rank on cuda:0;
+    the shard is a view into the middle of the text with its own start range."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        rng = np.random.default_rng(9)
+        n = 300000
+        text = rng.integers(0, 4, n, dtype=np.uint8)
+        pats = [text[x : x + m].tobytes() for x, m in ((10, 8), (5000, 20), (123456, 33))]
+        a, b = 1000, 250000
+        blo, bhi = a, min(b + 33 - 1, n)
+        shard = torch.from_numpy(text[blo:bhi].copy()).cuda()
+        idx, off = sharded.search_multi_sharded(shard, pats, a, b, blo)
+        full = _oracle_multi(text, pats)
+        for j in range(len(pats)):
+            exp = [o for o in full[j].tolist() if a <= o < b]
+            assert off[idx == j].cpu().tolist() == exp
+    finally:
+        dist.destroy_process_group()
