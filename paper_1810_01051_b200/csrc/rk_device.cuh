@@ -6,7 +6,8 @@
 //   * low32(h) depends only on the last min(m,32) bytes of the window;
 //   * for m >= 32, low32(h(window ending at j)) = S(j) where S(j) = 2 S(j-1) + t[j] mod 2^32
 //     is a single running fold (the out-term 2^m * t[x] vanishes mod 2^32);
-//   * for m < 32 the exact 32-bit roll is L' = 2L + in - 2^m out (rkhash.py:48-60 `roll`);
+//   * for m < 32 the exact 32-bit roll is L' = 2L + in - 2^m out (rkhash.py:48-60 `roll`),
+//     and L(j) = S(j) mod 2^m (the out-term is a multiple of 2^m);
 //   * for m <= 24, h < 2^32, so low32 equality IS 64-bit hash equality.
 // A window is a hash hit iff all 64 bits agree; a hit is a match iff its bytes equal the
 // pattern, otherwise it is a collision (_scan.py:38-49).  The kernels filter on the exact

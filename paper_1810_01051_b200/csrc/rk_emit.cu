@@ -28,6 +28,7 @@ __device__ __forceinline__ void st_global_v2(int64_t* p, int64_t a, int64_t b) {
 }
 
 __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the scan's writes are visible
   extern __shared__ __align__(16) int64_t stage_all[];
   __shared__ unsigned long long red[kEmitWarps];
   __shared__ uint32_t wsum[kEmitWarps];
@@ -155,8 +156,20 @@ cudaError_t launch_emit(const EmitArgs& e, cudaStream_t s) {
     if (err != cudaSuccess) return err;
     if (dev < kMaxDevices) attr[dev] = true;
   }
-  rk_emit_kernel<<<(unsigned)blocks, kEmitTiles, emit_smem_bytes(), s>>>(e);
-  return cudaGetLastError();
+  // programmatic dependent launch: the emit grid is scheduled as the scan's CTAs retire
+  // and waits (griddepcontrol.wait) for the scan's results, instead of paying a full
+  // launch gap after the scan drains
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(kEmitTiles);
+  cfg.dynamicSmemBytes = emit_smem_bytes();
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, rk_emit_kernel, e);
 }
 
 }  // namespace rkb

@@ -2,10 +2,11 @@
 // /root/reference/pkg/src/rkmatch/_scan.py:28-50, and the range partition + ordered merge
 // of search_parallel, parallel.py:155-172):
 //
-//   TMA bulk copies (2 KiB stages, 4 in flight per warp) -> shared memory
-//     -> exact 32-bit rolling hash per window, compared with low32(hx)
-//        (candidates are ~2^-32 of windows on random text)
-//     -> candidate chunks: 64-bit hash + byte verify -> match / collision counters
+//   TMA bulk copies (4 KiB stages, 2 per warp) -> shared memory
+//     -> per window, the low 32 bits of its hash, by the cheapest exact form for m:
+//        m <= 8 dot products (hits settled inline), 9..14 the exact roll, 15..31 the
+//        32-byte fold as a filter mod 2^m, m >= 32 the fold itself
+//     -> candidate chunks: exact 32/64-bit hash + byte verify -> match / collision counts
 //     -> per-tile match count + hit masks (global), consumed by rk_emit.cu, which
 //        writes the ordered int64 window starts.
 //
@@ -293,6 +294,9 @@ __device__ __forceinline__ void finish_tile(const ScanArgs& a, uint64_t t, uint3
 
 template <int M>
 __global__ void __launch_bounds__(kBlock, 3) rk_scan_kernel(const ScanArgs a) {
+  // let the emit grid (launched with programmatic serialization) be scheduled as this
+  // grid's CTAs retire; it waits for our results with griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;");
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
