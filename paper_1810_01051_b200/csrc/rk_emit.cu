@@ -29,6 +29,7 @@ __device__ __forceinline__ void st_global_v2(int64_t* p, int64_t a, int64_t b) {
 
 __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the scan's writes are visible
+  asm volatile("griddepcontrol.launch_dependents;");  // the next scan may be scheduled
   extern __shared__ __align__(16) int64_t stage_all[];
   __shared__ unsigned long long red[kEmitWarps];
   __shared__ uint32_t wsum[kEmitWarps];

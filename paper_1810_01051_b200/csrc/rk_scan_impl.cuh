@@ -294,8 +294,10 @@ __device__ __forceinline__ void finish_tile(const ScanArgs& a, uint64_t t, uint3
 
 template <int M>
 __global__ void __launch_bounds__(kBlock, 3) rk_scan_kernel(const ScanArgs a) {
-  // let the emit grid (launched with programmatic serialization) be scheduled as this
-  // grid's CTAs retire; it waits for our results with griddepcontrol.wait
+  // PDL both ways: wait for the previous grid in the stream (its writes -- the text, the
+  // previous emit's reads of our scratch -- must be complete), and let the emit grid be
+  // scheduled as our CTAs retire (it waits for our results the same way)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
@@ -377,8 +379,19 @@ cudaError_t launch_m(const ScanArgs& a, int grid, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     if (dev < kMaxDevices) attr[dev] = true;
   }
-  rk_scan_kernel<M><<<grid, kBlock, smem, s>>>(a);
-  return cudaGetLastError();
+  // programmatic dependent launch: scheduled as the previous kernel's CTAs retire; the
+  // kernel waits for that grid's completion before touching memory (griddepcontrol.wait)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kBlock);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, rk_scan_kernel<M>, a);
 }
 
 template <int M>
