@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-seconds", type=float, default=150.0,
+                    help="--impl reference: host-CPU budget of the whole run")
     # test plumbing only: exercise the multi-rank path on a one-GPU box (all ranks on
     # cuda:0, gloo instead of NCCL so no collective kernels wait on each other there)
     ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"))
@@ -167,6 +169,16 @@ def cpu_fixed(text, patterns, sizes, threads):
     return sec_per_byte, t_all
 
 
+def workload_config(per: int, sweep, world: int) -> dict:
+    """The workload both arms report (BASELINE.json configs[1])."""
+    return {"workload": "C2: single-pattern length sweep over 1 GiB printable-ASCII "
+                        "text per GPU (BASELINE.json configs[1])",
+            "bytes_per_gpu": per, "sweep": sweep, "pattern_source": "sampled",
+            "corpus": "DnaSpec(42, N GiB, bytes(32..126))",
+            "l2": "inputs larger than L2 (1 GiB per GPU vs 126 MB)",
+            "parallelism": f"shard{world} (contiguous, (m-1)-byte halo)"}
+
+
 def run_reference(args):
     """--impl reference: the reference algorithm on the host cores, same metric."""
     rank = int(os.environ.get("RANK", "0"))
@@ -180,7 +192,7 @@ def run_reference(args):
     text = np.frombuffer(oracle.generate(SEED, n, ASCII), dtype=np.uint8)
     pats = {m: text[sampled_offset(n, m): sampled_offset(n, m) + m].tobytes() for m in sweep}
     # per-step sample sizes so that the run (warmup + steps) stays within minutes
-    budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    budget = max(min(2.0, args.ref_seconds), args.ref_seconds / max(1, args.steps + args.warmup))
     _, sizes = cpu_rates(text, pats, budget, threads)
     for _ in range(args.warmup):
         cpu_fixed(text, pats, sizes, threads)
@@ -198,10 +210,10 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": "C2 single-pattern length sweep, printable ASCII (seed 42)",
-                   "sweep": sweep, "sample_bytes_per_m": sizes},
+        "config": workload_config(args.bytes_per_gpu, sweep, args.gpus),
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"prefixes {sizes} of the 1 GiB C2 corpus, per step"},
+                         "sample": f"per step, prefixes {sizes} (bytes per m) of the C2 corpus; "
+                                   f"oracle C port of _scan_range + search_parallel ranges"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -375,12 +387,7 @@ def run_ours(args):
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (rkmatch generator, on device)",
-            "config": {"workload": "C2: single-pattern length sweep over 1 GiB printable-ASCII "
-                                   "text per GPU (BASELINE.json configs[1])",
-                       "bytes_per_gpu": per, "sweep": sweep, "pattern_source": "sampled",
-                       "corpus": "DnaSpec(42, N GiB, bytes(32..126))",
-                       "l2": "inputs larger than L2 (1 GiB per GPU vs 126 MB)",
-                       "parallelism": f"shard{world} (contiguous, (m-1)-byte halo)"},
+            "config": workload_config(per, sweep, world),
             "per_m_gbs": {str(m): (plans[m][1] - plans[m][0] + m - 1) / (per_m_ms[m] / 1e3) / 1e9
                           for m in sweep},
             "matches_per_m": {str(m): int(host_counts[i, 0]) for i, m in enumerate(sweep)},

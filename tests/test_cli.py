@@ -103,3 +103,26 @@ def test_bench_sweep_gpu(tmp_path, capsys, gpu):
     data = json.loads((tmp_path / "rep.json").read_text())
     assert [r["axis_value"] for r in data["rows"]] == [300 << 10, 1 << 20]
     assert (tmp_path / "rep.csv").read_text().startswith("axis_value,t_seq_ms,t_par_ms,speedup\n")
+
+
+def test_bench_reference_arm_line():
+    """bench.py --impl reference: one JSON line with the contract's keys, same config as
+    the GPU arm, the reference algorithm timed on the host cores (no GPU needed)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference",
+                        "--steps", "1", "--warmup", "0", "--sweep", "32,64",
+                        "--ref-seconds", "0.5"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "GB/s" and line["value"] > 0
+    for k in ("metric", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "dtype", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["config"]["sweep"] == [32, 64]
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["value"] == line["value"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
