@@ -202,7 +202,9 @@ def main():
     fns = {"C1": c1, "C3": c3, "C4": c4, "C5": c5,
            # not a BASELINE config: C3's shape over DNA (low-entropy q-grams)
            "C3dna": lambda r: c3(r, m=32, alphabet=b"ACGT", tag="C3dna"),
-           "C3mixed": c3_mixed}
+           "C3mixed": c3_mixed,
+           "C3short": lambda r: c3(r, m=5, tag="C3short"),
+           "C3short4": lambda r: c3(r, m=4, tag="C3short4")}
     for name in args.only.split(","):
         t0 = time.time()
         r = fns[name](args.reps)

@@ -22,7 +22,7 @@ CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "rkb200"
 LIB = PKG / "librkb200.so"
 SOURCES = ["rk_scan.cu", *[f"rk_scan_g{g}.cu" for g in range(4)], "rk_multi.cu",
-           "rk_multi_g0.cu", "rk_emit.cu", "rk_aux.cu", "rk_capi.cu"]
+           "rk_multi_g0.cu", "rk_pairs.cu", "rk_emit.cu", "rk_aux.cu", "rk_capi.cu"]
 HEADERS = ["rk_device.cuh", "rk_internal.h", "rk_scan_impl.cuh", "rk_multi_impl.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

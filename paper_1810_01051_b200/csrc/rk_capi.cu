@@ -135,6 +135,8 @@ struct MultiPlan {
   struct Group {
     uint32_t m, P, tsize;
     uint64_t pats, phash, order, gidx, table, filter;
+    uint64_t tiny = 0;  // m < 7: cuckoo table of the packed patterns
+    TinyHash tiny_hash{};
   };
   struct Sweep {
     std::vector<uint32_t> groups;  // ascending lengths
@@ -189,6 +191,8 @@ struct rk_ctx {
   cudaEvent_t ev_copied[kRing] = {};  // ring slot free again
   cudaEvent_t ev_ready = nullptr;                 // bytes of the current chunk landed
   // multi-pattern tables
+  uint8_t* d_sort = nullptr;   // scratch of the device pair sort
+  uint64_t sort_cap = 0;
   uint8_t* d_mblob = nullptr;  // every length group's patterns, hashes and tables
   uint64_t mblob_cap = 0;
   uint8_t* h_mstage = nullptr;  // pinned staging of the blob
@@ -492,6 +496,61 @@ int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, 
       const uint32_t bit = (r.first * 0x9E3779B1u) >> 16;
       filter[bit >> 5] |= 1u << (bit & 31);
     }
+    if (m < 7) {
+      // cuckoo table of the packed patterns (index in the top 16 bits), 2 slots per key
+      std::vector<uint64_t> key(b.P);
+      for (uint32_t i = 0; i < b.P; ++i) {
+        uint64_t k = 0;
+        memcpy(&k, h_patterns + first_byte[members[i]], m);
+        key[i] = k;
+      }
+      std::vector<uint64_t> slots;
+      TinyHash th{};
+      bool ok = false;
+      for (uint32_t size = 64; !ok && size <= kTinySlotsMax; size <<= 1) {
+        if (size < 2 * b.P) continue;
+        uint32_t lg = 0;
+        while ((1u << lg) < size) ++lg;
+        for (uint32_t seed = 0; !ok && seed < 64; ++seed) {
+          th.c1 = 0x9E3779B1u + 0x6A09E667u * seed;
+          th.c2 = 0x85EBCA77u ^ (0xBB67AE85u * seed);
+          th.c3 = 0xC2B2AE3Du + 0x3C6EF372u * seed;
+          th.c1 |= 1u;
+          th.c3 |= 1u;
+          th.shift = 32 - lg;
+          th.size = size;
+          slots.assign(size, ~0ull);
+          ok = true;
+          for (uint32_t i = 0; i < b.P && ok; ++i) {
+            uint64_t cur = key[i] | ((uint64_t)members[i] << 48);
+            uint32_t s1, s2;
+            tiny_slots(tiny_key_hash((uint32_t)cur, (uint32_t)(cur >> 32) & 0xffffu, th), th, s1,
+                       s2);
+            uint32_t at = s1;
+            for (int kick = 0; kick < 500; ++kick) {
+              std::swap(cur, slots[at]);
+              if (cur == ~0ull) break;
+              tiny_slots(tiny_key_hash((uint32_t)cur, (uint32_t)(cur >> 32) & 0xffffu, th), th,
+                         s1, s2);
+              at = (at == s1) ? s2 : s1;
+              if (kick == 499) ok = false;
+            }
+          }
+        }
+      }
+      if (!ok) return fail(RK_ECUDA, "cannot build the short-pattern table");
+      b.tiny_hash = th;
+      b.tiny = reserve((uint64_t)th.size * 8 + kTinyFilterBytes);
+      memcpy(blob.data() + b.tiny, slots.data(), (uint64_t)th.size * 8);
+      uint32_t* filt = reinterpret_cast<uint32_t*>(blob.data() + b.tiny + (uint64_t)th.size * 8);
+      for (uint32_t i = 0; i < b.P; ++i) {
+        const uint32_t f = tiny_key_hash((uint32_t)key[i], (uint32_t)(key[i] >> 32), th);
+        uint32_t* blk = filt + 2 * (f >> kTinyFilterShift);
+        const uint32_t q = f ^ (f >> 13);
+        blk[0] |= (1u << (q & 31)) | (1u << ((q >> 5) & 31));
+        blk[1] |= (1u << ((q >> 10) & 31)) | (1u << ((q >> 15) & 31));
+      }
+    }
     plan.groups.push_back(b);
   }
 
@@ -639,6 +698,7 @@ int rk_ctx_destroy(rk_ctx_t* c) {
   cudaStreamDestroy(c->s_copy);
   cudaStreamDestroy(c->s_comp);
   cudaFree(c->d_mblob);
+  cudaFree(c->d_sort);
   cudaFreeHost(c->h_mstage);
   cudaFreeHost(c->h_mresult);
   delete c;
@@ -893,9 +953,12 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
     G.gidx = reinterpret_cast<const uint32_t*>(dev + b.gidx);
     G.table = reinterpret_cast<const uint2*>(dev + b.table);
     G.filter = reinterpret_cast<const uint32_t*>(dev + b.filter);
+    G.tiny = dev + b.tiny;
+    G.tiny_hash = b.tiny_hash;
     G.ys_hi = b.m <= n ? amis + (n - b.m + 1) : amis;  // longer than the text: no windows
     G.m = b.m;
     G.tsize = b.tsize;
+    G.P = b.P;
     return G;
   };
   for (const MultiPlan::Sweep& sw : plan.sweeps) {
@@ -952,17 +1015,15 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
   const uint64_t total = c->h_mresult[0];
   *pairs = total;
   const uint64_t k = std::min(total, cap);
-  if (k > 1) {
+  if (k > pre) {  // too many for a host round trip: radix-sort the pairs on the device
+    const size_t need = sort_pairs_scratch(k);
+    if (int r = grow(&c->d_sort, &c->sort_cap, (uint64_t)need, false, s)) return r;
+    RK_CUDA(sort_pairs(d_off, d_idx, k, c->d_sort, c->sort_cap, s));
+  } else if (k > 1) {
     std::vector<int64_t> off(k);
     std::vector<uint32_t> idx(k);
-    if (k <= pre) {
-      memcpy(off.data(), c->h_mresult + 1, k * sizeof(int64_t));
-      memcpy(idx.data(), c->h_mresult + 1 + kMultiPrefix, k * sizeof(uint32_t));
-    } else {
-      RK_CUDA(cudaMemcpyAsync(off.data(), d_off, k * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-      RK_CUDA(cudaMemcpyAsync(idx.data(), d_idx, k * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-      RK_CUDA(cudaStreamSynchronize(s));
-    }
+    memcpy(off.data(), c->h_mresult + 1, k * sizeof(int64_t));
+    memcpy(idx.data(), c->h_mresult + 1 + kMultiPrefix, k * sizeof(uint32_t));
     std::vector<uint64_t> perm(k);
     for (uint64_t i = 0; i < k; ++i) perm[i] = i;
     std::sort(perm.begin(), perm.end(), [&](uint64_t x, uint64_t y) {

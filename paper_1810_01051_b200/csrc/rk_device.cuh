@@ -137,6 +137,36 @@ __device__ __forceinline__ uint32_t bsel(uint32_t w, int k) {
   return __byte_perm(w, 0u, 0x4440u | (uint32_t)k);
 }
 
+// word (4 bytes) of lb ++ v starting at byte p (static after unrolling; p + 4 <= 64)
+__device__ __forceinline__ uint32_t w64(const uint32_t (&lb)[8], const Vec32& v, int p) {
+  const int q = p >> 2, r = p & 3;
+  const uint32_t lo = q < 8 ? lb[q] : v.w[q - 8];
+  if (r == 0) return lo;
+  const uint32_t hi = (q + 1) < 8 ? lb[q + 1] : ((q + 1) < 16 ? v.w[q + 1 - 8] : 0u);
+  return __funnelshift_r(lo, hi, 8 * r);
+}
+
+// dp4a weights of window bytes [4q, 4q+4) in the hash of an M-byte window (M <= 8):
+// byte i carries 2^(M-1-i).
+template <int M>
+__host__ __device__ constexpr uint32_t win_weights(int q) {
+  uint32_t w = 0;
+  for (int b = 0; b < 4; ++b) {
+    const int i = 4 * q + b;
+    if (i < M) w |= (uint32_t)(1u << (M - 1 - i)) << (8 * b);
+  }
+  return w;
+}
+
+// Bit k set when window end J + k is in the launch's range [ja_lo, ja_hi).
+__device__ __forceinline__ uint32_t valid_mask(const TextGeom& g, int64_t J) {
+  const int64_t lo = min(max((int64_t)g.ja_lo - J, (int64_t)0), (int64_t)32);
+  const int64_t hi = min(max((int64_t)g.ja_hi - J, (int64_t)0), (int64_t)32);
+  const uint32_t above = lo >= 32 ? 0u : (0xffffffffu << lo);
+  const uint32_t below = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
+  return above & below;
+}
+
 // fold of 32 bytes, mod 2^32 (= S at the last byte): 8 dp4a + 7 shifts.
 __device__ __forceinline__ uint32_t fold32(const uint32_t (&w)[8]) {
   uint32_t s = __dp4a(w[0], kFoldW, 0u);

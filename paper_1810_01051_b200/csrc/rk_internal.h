@@ -60,6 +60,27 @@ __host__ __device__ __forceinline__ uint32_t qgram_hash(const uint32_t* w) {
   return h ^ (h >> 15);
 }
 
+// m < 7: cuckoo table of the patterns (slot = key bytes | index << 48, empty = ~0): the
+// two slots of a key of low word lo and high word hi (bytes 4..5), for the same
+// function on the host (build) and the device (lookup).
+struct TinyHash {
+  uint32_t c1, c2, c3;  // seeds (the host retries others if an insertion cycles)
+  uint32_t shift;       // 32 - log2(size)
+  uint32_t size;        // slots, a power of two
+};
+constexpr uint32_t kTinySlotsMax = 8192;             // 64 KiB of shared memory
+constexpr uint32_t kTinyFilterBytes = (1u << 17) / 8;  // 2^17-bit key filter, 16 KiB
+constexpr uint32_t kTinyFilterShift = 32 - 11;         // 64-bit block: top 11 bits of f
+__host__ __device__ __forceinline__ uint32_t tiny_key_hash(uint32_t lo, uint32_t hi,
+                                                           const TinyHash& t) {
+  return lo * t.c1 + hi * t.c2;
+}
+__host__ __device__ __forceinline__ void tiny_slots(uint32_t f, const TinyHash& t, uint32_t& s1,
+                                                    uint32_t& s2) {
+  s1 = f >> t.shift;
+  s2 = ((f ^ (f >> 15)) * t.c3) >> t.shift;
+}
+
 // One length group of a multi-pattern launch (all arrays device-resident).
 struct MultiGroup {
   const uint8_t* pats;     // P_g * m bytes, the group's patterns back to back
@@ -68,8 +89,10 @@ struct MultiGroup {
   const uint32_t* gidx;    // group-local index -> the caller's pattern index
   const uint2* table;      // tsize entries: {key, (first << 13) | count}, y = empty marker
   const uint32_t* filter;  // kMultiFilterWords words over the low-32 keys
+  const uint8_t* tiny;     // m < 7: the cuckoo table (see rk_multi_tiny_kernel)
+  TinyHash tiny_hash;
   uint64_t ys_hi;          // one past the last window start with room for m bytes (a-space)
-  uint32_t m, tsize;
+  uint32_t m, tsize, P;
 };
 constexpr int kMultiMaxGroups = 64;  // length groups per sweep (kernel parameter space)
 constexpr int kMultiWarps = 16;      // one 16-warp CTA per SM shares the 64 KiB q-gram filter
@@ -91,8 +114,14 @@ struct MultiArgs {
   MultiGroup grp[kMultiMaxGroups];
 };
 size_t multi_smem_bytes();
+size_t multi_tiny_smem_bytes();
 int multi_blocks_per_sm(uint32_t qmode, uint32_t m);
 cudaError_t launch_multi(const MultiArgs& a, int grid, cudaStream_t s);
+
+// device ordering of (pattern index, offset) pairs (rk_pairs.cu)
+size_t sort_pairs_scratch(uint64_t k);
+cudaError_t sort_pairs(int64_t* d_off, uint32_t* d_idx, uint64_t k, void* scratch,
+                       size_t scratch_bytes, cudaStream_t s);
 
 // auxiliaries (rk_aux.cu)
 cudaError_t launch_window_hashes(const uint8_t* text, uint64_t n, uint32_t m, uint64_t start,

@@ -33,33 +33,38 @@ __global__ void __launch_bounds__(kMultiBlock) rk_multi_qgram_kernel(const __gri
 }
 
 template <int M>
-cudaError_t launch_multi_short(const MultiArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_multi_tiny(const MultiArgs& a, int grid, cudaStream_t s);
 template <int M>
-int multi_short_occupancy();
+int multi_tiny_occupancy();
 
 using MultiLaunchFn = cudaError_t (*)(const MultiArgs&, int, cudaStream_t);
 using MultiOccFn = int (*)();
-static constexpr MultiLaunchFn kShortLaunch[6] = {
-    &launch_multi_short<1>, &launch_multi_short<2>, &launch_multi_short<3>,
-    &launch_multi_short<4>, &launch_multi_short<5>, &launch_multi_short<6>};
-static constexpr MultiOccFn kShortOcc[6] = {
-    &multi_short_occupancy<1>, &multi_short_occupancy<2>, &multi_short_occupancy<3>,
-    &multi_short_occupancy<4>, &multi_short_occupancy<5>, &multi_short_occupancy<6>};
+static constexpr MultiLaunchFn kTinyLaunch[6] = {
+    &launch_multi_tiny<1>, &launch_multi_tiny<2>, &launch_multi_tiny<3>,
+    &launch_multi_tiny<4>, &launch_multi_tiny<5>, &launch_multi_tiny<6>};
+static constexpr MultiOccFn kTinyOcc[6] = {
+    &multi_tiny_occupancy<1>, &multi_tiny_occupancy<2>, &multi_tiny_occupancy<3>,
+    &multi_tiny_occupancy<4>, &multi_tiny_occupancy<5>, &multi_tiny_occupancy<6>};
 
 size_t multi_smem_bytes() {
   return sizeof(MultiRing) * kMultiWarps + kQFilterWords * sizeof(uint32_t);
 }
 
+size_t multi_tiny_smem_bytes() {  // rings + the largest cuckoo table
+  return sizeof(MultiRing) * kMultiWarps + kTinySlotsMax * 8u + kTinyFilterBytes;
+}
+
 int multi_blocks_per_sm(uint32_t qmode, uint32_t m) {
-  if (qmode == 0) return kShortOcc[m - 1]();
+  if (qmode == 0) return kTinyOcc[m - 1]();
   static int occ = 0;  // same on every B200
-  if (!occ) occ = multi_occupancy(rk_multi_qgram_kernel);
+  if (!occ) occ = multi_occupancy(rk_multi_qgram_kernel, multi_smem_bytes());
   return occ;
 }
 
 cudaError_t launch_multi(const MultiArgs& a, int grid, cudaStream_t s) {
-  if (a.qmode == 0) return kShortLaunch[a.g.m - 1](a, grid, s);
-  return multi_launch_kernel<struct QgramAttr>(rk_multi_qgram_kernel, a, grid, s);
+  if (a.qmode == 0) return kTinyLaunch[a.g.m - 1](a, grid, s);
+  return multi_launch_kernel<struct QgramAttr>(rk_multi_qgram_kernel, a, grid,
+                                               multi_smem_bytes(), s);
 }
 
 }  // namespace rkb

@@ -22,8 +22,8 @@
 //     group (exact hash + table + bytes), and since each window has one anchor nothing
 //     is reported twice.  (s, q) is chosen on the host from the lengths and the pattern
 //     alphabet: q up to 16 bytes so that low-entropy texts (DNA: 4^q q-grams) still filter.
-//   * m < 7 (one length per launch): every window's exact 32-bit rolling hash is tested
-//     against a 2^16-bit filter of the pattern hashes.
+//   * m < 7 (one length per launch): the window is its own exact key, looked up in a cuckoo
+//     table of the patterns in shared memory (rk_multi_tiny_kernel).
 // Hits are appended with warp ballot/popc and one atomic per warp; the host orders them
 // by (pattern index, offset), which is exactly the reference's per-pattern ascending lists.
 #pragma once
@@ -145,31 +145,6 @@ __device__ __forceinline__ void multi_append(const MultiArgs& a, int idx, int64_
   }
 }
 
-// Exact pass over the 32 windows ending at [J, J+32) of this lane (a-space), for the
-// single length group of an m < 7 launch.
-template <int M>
-__device__ __forceinline__ void multi_exact(const MultiArgs& a, int64_t J, int lane) {
-  const TextGeom& g = a.g;
-  const Vec32 v = load_edge(g, J);
-  const Vec32 lbv = load_edge(g, J - 32);
-  const uint8_t* text = g.abase + g.amis;
-  uint32_t L = fold_tail<M>(lbv.w);
-#pragma unroll 4
-  for (int k = 0; k < 32; ++k) {
-    const int io = 32 + k - M;
-    const uint32_t in = bsel(v.w[k >> 2], k & 3);
-    const uint32_t out =
-        io < 32 ? bsel(lbv.w[io >> 2], io & 3) : bsel(v.w[(io - 32) >> 2], io & 3);
-    L = 2u * L + in - (out << M);
-    const int64_t ja = J + k;             // window end (a-space)
-    const int64_t ya = ja - (int64_t)M + 1;  // window start (a-space)
-    int idx = -1;
-    if (ya >= (int64_t)a.ys_lo && ya < (int64_t)a.grp[0].ys_hi && filter_test(a.grp[0].filter, L))
-      idx = group_resolve(a.grp[0], text, L, ja - (int64_t)g.amis);
-    multi_append(a, idx, ya - (int64_t)g.amis, lane);
-  }
-}
-
 // Length groups (bit i = grp[i]) with a pattern whose sampled q-grams include the one
 // hashing to h: an open-addressing table {key, -, mask lo, mask hi} built with the filter.
 __device__ __forceinline__ uint64_t qgram_groups(const MultiArgs& a, uint32_t h) {
@@ -249,14 +224,93 @@ __device__ __forceinline__ void qgram_tile(const MultiArgs& a, MultiRing* R, Str
       });
 }
 
-// m < 7: one length group, every window's exact rolling hash against a 2^16-bit filter.
+// m < 7: a window is at most 6 bytes, so it is its own exact key.  The set's patterns sit
+// in a cuckoo table in shared memory -- slot = key bytes | pattern index << 48, every
+// key in one of its two slots -- so a window is looked up with two 8-byte loads and no
+// loop or branch: the reference's "hash equal, then bytes equal" (matcher.py:147-153)
+// collapses into one exact comparison, since a window of this length IS its hash input.
+// (The rolling-hash filter of the longer lengths would pass most windows here: a 5-byte
+// hash takes ~3000 values over printable ASCII.)
+__device__ __forceinline__ unsigned long long ld_shared_u64(uint32_t a) {
+  unsigned long long v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+// Blocked Bloom filter of the keys: 2048 blocks of 64 bits, 4 bits per key (2 per half),
+// one LDS.64 per window; ~5e-5 false positives per window at 1024 patterns, so a group
+// of 8 windows rarely leaves the fast path.
+__device__ __forceinline__ uint32_t tiny_filter_test(uint32_t bitmap, uint32_t f) {
+  unsigned long long x = ld_shared_u64(bitmap + 8 * (f >> kTinyFilterShift));
+  const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+  const uint32_t p = f ^ (f >> 13);  // bit positions from mixed bits, each mod 32
+  return __funnelshift_r(xl, xl, p) & __funnelshift_r(xl, xl, p >> 5) &
+         __funnelshift_r(xh, xh, p >> 10) & __funnelshift_r(xh, xh, p >> 15) & 1u;
+}
+
+// The 32 windows go in four groups of 8: one filter probe each and one predicate per
+// group; a group with a filter hit looks its passing windows up in the cuckoo table.
 template <int M>
-__global__ void __launch_bounds__(kMultiBlock) rk_multi_short_kernel(const __grid_constant__ MultiArgs a) {
+__device__ __forceinline__ void tiny_chunk(const MultiArgs& a, const Vec32& v,
+                                           const uint32_t (&lb)[8], int64_t J, uint32_t vmask,
+                                           uint32_t slots, uint32_t bitmap, const TinyHash& th) {
+  constexpr uint32_t K0 = M >= 4 ? 0xffffffffu : ((1u << (8 * M)) - 1u);
+  constexpr uint32_t K1 = M > 4 ? ((1u << (8 * (M - 4))) - 1u) : 0u;
+#pragma unroll
+  for (int grp = 0; grp < 4; ++grp) {
+    uint32_t lo[8], hi[8], f[8], pass = 0;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int s0 = 33 + grp * 8 + kk - M;  // first byte of the window, in lb ++ v
+      lo[kk] = w64(lb, v, s0) & K0;
+      hi[kk] = M > 4 ? (w64(lb, v, s0 + 4) & K1) : 0u;
+      f[kk] = tiny_key_hash(lo[kk], hi[kk], th);
+      pass |= tiny_filter_test(bitmap, f[kk]) << kk;
+    }
+    pass &= vmask >> (grp * 8);
+    if (pass & 0xffu) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        if ((pass >> kk) & 1u) {
+          uint32_t s1, s2;
+          tiny_slots(f[kk], th, s1, s2);
+          const unsigned long long key = ((unsigned long long)hi[kk] << 32) | lo[kk];
+          const unsigned long long e1 = ld_shared_u64(slots + 8 * s1) ^ key;
+          const unsigned long long e2 = ld_shared_u64(slots + 8 * s2) ^ key;
+          // a hit leaves only the index (< 2^12) in the top 16 bits; empty slots are ~0
+          const bool h1 = (e1 & 0xffffffffffffull) == 0 && (e1 >> 48) < 0xffffull;
+          const bool h2 = (e2 & 0xffffffffffffull) == 0 && (e2 >> 48) < 0xffffull;
+          if (h1 || h2) {
+            const unsigned long long pos = atomicAdd(&a.counters[0], 1ull);
+            if (pos < a.cap) {
+              a.out_off[pos] = J + grp * 8 + kk - M + 1 - (int64_t)a.g.amis;
+              a.out_idx[pos] = (uint32_t)((h1 ? e1 : e2) >> 48);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(kMultiBlock) rk_multi_tiny_kernel(const __grid_constant__ MultiArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   MultiRing* rings = reinterpret_cast<MultiRing*>(smem);
-  uint32_t* sfilter = reinterpret_cast<uint32_t*>(smem + sizeof(MultiRing) * kMultiWarps);
-  for (int i = threadIdx.x; i < kMultiFilterWords; i += blockDim.x) sfilter[i] = a.grp[0].filter[i];
+  uint8_t* tab = smem + sizeof(MultiRing) * kMultiWarps;
+  const TinyHash th = a.grp[0].tiny_hash;
+  const uint32_t n16 = (th.size * 8u + kTinyFilterBytes) / 16u;  // slots, then the filter
+  const uint4* src = reinterpret_cast<const uint4*>(a.grp[0].tiny);
+  for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) reinterpret_cast<uint4*>(tab)[i] = src[i];
   __syncthreads();
+  const uint32_t slots = smem_u32(tab);
+  const uint32_t bitmap = slots + th.size * 8u;
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -266,21 +320,19 @@ __global__ void __launch_bounds__(kMultiBlock) rk_multi_short_kernel(const __gri
   const uint64_t w = (uint64_t)blockIdx.x * kMultiWarps + warp;
   Stream S;
   stream_init(a.g, R, S, (uint32_t)w, (uint32_t)W, lane);
-  const auto pred = [sfilter](uint32_t L) { return filter_test(sfilter, L); };
   for (uint32_t t = (uint32_t)w; t < (uint32_t)a.g.num_tiles; t += (uint32_t)W) {
     const int64_t ta = a.g.tile_a(t);
-    uint32_t cand = fast_tile<M, false>(a.g, R, S, t, lane, pred);
-    while (cand) {
-      const int c = __ffs(cand) - 1;
-      cand &= cand - 1;
-      multi_exact<M>(a, ta + c * kChunk + lane * kR, lane);
-    }
+    const bool full = ta >= (int64_t)a.g.ja_lo && ta + kTile <= (int64_t)a.g.ja_hi;
+    stream_tile<M, false>(a.g, R, S, t, lane,
+                          [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J, int) {
+                            tiny_chunk<M>(a, v, lb, J, full ? 0xffffffffu : valid_mask(a.g, J),
+                                          slots, bitmap, th);
+                          });
   }
 }
 
 template <class K>
-int multi_occupancy(K kernel) {
-  const size_t smem = multi_smem_bytes();
+int multi_occupancy(K kernel, size_t smem) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int b = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kMultiBlock, smem);
@@ -289,8 +341,8 @@ int multi_occupancy(K kernel) {
 
 // (Attr is a per-kernel tag so each kernel opts in to > 48 KiB of smem once per device.)
 template <class Attr, class K>
-cudaError_t multi_launch_kernel(K kernel, const MultiArgs& a, int grid, cudaStream_t s) {
-  const size_t smem = multi_smem_bytes();
+cudaError_t multi_launch_kernel(K kernel, const MultiArgs& a, int grid, size_t smem,
+                                cudaStream_t s) {
   static bool attr[kMaxDevices] = {};
   int dev = 0;
   cudaGetDevice(&dev);

@@ -343,6 +343,21 @@ def test_multi_mixed_lengths_longer_than_text(gpu):
             assert r == rk.search_naive(text, ps[i]), (n, i, len(ps[i]))
 
 
+def test_multi_many_pairs_device_sorted(gpu):
+    """More pairs than the host round trip takes (4096): ordered on the device."""
+    rng = np.random.default_rng(83)
+    text = rng.integers(0, 2, 300000, dtype=np.uint8).tobytes()
+    pats = [bytes(rng.integers(0, 2, m, dtype=np.uint8)) for m in (3, 5, 8, 8, 9, 12, 20)]
+    out = rk.search_multi(text, pats)
+    ps, _, _ = oracle.pattern_set(pats)
+    total = 0
+    for i, r in out:
+        exp = rk.search_naive(text, ps[i])
+        assert r == exp, i
+        total += len(exp.offsets)
+    assert total > 20000
+
+
 def test_multi_plan_cache_keys_on_bytes(gpu):
     """The per-context plan cache must not confuse sets that differ only in pattern bytes
     (equal lengths and hashes: "ac" / "ba", tests/test_matcher.py:139-146 of the reference)."""
