@@ -95,18 +95,33 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
     }
     return;
   }
+  // the hit masks of a tile come in one round of independent loads, issued while the
+  // previous tile is being expanded (not one load latency per chunk)
+  uint32_t hms[kTileChunks], nxt[kTileChunks];
+  auto fetch = [&](int j, uint32_t(&dst)[kTileChunks]) {
+    const uint64_t tseq = b * kEmitTiles + warp * 32 + j;
+    const uint32_t fl = __shfl_sync(kFull, info, j) >> 16;
+    const uint32_t* tm = e.masks + tseq * (kTileChunks * 32);
+#pragma unroll
+    for (int c = 0; c < kTileChunks; ++c) dst[c] = ((fl >> c) & 1u) ? tm[c * 32 + lane] : 0u;
+  };
+  int jn = todo ? __ffs(todo) - 1 : -1;
+  if (jn >= 0) fetch(jn, nxt);
   while (todo) {
-    const int j = __ffs(todo) - 1;
+    const int j = jn;
     todo &= todo - 1;
+#pragma unroll
+    for (int c = 0; c < kTileChunks; ++c) hms[c] = nxt[c];
+    jn = todo ? __ffs(todo) - 1 : -1;
+    if (jn >= 0) fetch(jn, nxt);
     const uint64_t tseq = b * kEmitTiles + warp * 32 + j;
     uint32_t flags = __shfl_sync(kFull, info, j) >> 16;
     uint64_t run = __shfl_sync(kFull, excl, j);
     const int64_t tile_a = (int64_t)((e.tile0 + tseq) * (uint64_t)kTile);
-    const uint32_t* tm = e.masks + tseq * (kTileChunks * 32);
-    while (flags) {
-      const int c = __ffs(flags) - 1;
-      flags &= flags - 1;
-      uint32_t hm = tm[c * 32 + lane];
+#pragma unroll
+    for (int c = 0; c < kTileChunks; ++c) {
+      if (!((flags >> c) & 1u)) continue;
+      uint32_t hm = hms[c];
       const int64_t chunk0 = tile_a + c * kChunk + e.start_bias;  // value of window 0
       if (__all_sync(kFull, hm == 0xffffffffu)) {
         // all 1024 windows match: a contiguous arithmetic run
