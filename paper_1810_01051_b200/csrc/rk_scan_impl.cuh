@@ -153,6 +153,24 @@ __device__ __forceinline__ void short_chunk(const ScanArgs& a, const Vec32& v,
                                             const uint32_t (&lb)[8], bool full, uint32_t vmask,
                                             uint32_t& hm, uint32_t& hits) {
   static_assert(M <= 8, "dot-product hashes need M <= 8");
+  if constexpr (M == 1) {
+    // the hash of a 1-byte window is the byte: four windows per SIMD byte compare, and
+    // a hash hit is a match iff hx is the pattern's own hash (hx is a parameter)
+    if (a.hx > 255u) return;  // no byte hashes to hx
+    const uint32_t splat = (uint32_t)a.hx * 0x01010101u;
+    uint32_t hmask = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t eq = __vcmpeq4(v.w[i], splat) & 0x80808080u;
+      hmask |= ((eq * 0x00204081u) >> 28) << (4 * i);  // byte MSBs -> 4 window bits
+    }
+    hmask &= vmask;
+    hits += __popc(hmask);
+    if (a.hx == (a.pw.w[0] & 0xffu)) hm |= hmask;
+    (void)full;
+    (void)lb;
+    return;
+  }
   const uint32_t negT = 0u - (uint32_t)a.hx;
   constexpr uint32_t W0 = win_weights<M>(0), W1 = win_weights<M>(1);
   constexpr uint32_t K0 = M >= 4 ? 0xffffffffu : ((1u << (8 * M)) - 1u);

@@ -103,10 +103,11 @@ def test_foreign_hx_semantics(gpu):
     byte-verified against the pattern bytes."""
     rng = np.random.default_rng(5)
     host = rng.integers(97, 100, 5000, dtype=np.uint8)
-    for m in (2, 8, 30, 40, 70):
+    for m, hx_kind in [(1, "other"), (1, "big"), (2, "other"), (4, "other"), (8, "other"),
+                       (30, "other"), (40, "other"), (70, "other")]:
         pat = host[100 : 100 + m]
-        other = host[200 : 200 + m]
-        hx = oracle.hash_full(other.tobytes())
+        other = host[200 : 200 + m] if m > 1 else np.array([98], dtype=np.uint8)
+        hx = oracle.hash_full(other.tobytes()) if hx_kind == "other" else 1000
         lib = oracle.load()
         import ctypes
 
