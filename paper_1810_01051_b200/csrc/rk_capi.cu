@@ -336,9 +336,9 @@ TextGeom text_geom(const Geometry& g, uint64_t n, uint32_t m, uint64_t seq_base)
 }
 
 // Persistent grid: every SM full, never more warps than tiles.
-int grid_for(uint64_t tiles, int num_sms, int blocks_per_sm) {
+int grid_for(uint64_t tiles, int num_sms, int blocks_per_sm, int warps_per_block) {
   const uint64_t max_grid = (uint64_t)num_sms * (uint64_t)blocks_per_sm;
-  const uint64_t want = (tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const uint64_t want = (tiles + warps_per_block - 1) / warps_per_block;
   return (int)std::max<uint64_t>(1, std::min(max_grid, want));
 }
 
@@ -354,7 +354,8 @@ int launch_one(rk_ctx* c, const uint8_t* d_text, uint64_t n, uint32_t m, uint64_
   a.tile_info = c->d_tile_info;
   a.masks = c->d_masks;
   a.pw = pw;
-  RK_CUDA(launch_scan(a, grid_for(g.num_tiles, c->num_sms, scan_blocks_per_sm(m)), s));
+  RK_CUDA(launch_scan(a, grid_for(g.num_tiles, c->num_sms, scan_blocks_per_sm(m), scan_warps(m)),
+                      s));
   ++c->launches;
   return RK_OK;
 }

@@ -18,7 +18,14 @@ struct ScanArgs {
   uint32_t* masks;                // per sequence number: kTileChunks x 32 lane hit masks
   PatWords pw;
 };
-size_t scan_smem_bytes();
+// Shape of the scan kernel per pattern length: m >= 32 (one running fold, the least work
+// per byte) streams 8 KiB stages -- one TMA copy and one ring hand-off per tile -- with 12
+// warps per SM; the shorter paths keep 4 KiB stages and 3 x 8 warps per SM, the latency
+// cover their longer per-byte work needs.
+__host__ __device__ constexpr int scan_warps(uint32_t m) { return m >= 32 ? 12 : 8; }
+__host__ __device__ constexpr int scan_stage_chunks(uint32_t m) { return m >= 32 ? 8 : 4; }
+__host__ __device__ constexpr int scan_min_blocks(uint32_t m) { return m >= 32 ? 1 : 3; }
+size_t scan_smem_bytes(uint32_t m);
 int scan_blocks_per_sm(uint32_t m);
 cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t s);
 

@@ -22,7 +22,10 @@ using ScanTable = Table<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 1
                         21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32>;
 static int variant_of(uint32_t m) { return m >= 32 ? 31 : (int)m - 1; }
 
-size_t scan_smem_bytes() { return sizeof(WarpRing) * kWarpsPerBlock; }
+size_t scan_smem_bytes(uint32_t m) {
+  return m >= 32 ? sizeof(WarpRingT<scan_stage_chunks(32)>) * scan_warps(32)
+                 : sizeof(WarpRingT<scan_stage_chunks(1)>) * scan_warps(1);
+}
 
 int scan_blocks_per_sm(uint32_t m) {
   static int cache[32] = {0};  // same on every B200

@@ -282,7 +282,10 @@ __device__ __forceinline__ void finish_tile(const ScanArgs& a, uint64_t t, uint3
 }
 
 template <int M>
-__global__ void __launch_bounds__(kBlock, 3) rk_scan_kernel(const ScanArgs a) {
+__global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
+    rk_scan_kernel(const ScanArgs a) {
+  constexpr int kWarps = scan_warps(M);
+  using Ring = WarpRingT<scan_stage_chunks(M)>;
   // PDL both ways: wait for the previous grid in the stream (its writes -- the text, the
   // previous emit's reads of our scratch -- must be complete), and let the emit grid be
   // scheduled as our CTAs retire (it waits for our results the same way)
@@ -291,10 +294,10 @@ __global__ void __launch_bounds__(kBlock, 3) rk_scan_kernel(const ScanArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  WarpRing* R = reinterpret_cast<WarpRing*>(smem) + warp;
+  Ring* R = reinterpret_cast<Ring*>(smem) + warp;
   ring_init(R, lane);
-  const uint64_t W = (uint64_t)gridDim.x * kWarpsPerBlock;
-  const uint64_t w = (uint64_t)blockIdx.x * kWarpsPerBlock + warp;
+  const uint64_t W = (uint64_t)gridDim.x * kWarps;
+  const uint64_t w = (uint64_t)blockIdx.x * kWarps + warp;
   const uint32_t T = (uint32_t)a.hx;
   const auto pred = [T](uint32_t L) { return L == T; };
   Stream S;
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(kBlock, 3) rk_scan_kernel(const ScanArgs a) {
 
 template <int M>
 cudaError_t launch_m(const ScanArgs& a, int grid, cudaStream_t s) {
-  const size_t smem = scan_smem_bytes();
+  const size_t smem = scan_smem_bytes(M);
   static bool attr[kMaxDevices] = {};  // per-variant, per-device opt-in to > 48 KiB smem
   int dev = 0;
   cudaGetDevice(&dev);
@@ -372,7 +375,7 @@ cudaError_t launch_m(const ScanArgs& a, int grid, cudaStream_t s) {
   // kernel waits for that grid's completion before touching memory (griddepcontrol.wait)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kBlock);
+  cfg.blockDim = dim3(32 * scan_warps(M));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -386,9 +389,10 @@ cudaError_t launch_m(const ScanArgs& a, int grid, cudaStream_t s) {
 template <int M>
 int occupancy_m() {
   cudaFuncSetAttribute(rk_scan_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)scan_smem_bytes());
+                       (int)scan_smem_bytes(M));
   int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rk_scan_kernel<M>, kBlock, scan_smem_bytes());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rk_scan_kernel<M>, 32 * scan_warps(M),
+                                                scan_smem_bytes(M));
   return b > 0 ? b : 1;
 }
 
