@@ -237,12 +237,6 @@ __device__ __forceinline__ unsigned long long ld_shared_u64(uint32_t a) {
   return v;
 }
 
-__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
-}
-
 // Blocked Bloom filter of the keys: 2048 blocks of 64 bits, 4 bits per key (2 per half),
 // one LDS.64 per window; ~5e-5 false positives per window at 1024 patterns, so a group
 // of 8 windows rarely leaves the fast path.
