@@ -209,7 +209,9 @@ __device__ __forceinline__ uint32_t dp4a_us(uint32_t a, uint32_t b, uint32_t c) 
 //  M < 32: exact roll L' = 2L + in - 2^M out seeded with the fold of the M bytes before
 //    J, alternating two instruction mixes so the ALU and FMA pipes carry ~2.5
 //    instructions per byte each.
-template <int M, class Pred>
+// (FmaBytes: take b1 with a one-hot dp4a on the FMA pipe instead of a PRMT -- for callers
+// whose compares load the ALU pipe, e.g. the masked compares of the fold filter.)
+template <int M, bool FmaBytes = false, class Pred>
 __device__ __forceinline__ bool fast_chunk(const Vec32& v, const uint32_t (&lb)[8], int lane,
                                            uint32_t& carryS, const RollConsts& K, Pred pred) {
   bool any = false;
@@ -227,8 +229,10 @@ __device__ __forceinline__ bool fast_chunk(const Vec32& v, const uint32_t (&lb)[
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t w = v.w[i];
-      const uint32_t s1 = S * K.k2 + bsel(w, 0);
-      const uint32_t s2 = s1 * K.k2 + bsel(w, 1);
+      const uint32_t s1 =
+          FmaBytes ? __dp4a(w, 0x00000001u, S * K.k2) : S * K.k2 + bsel(w, 0);
+      const uint32_t s2 =
+          FmaBytes ? __dp4a(w, 0x00000100u, s1 * K.k2) : s1 * K.k2 + bsel(w, 1);
       const uint32_t s3 = S * K.k8 + __dp4a(w, 0x00010204u, 0u);
       const uint32_t s4 = S * K.k16 + c4[i];
       any |= pred(s1);

@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
       stream_tile<32>(a.g, R, S, t, lane,
                       [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t& carryS, int64_t,
                           int c) {
-                        const bool any = fast_chunk<32>(v, lb, lane, carryS, a.g.K, fpred);
+                        const bool any = fast_chunk<32, true>(v, lb, lane, carryS, a.g.K, fpred);
                         if (__any_sync(kFull, any)) cand |= 1u << c;
                       });
       finish_tile<M>(a, t, cand, lane, tot);
