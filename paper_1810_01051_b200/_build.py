@@ -19,8 +19,11 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-BUILD = ROOT / "build" / "rkb200"
-LIB = PKG / "librkb200.so"
+# RK_DEFINES / RK_LIB_OUT: build a variant library (extra -D flags, another output path)
+# for A/B timing with tools/ (the package itself always loads librkb200.so)
+BUILD = ROOT / "build" / ("rkb200" + os.environ.get("RK_LIB_TAG", ""))
+LIB = Path(os.environ["RK_LIB_OUT"]).resolve() if os.environ.get("RK_LIB_OUT") else PKG / "librkb200.so"
+DEFINES = os.environ.get("RK_DEFINES", "").split()
 SOURCES = ["rk_scan.cu", *[f"rk_scan_g{g}.cu" for g in range(4)], "rk_multi.cu",
            "rk_multi_g0.cu", "rk_pairs.cu", "rk_emit.cu", "rk_aux.cu", "rk_capi.cu"]
 HEADERS = ["rk_device.cuh", "rk_internal.h", "rk_scan_impl.cuh", "rk_multi_impl.cuh"]
@@ -54,7 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(src: str) -> Path:
         obj = BUILD / (Path(src).stem + ".o")
-        cmd = [cc, *ARCH, *NVFLAGS, *inc, "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [cc, *ARCH, *NVFLAGS, *DEFINES, *inc, "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

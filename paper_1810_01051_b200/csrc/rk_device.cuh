@@ -21,6 +21,7 @@
 // in flight live in shared memory, not registers.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace rkb {
@@ -195,6 +196,25 @@ __device__ __forceinline__ uint32_t dp4a_us(uint32_t a, uint32_t b, uint32_t c) 
   return d;
 }
 
+// Masked-equality filter test: L is a candidate iff ((L ^ T) & mask) == 0.  Its windows
+// are accumulated with lop3's predicate output (PTX lop3.and: p = (result != 0) AND q), so
+// each window costs one LOP3.PAND and no separate predicate-combining PLOP3.
+struct MaskedEq {
+  uint32_t T, mask;
+};
+
+// q && ((a ^ b) & c) != 0, in one LOP3.LUT.PAND (ptxas folds the selp/setp wrapper)
+__device__ __forceinline__ bool lop3_nz_and(uint32_t a, uint32_t b, uint32_t c, bool q) {
+  uint32_t r;
+  asm("{.reg .pred p, qq;\n"
+      "setp.ne.u32 qq, %4, 0;\n"
+      "lop3.and.b32 _|p, %1, %2, %3, 0x28, qq;\n"
+      "selp.u32 %0, 1, 0, p;}\n"
+      : "=r"(r)
+      : "r"(a), "r"(b), "r"(c), "r"((uint32_t)q));
+  return r != 0;
+}
+
 // ---------------------------------------------------------------------------------
 // The fast roll over one chunk: the lane owns window END positions [J, J+32), its 32
 // bytes in v; for M < 32, lb holds the 32 bytes before J.  Returns whether
@@ -209,13 +229,23 @@ __device__ __forceinline__ uint32_t dp4a_us(uint32_t a, uint32_t b, uint32_t c) 
 //  M < 32: exact roll L' = 2L + in - 2^M out seeded with the fold of the M bytes before
 //    J, alternating two instruction mixes so the ALU and FMA pipes carry ~2.5
 //    instructions per byte each.
-// (FmaBytes: take b1 with a one-hot dp4a on the FMA pipe instead of a PRMT -- for callers
-// whose compares load the ALU pipe, e.g. the masked compares of the fold filter.)
+// (FmaBytes: take b0/b1 with a one-hot dp4a on the FMA pipe instead of a PRMT -- for
+// callers whose compares load the ALU pipe.)  pred is either a callable (candidate iff
+// pred(L)) or a MaskedEq (M >= 32 chain only), accumulated as "all windows miss".
 template <int M, bool FmaBytes = false, class Pred>
 __device__ __forceinline__ bool fast_chunk(const Vec32& v, const uint32_t (&lb)[8], int lane,
                                            uint32_t& carryS, const RollConsts& K, Pred pred) {
   bool any = false;
   if constexpr (M >= 32) {
+    constexpr bool kMasked = std::is_same<Pred, MaskedEq>::value;
+    bool allnz = true;
+    const auto test = [&](uint32_t s) {
+      if constexpr (kMasked) {
+        allnz = lop3_nz_and(s, pred.T, pred.mask, allnz);
+      } else {
+        any |= pred(s);
+      }
+    };
     uint32_t c4[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) c4[i] = __dp4a(v.w[i], kFoldW, 0u);
@@ -235,12 +265,13 @@ __device__ __forceinline__ bool fast_chunk(const Vec32& v, const uint32_t (&lb)[
           FmaBytes ? __dp4a(w, 0x00000100u, s1 * K.k2) : s1 * K.k2 + bsel(w, 1);
       const uint32_t s3 = S * K.k8 + __dp4a(w, 0x00010204u, 0u);
       const uint32_t s4 = S * K.k16 + c4[i];
-      any |= pred(s1);
-      any |= pred(s2);
-      any |= pred(s3);
-      any |= pred(s4);
+      test(s1);
+      test(s2);
+      test(s3);
+      test(s4);
       S = s4;
     }
+    if constexpr (kMasked) any = !allnz;
   } else {
     uint32_t L = fold_tail<M>(lb);
 #pragma unroll
@@ -333,7 +364,16 @@ struct Stream {
   uint32_t pslot;       // ring slot the producer fills next
   uint32_t W, int_lo, int_hi, ntiles;
   int64_t tile_jump;    // bytes from the end of one of the warp's tiles to its next one
+  uint32_t cur;         // during op(): shared-space address of the current chunk's bytes
+                        // from its 32-byte lookback on, or 0 (edge tiles: read from global)
 };
+
+// 4 bytes of shared memory at shared-space address a (4-byte aligned)
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t x;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(a));
+  return x;
+}
 
 __device__ __forceinline__ void stream_seek(const TextGeom& g, Stream& S) {
   while (S.pt < S.ntiles && (S.pt < S.int_lo || S.pt >= S.int_hi)) S.pt += S.W;
@@ -407,6 +447,7 @@ __device__ __forceinline__ void stream_tile(const TextGeom& g, WarpRingT<SC>* R,
           for (int i = 0; i < 8; ++i) lb[i] = l.w[i];
         }
         const int c = s * SC + j;
+        S.cur = smem_u32(st) + j * kChunk;
         op(v, lb, carryS, ta + c * kChunk + lane * kR, c);
       }
       // the slot's bytes are consumed: hand it back to the producer
@@ -418,6 +459,7 @@ __device__ __forceinline__ void stream_tile(const TextGeom& g, WarpRingT<SC>* R,
     }
   } else {
     if constexpr (M >= 32) carryS = fold32(load_edge(g, ta - 32).w);
+    S.cur = 0;
 #pragma unroll 1
     for (int c = 0; c < kTileChunks; ++c) {
       const int64_t J = ta + c * kChunk + lane * kR;

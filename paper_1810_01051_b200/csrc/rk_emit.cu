@@ -158,7 +158,18 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
   }
 }
 
-size_t emit_smem_bytes() { return (size_t)kEmitWarps * kPadded * sizeof(int64_t); }
+// The emit grid is launched as a programmatic dependent of the scan, so its CTAs are
+// placed as scan CTAs retire: with a small footprint several would pile onto the first SMs
+// to free up (a dense emit then ran on a third of the SMs, 2.4x slower).  Reserving more
+// than half an SM's shared memory keeps it to one CTA per SM.
+#ifndef RK_EMIT_MIN_SMEM_KB
+#define RK_EMIT_MIN_SMEM_KB 116
+#endif
+constexpr size_t kEmitMinSmem = RK_EMIT_MIN_SMEM_KB * 1024;
+size_t emit_smem_bytes() {
+  const size_t b = (size_t)kEmitWarps * kPadded * sizeof(int64_t);
+  return b < kEmitMinSmem ? kEmitMinSmem : b;
+}
 
 cudaError_t launch_emit(const EmitArgs& e, cudaStream_t s) {
   const uint64_t blocks = (e.num_tiles + kEmitTiles - 1) / kEmitTiles;
@@ -182,7 +193,7 @@ cudaError_t launch_emit(const EmitArgs& e, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[0].val.programmaticStreamSerializationAllowed = RK_PDL;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, rk_emit_kernel, e);

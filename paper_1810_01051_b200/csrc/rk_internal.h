@@ -22,9 +22,32 @@ struct ScanArgs {
 // per byte) streams 8 KiB stages -- one TMA copy and one ring hand-off per tile -- with 12
 // warps per SM; the shorter paths keep 4 KiB stages and 3 x 8 warps per SM, the latency
 // cover their longer per-byte work needs.
-__host__ __device__ constexpr int scan_warps(uint32_t m) { return m >= 32 ? 12 : 8; }
-__host__ __device__ constexpr int scan_stage_chunks(uint32_t m) { return m >= 32 ? 8 : 4; }
-__host__ __device__ constexpr int scan_min_blocks(uint32_t m) { return m >= 32 ? 1 : 3; }
+#ifndef RK_PDL
+#define RK_PDL 1  // programmatic dependent launch of the scan and emit grids
+#endif
+#ifndef RK_WIDE_FROM
+#define RK_WIDE_FROM 15
+#endif
+#ifndef RK_SHORT_FROM
+#define RK_SHORT_FROM 5
+#endif
+#ifndef RK_SHORT_W
+#define RK_SHORT_W 16
+#define RK_SHORT_S 4
+#define RK_SHORT_B 1
+#endif
+struct ScanShape {
+  int warps, stage_chunks, min_blocks;
+};
+constexpr uint32_t kWideFrom = RK_WIDE_FROM;  // first m with the wide shape
+__host__ __device__ constexpr ScanShape scan_shape(uint32_t m) {
+  return m >= kWideFrom ? ScanShape{12, 8, 1}
+                        : (m >= RK_SHORT_FROM && m <= 8 ? ScanShape{RK_SHORT_W, RK_SHORT_S, RK_SHORT_B}
+                                                        : ScanShape{8, 4, 3});
+}
+__host__ __device__ constexpr int scan_warps(uint32_t m) { return scan_shape(m).warps; }
+__host__ __device__ constexpr int scan_stage_chunks(uint32_t m) { return scan_shape(m).stage_chunks; }
+__host__ __device__ constexpr int scan_min_blocks(uint32_t m) { return scan_shape(m).min_blocks; }
 size_t scan_smem_bytes(uint32_t m);
 int scan_blocks_per_sm(uint32_t m);
 cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t s);

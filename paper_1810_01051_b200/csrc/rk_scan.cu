@@ -23,8 +23,16 @@ using ScanTable = Table<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 1
 static int variant_of(uint32_t m) { return m >= 32 ? 31 : (int)m - 1; }
 
 size_t scan_smem_bytes(uint32_t m) {
-  return m >= 32 ? sizeof(WarpRingT<scan_stage_chunks(32)>) * scan_warps(32)
-                 : sizeof(WarpRingT<scan_stage_chunks(1)>) * scan_warps(1);
+  // per warp: its TMA ring + the short-pattern settle scratch (rk_scan_impl.cuh)
+  const size_t scratch = 20 * sizeof(uint32_t);
+  size_t b;
+  switch (scan_stage_chunks(m)) {
+    case 8: b = (sizeof(WarpRingT<8>) + scratch) * scan_warps(m); break;
+    case 4: b = (sizeof(WarpRingT<4>) + scratch) * scan_warps(m); break;
+    case 2: b = (sizeof(WarpRingT<2>) + scratch) * scan_warps(m); break;
+    default: b = (sizeof(WarpRingT<1>) + scratch) * scan_warps(m); break;
+  }
+  return b;
 }
 
 int scan_blocks_per_sm(uint32_t m) {

@@ -136,6 +136,10 @@ constexpr int kShortInline = 9;
 // beats the exact roll from M = 15 (measured: m = 20 4.74 vs 4.27 TB/s, m = 15 4.54 vs 4.3,
 // m = 14 4.27 vs 4.3).
 constexpr int kFoldFilter = 15;
+#ifndef RK_FOLD_FMA_BYTES
+#define RK_FOLD_FMA_BYTES 0
+#endif
+constexpr bool kFoldFmaBytes = RK_FOLD_FMA_BYTES;
 
 // M <= 8: the whole hash of a window is a dot product of its (at most two) words with
 // the weights 2^(M-1-i), so there is no serial roll chain: per window one funnel shift
@@ -226,6 +230,109 @@ __device__ __forceinline__ void short_chunk(const ScanArgs& a, const Vec32& v,
   }
 }
 
+// M in [2, 8]: lane-flag fast pass + warp-cooperative settle.
+// The fast pass only answers "does some window of the lane's chunk have hash == hx": the
+// d = hash - hx of two neighbouring windows are multiplied (|d| < 2^16, so the product is
+// exact and zero iff one of them is) and the products tested with one accumulated ISETP,
+// i.e. per window one dp4a (two for M > 4), half an IMAD and half an ISETP, plus the
+// funnel shift that forms the window word.  Lanes whose chunk has a hash hit (m = 4 over
+// printable ASCII: ~2.6% of lane-chunks; m = 8: ~0.2%) are settled one at a time by the
+// whole warp: the flagged lane publishes its 64 bytes in a per-warp scratch, each lane
+// takes one of its 32 windows (exact hash, validity, bytes) and two ballots give the hit
+// count and the match mask.  A chunk with many flagged lanes (dense matches, e.g. all 'a')
+// goes to the per-lane inline settle instead (short_chunk).
+constexpr int kCoopFrom = 5;
+// M <= this: test the windows in pairs by the product of their d's (moves half the
+// compares to the FMA pipe); longer patterns already load the FMA pipe with two dp4a per
+// window and test each d directly
+constexpr int kPairProductsTo = 4;
+constexpr int kCoopMaxLanes = 6;
+constexpr int kScratchWords = 20;  // 64 bytes + padding for the last window (16-B aligned)
+
+template <int M>
+__device__ __forceinline__ bool short_any(const ScanArgs& a, const Vec32& v,
+                                          const uint32_t (&lb)[8]) {
+  static_assert(M >= 2 && M <= 8, "two-word dot products");
+  const uint32_t negT = 0u - (uint32_t)a.hx;
+  constexpr uint32_t W0 = win_weights<M>(0), W1 = win_weights<M>(1);
+  uint32_t d[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const int s0 = 33 + k - M;
+    if constexpr (M > 4) {
+      d[k] = __dp4a(w64(lb, v, s0), W0, __dp4a(w64(lb, v, s0 + 4), W1, negT));
+    } else {
+      d[k] = __dp4a(w64(lb, v, s0), W0, negT);
+    }
+  }
+  bool any = false;
+  if constexpr (M > kPairProductsTo) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) any |= (d[k] == 0u);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 32; k += 2) any |= (d[k] * d[k + 1] == 0u);
+  }
+  return any;
+}
+
+// Settles the flagged lanes of one chunk (see above).  sp = the chunk's bytes in shared
+// memory from its 32-byte lookback on (the TMA stage), or null for edge tiles, whose
+// flagged lanes publish their 64 bytes in the warp's scratch first.  Adds to the caller's
+// per-lane hit and match counts; returns the lane's match mask for the chunk.
+template <int M>
+__device__ __forceinline__ uint32_t coop_settle(const ScanArgs& a, uint32_t sp, const Vec32& v,
+                                                const uint32_t (&lb)[8], int64_t J, bool full,
+                                                unsigned flags, int lane, uint32_t* scratch,
+                                                uint32_t& my_hits, uint32_t& my_matches) {
+  const uint32_t negT = 0u - (uint32_t)a.hx;
+  constexpr uint32_t W0 = win_weights<M>(0), W1 = win_weights<M>(1);
+  constexpr uint32_t K0 = M >= 4 ? 0xffffffffu : ((1u << (8 * M)) - 1u);
+  constexpr uint32_t K1 = M >= 8 ? 0xffffffffu : M > 4 ? ((1u << (8 * (M - 4))) - 1u) : 0u;
+  const bool staged = sp != 0u;
+  if (!staged) sp = smem_u32(scratch);
+  // this lane takes the window ending at byte 32 + lane of lane L's 64 bytes (lb ++ v),
+  // i.e. starting at byte 33 + lane - M; a staged chunk holds lane L's bytes at 32 L
+  const uint32_t off = 33u + lane - M;
+  const uint32_t base = sp + (off & ~3u), r = 8u * (off & 3u);
+  uint32_t hm = 0;
+  while (flags) {
+    const int L = __ffs(flags) - 1;
+    flags &= flags - 1;
+    uint32_t p = base;
+    if (staged) {
+      p += 32u * L;
+    } else {
+      if (lane == L) {
+        uint4* dst = reinterpret_cast<uint4*>(scratch);
+        dst[0] = make_uint4(lb[0], lb[1], lb[2], lb[3]);
+        dst[1] = make_uint4(lb[4], lb[5], lb[6], lb[7]);
+        dst[2] = make_uint4(v.w[0], v.w[1], v.w[2], v.w[3]);
+        dst[3] = make_uint4(v.w[4], v.w[5], v.w[6], v.w[7]);
+      }
+      __syncwarp();
+    }
+    const uint32_t x1 = lds_u32(p + 4);
+    const uint32_t A = __funnelshift_r(lds_u32(p), x1, r);
+    uint32_t d, B = 0;
+    if constexpr (M > 4) {
+      B = __funnelshift_r(x1, lds_u32(p + 8), r);
+      d = __dp4a(A, W0, __dp4a(B, W1, negT));
+    } else {
+      d = __dp4a(A, W0, negT);
+    }
+    // a-space end position: lane L's chunk bytes start 32 (L - lane) after ours
+    const bool hit = d == 0u && (full || a.g.valid_end(J + 32 * (L - lane) + lane));
+    const bool eq = hit && ((A ^ a.pw.w[0]) & K0) == 0u && ((B ^ a.pw.w[1]) & K1) == 0u;
+    my_hits += hit;
+    my_matches += eq;
+    const unsigned em = __ballot_sync(kFull, eq);
+    if (lane == L) hm = em;
+    if (!staged) __syncwarp();  // the scratch is rewritten for the next flagged lane
+  }
+  return hm;
+}
+
 // Per-warp totals of hash hits and matches, flushed to the global counters once per
 // warp at the end of the kernel (m = 4 hits most tiles: a per-tile atomic on one address
 // from every warp would serialise in its L2 slice).
@@ -295,6 +402,9 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   Ring* R = reinterpret_cast<Ring*>(smem) + warp;
+  uint32_t* scratch =
+      reinterpret_cast<uint32_t*>(smem + kWarps * sizeof(Ring)) + warp * kScratchWords;
+  (void)scratch;
   ring_init(R, lane);
   const uint64_t W = (uint64_t)gridDim.x * kWarps;
   const uint64_t w = (uint64_t)blockIdx.x * kWarps + warp;
@@ -303,6 +413,8 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
   Stream S;
   stream_init(a.g, R, S, (uint32_t)w, (uint32_t)W, lane);
   WarpTotals tot;
+  bool dense = false;  // warp-uniform: the last settled chunk of M <= 8 had dense hits
+  (void)dense;
   for (uint32_t t = (uint32_t)w; t < (uint32_t)a.g.num_tiles; t += (uint32_t)W) {
     if constexpr (M >= 32) {
       // candidates are ~2^-32 per window: one vote per tile, and a tile with any
@@ -316,16 +428,16 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
     } else if constexpr (M >= kFoldFilter) {
       // the 32-byte fold S(j) agrees with the window hash mod 2^M (the out-term is a
       // multiple of 2^M), so the m >= 32 chain with a masked compare is an exact-hit
-      // filter (false positives ~2^-M per window); flagged chunks get the exact pass
-      // (a literal 0xffff would be matched to PRMT half-word extracts instead of one
-      // predicate-producing LOP3, so M = 16 takes it from a kernel argument)
-      const uint32_t mask = M == 16 ? ~a.g.K.negpow : (1u << M) - 1u;
-      const auto fpred = [T, mask](uint32_t L) { return ((L ^ T) & mask) == 0u; };
+      // filter (false positives ~2^-M per window); flagged chunks get the exact pass.
+      // The masked compares accumulate through lop3's predicate output (one LOP3 per
+      // window, as the ISETP.EQ.OR of m >= 32).
+      const MaskedEq fpred{T, (uint32_t)((1ull << M) - 1u)};
       uint32_t cand = 0;
       stream_tile<32>(a.g, R, S, t, lane,
                       [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t& carryS, int64_t,
                           int c) {
-                        const bool any = fast_chunk<32, true>(v, lb, lane, carryS, a.g.K, fpred);
+                        const bool any =
+                            fast_chunk<32, kFoldFmaBytes>(v, lb, lane, carryS, a.g.K, fpred);
                         if (__any_sync(kFull, any)) cand |= 1u << c;
                       });
       finish_tile<M>(a, t, cand, lane, tot);
@@ -343,9 +455,29 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
       stream_tile<M, false>(a.g, R, S, t, lane,
                             [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J,
                                 int c) {
-                       uint32_t hm = 0, hits = 0;
+                       uint32_t hm = 0;
+                       if constexpr (M >= kCoopFrom) {
+                         if (!dense) {
+                           const unsigned flags = __ballot_sync(kFull, short_any<M>(a, v, lb));
+                           if (!flags) return;
+                           if (__popc(flags) <= kCoopMaxLanes) {
+                             hm = coop_settle<M>(a, S.cur, v, lb, J, full, flags, lane,
+                                                 scratch, my_hits, my_matches);
+                             if (__ballot_sync(kFull, hm != 0)) {
+                               tmask[c * 32 + lane] = hm;
+                               hitflags |= 1u << c;
+                             }
+                             return;
+                           }
+                         }
+                       }
+                       uint32_t hits = 0;
                        short_chunk<M>(a, v, lb, full, full ? 0xffffffffu : valid_mask(a.g, J),
                                       hm, hits);
+                       // dense hits (e.g. all 'a'): stay on the inline settle, skipping the
+                       // flag pass, while most lanes keep hitting
+                       if constexpr (M >= kCoopFrom)
+                         dense = __popc(__ballot_sync(kFull, hits != 0)) > kCoopMaxLanes;
                        my_hits += hits;
                        my_matches += __popc(hm);
                        if (__ballot_sync(kFull, hm != 0)) {
@@ -380,7 +512,7 @@ cudaError_t launch_m(const ScanArgs& a, int grid, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[0].val.programmaticStreamSerializationAllowed = RK_PDL;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, rk_scan_kernel<M>, a);
