@@ -241,7 +241,13 @@ __device__ __forceinline__ void short_chunk(const ScanArgs& a, const Vec32& v,
 // takes one of its 32 windows (exact hash, validity, bytes) and two ballots give the hit
 // count and the match mask.  A chunk with many flagged lanes (dense matches, e.g. all 'a')
 // goes to the per-lane inline settle instead (short_chunk).
-constexpr int kCoopFrom = 5;
+#ifndef RK_COOP_FROM
+#define RK_COOP_FROM 5
+#endif
+constexpr int kCoopFrom = RK_COOP_FROM;
+#ifndef RK_UNROLL_FROM
+#define RK_UNROLL_FROM 5  // chunk loop unrolled per stage (M >= this)
+#endif
 // M <= this: test the windows in pairs by the product of their d's (moves half the
 // compares to the FMA pipe); longer patterns already load the FMA pipe with two dp4a per
 // window and test each d directly
@@ -282,36 +288,24 @@ __device__ __forceinline__ bool short_any(const ScanArgs& a, const Vec32& v,
 // per-lane hit and match counts; returns the lane's match mask for the chunk.
 template <int M>
 __device__ __forceinline__ uint32_t coop_settle(const ScanArgs& a, uint32_t sp, const Vec32& v,
-                                                const uint32_t (&lb)[8], int64_t J, bool full,
+                                                const uint32_t (&lb)[8], int64_t J,
                                                 unsigned flags, int lane, uint32_t* scratch,
                                                 uint32_t& my_hits, uint32_t& my_matches) {
   const uint32_t negT = 0u - (uint32_t)a.hx;
   constexpr uint32_t W0 = win_weights<M>(0), W1 = win_weights<M>(1);
   constexpr uint32_t K0 = M >= 4 ? 0xffffffffu : ((1u << (8 * M)) - 1u);
   constexpr uint32_t K1 = M >= 8 ? 0xffffffffu : M > 4 ? ((1u << (8 * (M - 4))) - 1u) : 0u;
-  const bool staged = sp != 0u;
-  if (!staged) sp = smem_u32(scratch);
+  // valid window ends of the chunk, relative to its first end position (lane 0's J):
+  // window 32 L + lane is valid iff it lies in [vlo, vhi)
+  const int64_t J0 = J - kR * lane;
+  const uint32_t vlo = (uint32_t)min(max((int64_t)a.g.ja_lo - J0, (int64_t)0), (int64_t)kChunk);
+  const uint32_t vspan =
+      (uint32_t)min(max((int64_t)a.g.ja_hi - J0, (int64_t)0), (int64_t)kChunk) - vlo;
   // this lane takes the window ending at byte 32 + lane of lane L's 64 bytes (lb ++ v),
   // i.e. starting at byte 33 + lane - M; a staged chunk holds lane L's bytes at 32 L
-  const uint32_t off = 33u + lane - M;
-  const uint32_t base = sp + (off & ~3u), r = 8u * (off & 3u);
+  const uint32_t off = 33u + lane - M, r = 8u * (off & 3u);
   uint32_t hm = 0;
-  while (flags) {
-    const int L = __ffs(flags) - 1;
-    flags &= flags - 1;
-    uint32_t p = base;
-    if (staged) {
-      p += 32u * L;
-    } else {
-      if (lane == L) {
-        uint4* dst = reinterpret_cast<uint4*>(scratch);
-        dst[0] = make_uint4(lb[0], lb[1], lb[2], lb[3]);
-        dst[1] = make_uint4(lb[4], lb[5], lb[6], lb[7]);
-        dst[2] = make_uint4(v.w[0], v.w[1], v.w[2], v.w[3]);
-        dst[3] = make_uint4(v.w[4], v.w[5], v.w[6], v.w[7]);
-      }
-      __syncwarp();
-    }
+  const auto item = [&](uint32_t p, int L) {
     const uint32_t x1 = lds_u32(p + 4);
     const uint32_t A = __funnelshift_r(lds_u32(p), x1, r);
     uint32_t d, B = 0;
@@ -321,14 +315,37 @@ __device__ __forceinline__ uint32_t coop_settle(const ScanArgs& a, uint32_t sp, 
     } else {
       d = __dp4a(A, W0, negT);
     }
-    // a-space end position: lane L's chunk bytes start 32 (L - lane) after ours
-    const bool hit = d == 0u && (full || a.g.valid_end(J + 32 * (L - lane) + lane));
-    const bool eq = hit && ((A ^ a.pw.w[0]) & K0) == 0u && ((B ^ a.pw.w[1]) & K1) == 0u;
+    const bool hit = (d == 0u) & ((uint32_t)(kR * L + lane) - vlo < vspan);
+    const bool eq = hit & (((A ^ a.pw.w[0]) & K0) == 0u) & (((B ^ a.pw.w[1]) & K1) == 0u);
     my_hits += hit;
     my_matches += eq;
     const unsigned em = __ballot_sync(kFull, eq);
-    if (lane == L) hm = em;
-    if (!staged) __syncwarp();  // the scratch is rewritten for the next flagged lane
+    hm = lane == L ? em : hm;
+  };
+  if (sp) {
+    const uint32_t base = sp + (off & ~3u);
+    while (flags) {
+      const int L = __ffs(flags) - 1;
+      flags &= flags - 1;
+      item(base + 32u * L, L);
+    }
+  } else {
+    // edge tile (not staged): the flagged lane publishes its 64 bytes first
+    const uint32_t base = smem_u32(scratch) + (off & ~3u);
+    while (flags) {
+      const int L = __ffs(flags) - 1;
+      flags &= flags - 1;
+      if (lane == L) {
+        uint4* dst = reinterpret_cast<uint4*>(scratch);
+        dst[0] = make_uint4(lb[0], lb[1], lb[2], lb[3]);
+        dst[1] = make_uint4(lb[4], lb[5], lb[6], lb[7]);
+        dst[2] = make_uint4(v.w[0], v.w[1], v.w[2], v.w[3]);
+        dst[3] = make_uint4(v.w[4], v.w[5], v.w[6], v.w[7]);
+      }
+      __syncwarp();
+      item(base, L);
+      __syncwarp();  // the scratch is rewritten for the next flagged lane
+    }
   }
   return hm;
 }
@@ -451,8 +468,12 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
       uint32_t* tmask = a.masks + seq * (kTileChunks * 32);
       uint32_t hitflags = 0, my_matches = 0, my_hits = 0;
       const int64_t ta = a.g.tile_a(t);
-      const bool full = ta >= (int64_t)a.g.ja_lo && ta + kTile <= (int64_t)a.g.ja_hi;
-      stream_tile<M, false>(a.g, R, S, t, lane,
+      // computed once per tile (pinned where the per-chunk inline settle reads it: ptxas
+      // would otherwise rematerialise the 64-bit compares in every chunk)
+      uint32_t full_u = ta >= (int64_t)a.g.ja_lo && ta + kTile <= (int64_t)a.g.ja_hi;
+      if constexpr (M < kCoopFrom) asm volatile("" : "+r"(full_u));
+      const bool full = full_u != 0u;
+      stream_tile<M, (M >= RK_UNROLL_FROM)>(a.g, R, S, t, lane,
                             [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J,
                                 int c) {
                        uint32_t hm = 0;
@@ -461,8 +482,8 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
                            const unsigned flags = __ballot_sync(kFull, short_any<M>(a, v, lb));
                            if (!flags) return;
                            if (__popc(flags) <= kCoopMaxLanes) {
-                             hm = coop_settle<M>(a, S.cur, v, lb, J, full, flags, lane,
-                                                 scratch, my_hits, my_matches);
+                             hm = coop_settle<M>(a, S.cur, v, lb, J, flags, lane, scratch,
+                                                 my_hits, my_matches);
                              if (__ballot_sync(kFull, hm != 0)) {
                                tmask[c * 32 + lane] = hm;
                                hitflags |= 1u << c;
