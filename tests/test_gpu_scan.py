@@ -145,6 +145,38 @@ def test_random_fuzz_against_oracle(gpu):
         assert st.hash_hits == len(eo) + ec
 
 
+def test_short_patterns_density_mix(gpu):
+    """m = 2..9 over texts whose hit density changes from tile to tile: sparse chunks go
+    through the lane-flag pass + cooperative settle, dense ones through the inline settle
+    (and the kernel's dense mode must switch back), at interior (staged) and edge tiles."""
+    torch = _torch()
+    rng = np.random.default_rng(5150)
+    segs = []
+    for i in range(24):
+        kind = i % 4
+        ln = int(rng.integers(3000, 40000))
+        if kind == 0:
+            segs.append(np.full(ln, ord("a"), dtype=np.uint8))
+        elif kind == 1:
+            segs.append(rng.integers(0, 2, ln, dtype=np.uint8) + ord("a"))
+        elif kind == 2:
+            segs.append(rng.integers(32, 127, ln, dtype=np.uint8))
+        else:
+            segs.append(rng.integers(0, 256, ln, dtype=np.uint8))
+    text = np.concatenate(segs)
+    dev = torch.from_numpy(text).cuda()
+    for m in range(2, 10):
+        for pat in (b"a" * m, bytes(text[50000 : 50000 + m]), bytes(rng.integers(32, 127, m, dtype=np.uint8))):
+            eo, ec = oracle.c_scan(text, np.frombuffer(pat, dtype=np.uint8), workers=8)
+            for off in (0, 5):
+                st = rk.ScanStats()
+                r = rk.search_sequential(dev[off:], pat, stats=st)
+                want = [x - off for x in eo.tolist() if x >= off]
+                assert r.offsets == want, (m, pat[:4], off)
+                if off == 0:
+                    assert st.collisions == ec and st.hash_hits == len(eo) + ec, (m, pat[:4])
+
+
 def test_c1_sweep_golden(gpu):
     co = G.corpus()
     text = rk.generate(rk.DnaSpec(42, 2**20, G.ASCII))
