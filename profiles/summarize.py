@@ -1,7 +1,7 @@
 """Summarise ncu reports into small text files kept under profiles/ (the .ncu-rep files
 stay in gpurun_out/, which is scratch).
 
-    python profiles/summarize.py gpurun_out/prof_m32f.ncu-rep profiles/r01_m32_tma.txt "note"
+    python profiles/summarize.py gpurun_out/prof_m32f.ncu-rep profiles/r01_m32_tma.txt "note" [launch]
 """
 
 import collections
@@ -37,9 +37,9 @@ def ncu(rep, page, extra=()):
     return list(csv.reader(io.StringIO(r.stdout)))
 
 
-def main(rep, out, note=""):
+def main(rep, out, note="", launch=0):
     raw = ncu(rep, "raw")
-    h, u, v = raw[0], raw[1], raw[2]
+    h, u, v = raw[0], raw[1], raw[2 + launch]
     lines = [f"# ncu summary of {rep.split('/')[-1]}", f"# {note}", ""]
     name_i = h.index("Kernel Name") if "Kernel Name" in h else None
     if name_i is not None:
@@ -48,12 +48,15 @@ def main(rep, out, note=""):
         if k in h:
             i = h.index(k)
             lines.append(f"{k} = {v[i]} {u[i]}")
-    src = ncu(rep, "source", ["--print-source", "sass"])
+    src = ncu(rep, "source", ["--print-source", "sass", "--launch-skip", str(launch),
+                              "--launch-count", "1"])
     if len(src) > 2:
         hdr = src[1]
         idx = {x: i for i, x in enumerate(hdr)}
         data = src[2:]
         cnt = collections.Counter()
+        data = [r for r in data
+                if len(r) >= len(hdr) and (r[idx["Instructions Executed"]] or "0").isdigit()]
         for r in data:
             toks = r[idx["Source"]].strip().split()
             if not toks:
@@ -74,4 +77,5 @@ def main(rep, out, note=""):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "")
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "",
+         int(sys.argv[4]) if len(sys.argv) > 4 else 0)
