@@ -198,7 +198,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="C1,C3,C4,C5")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--lib", default=None, help="time a variant library (A/B experiments)")
     args = ap.parse_args()
+    if args.lib:
+        from pathlib import Path
+
+        from paper_1810_01051_b200 import _lib
+
+        _lib.LIB_PATH = Path(args.lib).resolve()
     fns = {"C1": c1, "C3": c3, "C4": c4, "C5": c5,
            # not a BASELINE config: C3's shape over DNA (low-entropy q-grams)
            "C3dna": lambda r: c3(r, m=32, alphabet=b"ACGT", tag="C3dna"),
@@ -209,6 +216,8 @@ def main():
         t0 = time.time()
         r = fns[name](args.reps)
         r["wall_s"] = round(time.time() - t0, 1)
+        if args.lib:
+            r["lib"] = args.lib
         print(json.dumps(r), flush=True)
 
 

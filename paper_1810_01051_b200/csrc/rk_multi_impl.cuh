@@ -32,6 +32,9 @@
 
 namespace rkb {
 
+#ifndef RK_MULTI_UNROLL
+#define RK_MULTI_UNROLL false
+#endif
 constexpr int kMultiBlock = 32 * kMultiWarps;
 using MultiRing = WarpRingT<kMultiStageChunks>;
 
@@ -204,7 +207,7 @@ template <int SS, int QW>
 __device__ __forceinline__ void qgram_tile(const MultiArgs& a, MultiRing* R, Stream& S,
                                            uint32_t t, int lane, const uint32_t* sfilter) {
   constexpr int q = 4 * QW;
-  stream_tile<31, false>(
+  stream_tile<31, RK_MULTI_UNROLL>(
       a.g, R, S, t, lane,
       [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J, int) {
         const uint32_t qm = qgram_tests<SS, QW>(sfilter, v, lb);
