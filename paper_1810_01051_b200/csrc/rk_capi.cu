@@ -544,12 +544,31 @@ int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, 
       b.tiny = reserve((uint64_t)th.size * 8 + kTinyFilterBytes);
       memcpy(blob.data() + b.tiny, slots.data(), (uint64_t)th.size * 8);
       uint32_t* filt = reinterpret_cast<uint32_t*>(blob.data() + b.tiny + (uint64_t)th.size * 8);
-      for (uint32_t i = 0; i < b.P; ++i) {
-        const uint32_t f = tiny_key_hash((uint32_t)key[i], (uint32_t)(key[i] >> 32), th);
-        uint32_t* blk = filt + 2 * (f >> kTinyFilterShift);
-        const uint32_t q = f ^ (f >> 13);
-        blk[0] |= (1u << (q & 31)) | (1u << ((q >> 5) & 31));
-        blk[1] |= (1u << ((q >> 10) & 31)) | (1u << ((q >> 15) & 31));
+      if ((int)m >= kTinyAnchorFrom) {
+        // anchored q-grams: an occurrence at y holds the q-gram ending at the first anchor
+        // e >= y + q - 1 (anchors every 2 bytes), i.e. p[j:j+q] with j in {0, 1}
+        const int q = tiny_gram_q((int)m);
+        b.tiny_hash.p11 = 1u << 11;
+        b.tiny_hash.p16 = 1u << 16;
+        b.tiny_hash.p21 = 1u << 21;
+        for (uint32_t i = 0; i < b.P; ++i) {
+          for (int j = 0; j < 2; ++j) {
+            uint32_t gram = 0;
+            memcpy(&gram, h_patterns + first_byte[members[i]] + j, q);
+            const uint32_t h = gram * kGramMul;
+            uint32_t* blk = filt + 2 * (h >> 21);
+            blk[0] |= 1u << ((h >> 16) & 31);
+            blk[1] |= 1u << ((h >> 11) & 31);
+          }
+        }
+      } else {
+        for (uint32_t i = 0; i < b.P; ++i) {
+          const uint32_t f = tiny_key_hash((uint32_t)key[i], (uint32_t)(key[i] >> 32), th);
+          uint32_t* blk = filt + 2 * (f >> kTinyFilterShift);
+          const uint32_t q = f ^ (f >> 13);
+          blk[0] |= (1u << (q & 31)) | (1u << ((q >> 5) & 31));
+          blk[1] |= (1u << ((q >> 10) & 31)) | (1u << ((q >> 15) & 31));
+        }
       }
     }
     plan.groups.push_back(b);
@@ -983,6 +1002,14 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
       p.qfilter = reinterpret_cast<const uint32_t*>(dev + sw.qfilter);
       p.qmap = reinterpret_cast<const uint4*>(dev + sw.qmap);
       p.qmap_size = sw.qmap_size;
+    } else if ((int)m_min >= kTinyAnchorFrom) {
+      // anchored tiny kernel: tiles over the anchors (q-gram ends, every 2 bytes) of the
+      // window starts [amis, amis + nw); window validity is checked on the starts
+      const uint64_t q = (uint64_t)tiny_gram_q((int)m_min);
+      gg.ja_lo = gg.amis + q - 1;
+      gg.ja_hi = std::min<uint64_t>(gg.amis + nw - 1 + q - 1 + 2, gg.amis + n);
+      gg.tile_first = gg.ja_lo / kTile;
+      gg.num_tiles = (gg.ja_hi - 1) / kTile - gg.tile_first + 1;
     }
     p.G = (uint32_t)sw.groups.size();
     for (size_t k = 0; k < sw.groups.size(); ++k)

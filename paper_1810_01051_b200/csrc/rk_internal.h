@@ -97,7 +97,18 @@ struct TinyHash {
   uint32_t c1, c2, c3;  // seeds (the host retries others if an insertion cycles)
   uint32_t shift;       // 32 - log2(size)
   uint32_t size;        // slots, a power of two
+  // anchored q-gram filter (m >= kTinyAnchorFrom), a blocked Bloom filter of 2048 64-bit
+  // blocks: h = gram * kGramMul, block = h >> 21, bit h >> 16 (mod 32) of its low word
+  // and bit h >> 11 (mod 32) of its high word.  The shifts are taken by IMAD.HI with
+  // runtime powers of two (2^11, 2^16, 2^21) so they stay on the FMA pipe.
+  uint32_t p11, p16, p21;
 };
+// m >= this: the tiny kernel tests one anchored q-gram per 2 bytes (q = 3 for m = 4, else
+// 4; q + s - 1 <= m) instead of every window's key
+constexpr int kTinyAnchorFrom = 4;
+constexpr uint32_t kGramMul = 0x9E3779B1u;
+__host__ __device__ constexpr int tiny_gram_q(int m) { return m == 4 ? 3 : 4; }
+
 constexpr uint32_t kTinySlotsMax = 8192;             // 64 KiB of shared memory
 constexpr uint32_t kTinyFilterBytes = (1u << 17) / 8;  // 2^17-bit key filter, 16 KiB
 constexpr uint32_t kTinyFilterShift = 32 - 11;         // 64-bit block: top 11 bits of f

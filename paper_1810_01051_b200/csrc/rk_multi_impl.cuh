@@ -296,6 +296,79 @@ __device__ __forceinline__ void tiny_chunk(const MultiArgs& a, const Vec32& v,
   }
 }
 
+// 8 bytes of the text at a-space position p (the bytes of a candidate window): from the
+// TMA stage in shared memory when staged (cur = shared address of a-space position c0),
+// else from global memory with bounds checks (edge tiles, the end of a chunk).
+__device__ __forceinline__ uint2 tiny_window_bytes(const TextGeom& g, uint32_t cur, int64_t c0,
+                                                   int64_t p) {
+  // the stage holds the chunk's 32-byte lookback and its 1 KiB (a window may end up to 2
+  // bytes past the chunk: those bytes are the next chunk's, which the stage only holds
+  // when the chunk is not its last)
+  if (cur && p - c0 + 12 <= 32 + kChunk) {
+    const uint32_t addr = cur + (uint32_t)(p - c0);
+    const uint32_t al = addr & ~3u, r = 8u * (addr & 3u);
+    const uint32_t x0 = lds_u32(al), x1 = lds_u32(al + 4), x2 = lds_u32(al + 8);
+    return make_uint2(__funnelshift_r(x0, x1, r), __funnelshift_r(x1, x2, r));
+  }
+  const int64_t lo = (int64_t)g.amis, hi = (int64_t)(g.amis + g.n);
+  return make_uint2(edge_word(g.abase, lo, hi, p), edge_word(g.abase, lo, hi, p + 4));
+}
+
+// m in [kTinyAnchorFrom, 6]: one anchored q-gram per 2 bytes (anchors at odd lane offsets
+// k, the q-gram being the q bytes ending at J + k) is tested against a blocked Bloom
+// filter (2 bits in one 64-bit block, one LDS.64) of the patterns' anchored q-grams
+// (p[0:q], p[1:q+1]; ~0.1% false positives at 1024 patterns); a passing anchor makes its two
+// window starts (J + k - q + 1 - j, j = 0, 1) candidates, looked up exactly in the cuckoo
+// table.  Each window has exactly one anchor, so nothing is reported twice.
+template <int M>
+__device__ __forceinline__ void tiny_anchor_chunk(const MultiArgs& a, const Vec32& v,
+                                                  const uint32_t (&lb)[8], int64_t J,
+                                                  uint32_t cur, int lane, uint32_t slots,
+                                                  uint32_t bitmap, const TinyHash& th) {
+  constexpr int Q = tiny_gram_q(M);
+  constexpr uint32_t QK = Q >= 4 ? 0xffffffffu : ((1u << (8 * Q)) - 1u);
+  constexpr uint32_t K0 = M >= 4 ? 0xffffffffu : ((1u << (8 * M)) - 1u);
+  constexpr uint32_t K1 = M > 4 ? ((1u << (8 * (M - 4))) - 1u) : 0u;
+  uint32_t pass = 0;
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const int k = 2 * t + 1;  // the anchor is window end J + k
+    const uint32_t h = (w64(lb, v, 33 + k - Q) & QK) * kGramMul;
+    const unsigned long long x = ld_shared_u64(bitmap + 8u * __umulhi(h, th.p11));
+    const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+    pass |= (__funnelshift_r(xl, xl, __umulhi(h, th.p16)) &
+             __funnelshift_r(xh, xh, __umulhi(h, th.p21)) & 1u) << t;
+  }
+  if (!pass) return;
+  const int64_t c0 = J - kR * lane - 32;  // a-space position of the chunk's lookback start
+  do {
+    const int t = __ffs(pass) - 1;
+    pass &= pass - 1;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int64_t ya = J + 2 * t + 2 - Q - j;  // candidate window start, a-space
+      if (ya < (int64_t)a.ys_lo || ya >= (int64_t)a.grp[0].ys_hi) continue;
+      const uint2 w = tiny_window_bytes(a.g, cur, c0, ya);
+      const uint32_t lo = w.x & K0, hi = w.y & K1;
+      const uint32_t f = tiny_key_hash(lo, hi, th);
+      uint32_t s1, s2;
+      tiny_slots(f, th, s1, s2);
+      const unsigned long long key = ((unsigned long long)hi << 32) | lo;
+      const unsigned long long e1 = ld_shared_u64(slots + 8 * s1) ^ key;
+      const unsigned long long e2 = ld_shared_u64(slots + 8 * s2) ^ key;
+      const bool h1 = (e1 & 0xffffffffffffull) == 0 && (e1 >> 48) < 0xffffull;
+      const bool h2 = (e2 & 0xffffffffffffull) == 0 && (e2 >> 48) < 0xffffull;
+      if (h1 || h2) {
+        const unsigned long long pos = atomicAdd(&a.counters[0], 1ull);
+        if (pos < a.cap) {
+          a.out_off[pos] = ya - (int64_t)a.g.amis;
+          a.out_idx[pos] = (uint32_t)((h1 ? e1 : e2) >> 48);
+        }
+      }
+    }
+  } while (pass);
+}
+
 template <int M>
 __global__ void __launch_bounds__(kMultiBlock) rk_multi_tiny_kernel(const __grid_constant__ MultiArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -322,8 +395,12 @@ __global__ void __launch_bounds__(kMultiBlock) rk_multi_tiny_kernel(const __grid
     const bool full = ta >= (int64_t)a.g.ja_lo && ta + kTile <= (int64_t)a.g.ja_hi;
     stream_tile<M, false>(a.g, R, S, t, lane,
                           [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J, int) {
-                            tiny_chunk<M>(a, v, lb, J, full ? 0xffffffffu : valid_mask(a.g, J),
-                                          slots, bitmap, th);
+                            if constexpr (M >= kTinyAnchorFrom) {
+                              tiny_anchor_chunk<M>(a, v, lb, J, S.cur, lane, slots, bitmap, th);
+                            } else {
+                              tiny_chunk<M>(a, v, lb, J, full ? 0xffffffffu : valid_mask(a.g, J),
+                                            slots, bitmap, th);
+                            }
                           });
   }
 }
