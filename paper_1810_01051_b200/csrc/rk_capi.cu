@@ -548,9 +548,6 @@ int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, 
         // anchored q-grams: an occurrence at y holds the q-gram ending at the first anchor
         // e >= y + q - 1 (anchors every 2 bytes), i.e. p[j:j+q] with j in {0, 1}
         const int q = tiny_gram_q((int)m);
-        b.tiny_hash.p11 = 1u << 11;
-        b.tiny_hash.p16 = 1u << 16;
-        b.tiny_hash.p21 = 1u << 21;
         for (uint32_t i = 0; i < b.P; ++i) {
           for (int j = 0; j < 2; ++j) {
             uint32_t gram = 0;

@@ -97,12 +97,11 @@ struct TinyHash {
   uint32_t c1, c2, c3;  // seeds (the host retries others if an insertion cycles)
   uint32_t shift;       // 32 - log2(size)
   uint32_t size;        // slots, a power of two
-  // anchored q-gram filter (m >= kTinyAnchorFrom), a blocked Bloom filter of 2048 64-bit
-  // blocks: h = gram * kGramMul, block = h >> 21, bit h >> 16 (mod 32) of its low word
-  // and bit h >> 11 (mod 32) of its high word.  The shifts are taken by IMAD.HI with
-  // runtime powers of two (2^11, 2^16, 2^21) so they stay on the FMA pipe.
-  uint32_t p11, p16, p21;
 };
+// anchored q-gram filter (m >= kTinyAnchorFrom), a blocked Bloom filter of 2048 64-bit
+// blocks: h = gram * kGramMul, block = h >> 21, bit h >> 16 (mod 32) of its low word and
+// bit h >> 11 (mod 32) of its high word.  (Shifts by IMAD.HI on the FMA pipe measured
+// slower than SHF, here and in the q-gram kernel.)
 // m >= this: the tiny kernel tests one anchored q-gram per 2 bytes (q = 3 for m = 4, else
 // 4; q + s - 1 <= m) instead of every window's key
 constexpr int kTinyAnchorFrom = 4;

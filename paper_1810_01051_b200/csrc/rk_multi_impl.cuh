@@ -334,10 +334,9 @@ __device__ __forceinline__ void tiny_anchor_chunk(const MultiArgs& a, const Vec3
   for (int t = 0; t < 16; ++t) {
     const int k = 2 * t + 1;  // the anchor is window end J + k
     const uint32_t h = (w64(lb, v, 33 + k - Q) & QK) * kGramMul;
-    const unsigned long long x = ld_shared_u64(bitmap + 8u * __umulhi(h, th.p11));
+    const unsigned long long x = ld_shared_u64(bitmap + 8u * (h >> 21));
     const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
-    pass |= (__funnelshift_r(xl, xl, __umulhi(h, th.p16)) &
-             __funnelshift_r(xh, xh, __umulhi(h, th.p21)) & 1u) << t;
+    pass |= (__funnelshift_r(xl, xl, h >> 16) & __funnelshift_r(xh, xh, h >> 11) & 1u) << t;
   }
   if (!pass) return;
   const int64_t c0 = J - kR * lane - 32;  // a-space position of the chunk's lookback start
