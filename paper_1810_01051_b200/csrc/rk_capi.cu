@@ -305,7 +305,7 @@ int emit(rk_ctx* c, uint64_t tiles, uint64_t tile0, int64_t start_bias, int64_t*
     e.bitmap = d_bitmap;
     e.bit_bias = bit_bias;
   }
-  RK_CUDA(launch_emit(e, s));
+  RK_CUDA(launch_emit(e, c->num_sms, s));
   ++c->launches;
   return RK_OK;
 }

@@ -68,8 +68,9 @@ struct EmitArgs {
   uint64_t clear_words;
   uint32_t* bitmap;                // bitmap mode: bit (end position + bit_bias) per match
   int64_t bit_bias;
+  uint64_t groups_per_block;       // set by launch_emit
 };
-cudaError_t launch_emit(const EmitArgs& e, cudaStream_t s);
+cudaError_t launch_emit(EmitArgs e, int num_sms, cudaStream_t s);
 
 // multi pattern (rk_multi.cu, kernels in rk_multi_impl.cuh)
 constexpr int kMultiFilterWords = (1 << 16) / 32;
