@@ -57,6 +57,7 @@ def parse():
     # cuda:0, gloo instead of NCCL so no collective kernels wait on each other there)
     ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"))
     ap.add_argument("--same-device", action="store_true")
+    ap.add_argument("--lib", default=None, help=argparse.SUPPRESS)  # A/B of a variant build
     return ap.parse_args()
 
 
@@ -230,6 +231,8 @@ def run_ours(args):
     import paper_1810_01051_b200 as rk
     from paper_1810_01051_b200 import _lib, sharded
 
+    if args.lib:
+        _lib.LIB_PATH = Path(args.lib).resolve()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
