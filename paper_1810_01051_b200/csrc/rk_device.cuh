@@ -422,9 +422,17 @@ __device__ __forceinline__ void stream_init(const TextGeom& g, WarpRingT<SC>* R,
 // (window ends [J, J+32)), lb = the 32 bytes before J (M < 32 only), carryS = the fold
 // seed for M >= 32 (see fast_chunk), c = chunk index in the tile.  Interior tiles come
 // from the TMA ring; edge tiles go through the bounds-checked loader.
-template <int M, bool UNROLL = true, int SC, class Op>
+struct NoStageHook {
+  __device__ __forceinline__ void operator()(const uint8_t*, int, int) const {}
+};
+
+// stage_done(st, c_lo, c_n), called after the chunks [c_lo, c_lo + c_n) of a staged stage
+// have been through op and before the stage is handed back (st = the stage in shared
+// memory, its 32-byte lookback first), lets a caller revisit those bytes cheaply.
+template <int M, bool UNROLL = true, int SC, class Op, class Hook = NoStageHook>
 __device__ __forceinline__ void stream_tile(const TextGeom& g, WarpRingT<SC>* R, Stream& S,
-                                            uint32_t t, int lane, Op&& op) {
+                                            uint32_t t, int lane, Op&& op,
+                                            Hook&& stage_done = Hook{}) {
   const int64_t ta = g.tile_a(t);
   uint32_t carryS = 0;
   uint32_t lb[8];
@@ -450,6 +458,7 @@ __device__ __forceinline__ void stream_tile(const TextGeom& g, WarpRingT<SC>* R,
         S.cur = smem_u32(st) + j * kChunk;
         op(v, lb, carryS, ta + c * kChunk + lane * kR, c);
       }
+      stage_done(st, s * SC, SC);
       // the slot's bytes are consumed: hand it back to the producer
       S.cslot = (S.cslot + 1) & (kStages - 1);
       S.cphase ^= (S.cslot == 0);
