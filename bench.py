@@ -264,10 +264,25 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
     cap = 1 << 22
-    outs = {m: torch.empty(cap, dtype=torch.int64, device=f"cuda:{dev}") for m in sweep}
+    out_all = torch.empty((len(sweep), cap), dtype=torch.int64, device=f"cuda:{dev}")
+    outs = {m: out_all[i] for i, m in enumerate(sweep)}
     counts = torch.zeros((len(sweep), 3), dtype=torch.int64, device=f"cuda:{dev}")
+    # the exchange (N > 1): every rank's counters and ordered positions, per length, in
+    # two all_gathers per step over NVLink and no host round trip inside the step; the
+    # position slots hold GATHER_SLOT offsets per length (the C2 sweep finds <= 13 per
+    # GiB; a rank with more is caught by the gate after the timed region)
+    GATHER_SLOT = 8192
+    if world > 1:
+        all_counts = torch.empty((world, len(sweep), 3), dtype=torch.int64, device=f"cuda:{dev}")
+        all_pos = torch.empty((world, len(sweep), GATHER_SLOT), dtype=torch.int64, device=f"cuda:{dev}")
     pat_bufs = {m: np.frombuffer(pats[m], dtype=np.uint8) for m in sweep}
     n_local = int(text.numel())
+
+    def gather_into(out, inp):
+        if args.dist_backend == "nccl":
+            dist.all_gather_into_tensor(out, inp)
+        else:  # gloo (the one-GPU plumbing test): list form
+            dist.all_gather(list(out.unbind(0)), inp)
 
     def step(ev_pairs=None):
         for i, m in enumerate(sweep):
@@ -280,15 +295,8 @@ def run_ours(args):
             if ev_pairs is not None:
                 ev_pairs[i][1].record(stream)
         if world > 1:
-            # the exchange: counts, then positions padded to the max count, over NVLink
-            for i, m in enumerate(sweep):
-                k = counts[i, 0:1]
-                allk = [torch.empty_like(k) for _ in range(world)]
-                dist.all_gather(allk, k)
-                kmax = int(torch.stack(allk).max().item())
-                if kmax:
-                    parts = [torch.empty(kmax, dtype=torch.int64, device=k.device) for _ in range(world)]
-                    dist.all_gather(parts, outs[m][:kmax])
+            gather_into(all_counts, counts)
+            gather_into(all_pos, out_all[:, :GATHER_SLOT].contiguous())
         return counts
 
     for _ in range(max(args.warmup, 3)):
@@ -297,6 +305,13 @@ def run_ours(args):
     # correctness gate: every ordered list is what a second pass gives, and counts add up
     host_counts = counts.cpu().numpy()
     assert (host_counts[:, 1] == host_counts[:, 0] + host_counts[:, 2]).all()
+    if world > 1:
+        ac = all_counts.cpu().numpy()
+        assert (ac[:, :, 0] <= GATHER_SLOT).all(), "gather slot too small for this corpus"
+        ap = all_pos.cpu().numpy()
+        for i in range(len(sweep)):  # the global list, concatenated in rank order, ascends
+            glob = np.concatenate([ap[r, i, : ac[r, i, 0]] for r in range(world)])
+            assert (np.diff(glob) > 0).all()
 
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in sweep] for _ in range(args.steps)]
