@@ -18,9 +18,9 @@ struct ScanArgs {
   uint32_t* masks;                // per sequence number: kTileChunks x 32 lane hit masks
   PatWords pw;
 };
-// Shape of the scan kernel per pattern length: m >= 32 (one running fold, the least work
+// Shape of the scan kernel per pattern length: m >= 15 (the running fold, the least work
 // per byte) streams 8 KiB stages -- one TMA copy and one ring hand-off per tile -- with 12
-// warps per SM; the shorter paths keep 4 KiB stages and 3 x 8 warps per SM, the latency
+// warps per SM; the shorter paths keep 4 KiB stages and more warps per SM, the latency
 // cover their longer per-byte work needs.
 #ifndef RK_PDL
 #define RK_PDL 1  // programmatic dependent launch of the scan and emit grids
@@ -28,22 +28,18 @@ struct ScanArgs {
 #ifndef RK_WIDE_FROM
 #define RK_WIDE_FROM 15
 #endif
-#ifndef RK_SHORT_FROM
-#define RK_SHORT_FROM 5
-#endif
-#ifndef RK_SHORT_W
-#define RK_SHORT_W 16
-#define RK_SHORT_S 4
-#define RK_SHORT_B 1
-#endif
 struct ScanShape {
   int warps, stage_chunks, min_blocks;
 };
 constexpr uint32_t kWideFrom = RK_WIDE_FROM;  // first m with the wide shape
+// measured per length (tools/ab.sh): m = 8 likes 20 warps in one CTA, m = 5..7 two CTAs
+// of 8 warps (the two dependent dp4a per window want warps; the cooperative settle's
+// chunk-end ballots want smaller CTAs)
 __host__ __device__ constexpr ScanShape scan_shape(uint32_t m) {
   return m >= kWideFrom ? ScanShape{12, 8, 1}
-                        : (m >= RK_SHORT_FROM && m <= 8 ? ScanShape{RK_SHORT_W, RK_SHORT_S, RK_SHORT_B}
-                                                        : ScanShape{8, 4, 3});
+         : m == 8       ? ScanShape{20, 4, 1}
+         : (m >= 5 && m <= 7) ? ScanShape{8, 4, 2}
+                              : ScanShape{8, 4, 3};
 }
 __host__ __device__ constexpr int scan_warps(uint32_t m) { return scan_shape(m).warps; }
 __host__ __device__ constexpr int scan_stage_chunks(uint32_t m) { return scan_shape(m).stage_chunks; }
