@@ -28,6 +28,11 @@ struct ScanArgs {
 #ifndef RK_WIDE_FROM
 #define RK_WIDE_FROM 15
 #endif
+#ifndef RK_BASE_W
+#define RK_BASE_W 12
+#define RK_BASE_S 4
+#define RK_BASE_B 2
+#endif
 struct ScanShape {
   int warps, stage_chunks, min_blocks;
 };
@@ -39,7 +44,7 @@ __host__ __device__ constexpr ScanShape scan_shape(uint32_t m) {
   return m >= kWideFrom ? ScanShape{12, 8, 1}
          : m == 8       ? ScanShape{20, 4, 1}
          : (m >= 5 && m <= 7) ? ScanShape{8, 4, 2}
-                              : ScanShape{8, 4, 3};
+                              : ScanShape{RK_BASE_W, RK_BASE_S, RK_BASE_B};
 }
 __host__ __device__ constexpr int scan_warps(uint32_t m) { return scan_shape(m).warps; }
 __host__ __device__ constexpr int scan_stage_chunks(uint32_t m) { return scan_shape(m).stage_chunks; }
