@@ -28,6 +28,11 @@ struct ScanArgs {
 #ifndef RK_WIDE_FROM
 #define RK_WIDE_FROM 15
 #endif
+#ifndef RK_WIDE_W
+#define RK_WIDE_W 12
+#define RK_WIDE_S 8
+#define RK_WIDE_B 1
+#endif
 #ifndef RK_BASE_W
 #define RK_BASE_W 12
 #define RK_BASE_S 4
@@ -41,7 +46,7 @@ constexpr uint32_t kWideFrom = RK_WIDE_FROM;  // first m with the wide shape
 // of 8 warps (the two dependent dp4a per window want warps; the cooperative settle's
 // chunk-end ballots want smaller CTAs)
 __host__ __device__ constexpr ScanShape scan_shape(uint32_t m) {
-  return m >= kWideFrom ? ScanShape{12, 8, 1}
+  return m >= kWideFrom ? ScanShape{RK_WIDE_W, RK_WIDE_S, RK_WIDE_B}
          : m == 8       ? ScanShape{20, 4, 1}
          : (m >= 5 && m <= 7) ? ScanShape{8, 4, 2}
                               : ScanShape{RK_BASE_W, RK_BASE_S, RK_BASE_B};
