@@ -236,6 +236,33 @@ def test_golden_multi_cases(gpu):
             assert r.pattern_length == len(c["deduped"][i])
 
 
+def test_multi_short_lengths_at_chunk_and_tile_edges(gpu):
+    """m = 4..6 multi-pattern sets (anchored q-grams every 2 bytes + cuckoo lookups):
+    occurrences planted so that windows end at every offset around 1 KiB chunk ends
+    (their last bytes are the next chunk's), 4 KiB stage ends and 8 KiB tile ends, at the
+    text's first and last bytes, and at unaligned device views."""
+    torch = _torch()
+    rng = np.random.default_rng(99)
+    n = (1 << 20) + 37
+    text = rng.integers(32, 127, n, dtype=np.uint8)
+    for m in (4, 5, 6):
+        pats = [rng.integers(32, 127, m, dtype=np.uint8).tobytes() for _ in range(40)]
+        pats += [text[x : x + m].tobytes() for x in (0, n - m, 12345)]
+        t = text.copy()
+        # one intact occurrence per 1 KiB chunk end, ending d in [-3, 2] bytes from it
+        # (cycling), so every stage end (4 KiB) and tile end (8 KiB) gets each d
+        for k, base in enumerate(range(1024, n - 64, 1024)):
+            d = (k // 8) % 6 - 3
+            y = base + d - m + 1
+            t[y : y + m] = np.frombuffer(pats[k % len(pats)], dtype=np.uint8)
+        want = oracle.search_multi(t.tobytes(), pats)
+        dev = torch.from_numpy(t).cuda()
+        for off in (0, 3):
+            got = rk.search_multi(dev[off:], pats)
+            exp = [(i, [x - off for x in offs if x >= off]) for i, offs in want]
+            assert [(i, r.offsets) for i, r in got] == exp, (m, off)
+
+
 def test_multi_singleton_equals_sequential(gpu):
     rng = np.random.default_rng(5)
     for _ in range(40):
