@@ -155,7 +155,7 @@ constexpr bool kFoldFmaBytes = RK_FOLD_FMA_BYTES;
 // d's and words still in registers: hash hits are counted, and only when some window's
 // bytes equal the pattern (or the tile is at the edge of the range) are the hit and
 // byte masks built.
-template <int M>
+template <int M, bool Dense = false>
 __device__ __forceinline__ void short_chunk(const ScanArgs& a, const Vec32& v,
                                             const uint32_t (&lb)[8], bool full, uint32_t vmask,
                                             uint32_t& hm, uint32_t& hits) {
@@ -206,6 +206,22 @@ __device__ __forceinline__ void short_chunk(const ScanArgs& a, const Vec32& v,
       for (int kk = 0; kk < 8; ++kk) anyg |= (d[kk] == 0u);
     }
     if (anyg) {
+      // Dense (the warp's previous tile was mostly matches, e.g. all 'a'): when the whole
+      // group hits and matches -- the OR of its 8 d's and byte differences is 0 -- take
+      // it at once
+      if (Dense && full) {
+        uint32_t dor = 0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          dor |= d[kk] | ((wA[kk] ^ a.pw.w[0]) & K0);
+          if constexpr (M > 4) dor |= (wB[kk] ^ a.pw.w[1]) & K1;
+        }
+        if (dor == 0u) {
+          hits += 8;
+          hm |= 0xffu << (grp * 8);
+          continue;
+        }
+      }
       bool anyeq = false;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
@@ -498,6 +514,8 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
       uint32_t full_u = ta >= (int64_t)a.g.ja_lo && ta + kTile <= (int64_t)a.g.ja_hi;
       if constexpr (M < kCoopFrom) asm volatile("" : "+r"(full_u));
       const bool full = full_u != 0u;
+      const auto tile_body = [&](auto dense_tag) {
+        constexpr bool kDense = decltype(dense_tag)::value;
       stream_tile<M, (M >= RK_UNROLL_FROM)>(a.g, R, S, t, lane,
                             [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J,
                                 int c) {
@@ -518,7 +536,7 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
                          }
                        }
                        uint32_t hits = 0;
-                       short_chunk<M>(a, v, lb, full, full ? 0xffffffffu : valid_mask(a.g, J),
+                       short_chunk<M, kDense>(a, v, lb, full, full ? 0xffffffffu : valid_mask(a.g, J),
                                       hm, hits);
                        // dense hits (e.g. all 'a'): stay on the inline settle, skipping the
                        // flag pass, while most lanes keep hitting
@@ -531,7 +549,18 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
                          hitflags |= 1u << c;
                        }
                      });
+      };
+      if constexpr (M < kCoopFrom) {
+        if (dense) tile_body(std::true_type{});
+        else tile_body(std::false_type{});
+      } else {
+        tile_body(std::false_type{});
+      }
       record_tile(a, seq, my_matches, my_hits, hitflags, lane, tot);
+      if constexpr (M < kCoopFrom) {
+        // the next tile takes the dense settle when this one was mostly matches
+        dense = __reduce_add_sync(kFull, my_matches) > (uint32_t)(kTile / 2);
+      }
     }
   }
   flush_totals(a, tot, lane);
