@@ -364,6 +364,7 @@ struct Stream {
   uint32_t pslot;       // ring slot the producer fills next
   uint32_t W, int_lo, int_hi, ntiles;
   int64_t tile_jump;    // bytes from the end of one of the warp's tiles to its next one
+  uint32_t ring_s;      // shared-space address of the ring's first stage
   uint32_t cur;         // during op(): shared-space address of the current chunk's bytes
                         // from its 32-byte lookback on, or 0 (edge tiles: read from global)
 };
@@ -414,6 +415,7 @@ __device__ __forceinline__ void stream_init(const TextGeom& g, WarpRingT<SC>* R,
   S.cslot = S.pslot = 0;
   S.cphase = 0;
   S.tile_jump = (int64_t)(W - 1) * kTile;
+  S.ring_s = smem_u32(R->buf[0]);
   stream_seek(g, S);
   for (int i = 0; i < kStages; ++i) stream_issue(R, S, lane);
 }
@@ -455,7 +457,7 @@ __device__ __forceinline__ void stream_tile(const TextGeom& g, WarpRingT<SC>* R,
           for (int i = 0; i < 8; ++i) lb[i] = l.w[i];
         }
         const int c = s * SC + j;
-        S.cur = smem_u32(st) + j * kChunk;
+        S.cur = S.ring_s + S.cslot * (uint32_t)WarpRingT<SC>::kBytes + j * kChunk;
         op(v, lb, carryS, ta + c * kChunk + lane * kR, c);
       }
       stage_done(st, s * SC, SC);

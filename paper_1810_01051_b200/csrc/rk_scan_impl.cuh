@@ -259,7 +259,8 @@ __device__ __forceinline__ void short_chunk(const ScanArgs& a, const Vec32& v,
 // whole warp: the flagged lane publishes its 64 bytes in a per-warp scratch, each lane
 // takes one of its 32 windows (exact hash, validity, bytes) and two ballots give the hit
 // count and the match mask.  A chunk with many flagged lanes (dense matches, e.g. all 'a')
-// goes to the per-lane inline settle instead (short_chunk).
+// goes to the per-lane inline settle instead (short_chunk), where the warp stays while
+// the density lasts.
 #ifndef RK_COOP_FROM
 #define RK_COOP_FROM 5
 #endif
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
   Stream S;
   stream_init(a.g, R, S, (uint32_t)w, (uint32_t)W, lane);
   WarpTotals tot;
-  bool dense = false;  // warp-uniform: the last settled chunk of M <= 8 had dense hits
+  bool dense = false;  // warp-uniform: M <= 8 and the warp's last tile was mostly matches
   (void)dense;
   for (uint32_t t = (uint32_t)w; t < (uint32_t)a.g.num_tiles; t += (uint32_t)W) {
     if constexpr (M >= 32) {
@@ -514,45 +515,50 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
       uint32_t full_u = ta >= (int64_t)a.g.ja_lo && ta + kTile <= (int64_t)a.g.ja_hi;
       if constexpr (M < kCoopFrom) asm volatile("" : "+r"(full_u));
       const bool full = full_u != 0u;
+      // kDense (M < kCoopFrom): the warp's previous tile was mostly matches (e.g. all
+      // 'a'), so this one settles whole all-hit groups at once
       const auto tile_body = [&](auto dense_tag) {
         constexpr bool kDense = decltype(dense_tag)::value;
-      stream_tile<M, (M >= RK_UNROLL_FROM)>(a.g, R, S, t, lane,
-                            [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J,
-                                int c) {
-                       uint32_t hm = 0;
-                       if constexpr (M >= kCoopFrom) {
-                         if (!dense) {
-                           const unsigned flags = __ballot_sync(kFull, short_any<M>(a, v, lb));
-                           if (!flags) return;
-                           if (__popc(flags) <= kCoopMaxLanes) {
-                             hm = coop_settle<M>(a, S.cur, v, lb, J, flags, lane, scratch,
-                                                 my_hits, my_matches);
-                             if (__ballot_sync(kFull, hm != 0)) {
-                               tmask[c * 32 + lane] = hm;
-                               hitflags |= 1u << c;
-                             }
-                             return;
-                           }
-                         }
-                       }
-                       uint32_t hits = 0;
-                       short_chunk<M, kDense>(a, v, lb, full, full ? 0xffffffffu : valid_mask(a.g, J),
-                                      hm, hits);
-                       // dense hits (e.g. all 'a'): stay on the inline settle, skipping the
-                       // flag pass, while most lanes keep hitting
-                       if constexpr (M >= kCoopFrom)
-                         dense = __popc(__ballot_sync(kFull, hits != 0)) > kCoopMaxLanes;
-                       my_hits += hits;
-                       my_matches += __popc(hm);
-                       if (__ballot_sync(kFull, hm != 0)) {
-                         tmask[c * 32 + lane] = hm;
-                         hitflags |= 1u << c;
-                       }
-                     });
+        stream_tile<M, (M >= RK_UNROLL_FROM)>(
+            a.g, R, S, t, lane,
+            [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J, int c) {
+              uint32_t hm = 0;
+              if constexpr (M >= kCoopFrom) {
+                if (!dense) {
+                  const unsigned flags = __ballot_sync(kFull, short_any<M>(a, v, lb));
+                  if (!flags) return;
+                  if (__popc(flags) <= kCoopMaxLanes) {
+                    hm = coop_settle<M>(a, S.cur, v, lb, J, flags, lane, scratch, my_hits,
+                                        my_matches);
+                    if (__ballot_sync(kFull, hm != 0)) {
+                      tmask[c * 32 + lane] = hm;
+                      hitflags |= 1u << c;
+                    }
+                    return;
+                  }
+                }
+              }
+              uint32_t hits = 0;
+              short_chunk<M, kDense>(a, v, lb, full, full ? 0xffffffffu : valid_mask(a.g, J),
+                                     hm, hits);
+              // M >= kCoopFrom: stay on the inline settle, skipping the flag pass, while
+              // most lanes keep hitting
+              if constexpr (M >= kCoopFrom)
+                dense = __popc(__ballot_sync(kFull, hits != 0)) > kCoopMaxLanes;
+              my_hits += hits;
+              my_matches += __popc(hm);
+              if (__ballot_sync(kFull, hm != 0)) {
+                tmask[c * 32 + lane] = hm;
+                hitflags |= 1u << c;
+              }
+            });
       };
       if constexpr (M < kCoopFrom) {
-        if (dense) tile_body(std::true_type{});
-        else tile_body(std::false_type{});
+        if (dense) {
+          tile_body(std::true_type{});
+        } else {
+          tile_body(std::false_type{});
+        }
       } else {
         tile_body(std::false_type{});
       }
