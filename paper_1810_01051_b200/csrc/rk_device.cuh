@@ -421,9 +421,10 @@ __device__ __forceinline__ void stream_init(const TextGeom& g, WarpRingT<SC>* R,
 }
 
 // Streams tile t chunk by chunk into op(v, lb, carryS, J, c): v = the lane's 32 bytes
-// (window ends [J, J+32)), lb = the 32 bytes before J (M < 32 only), carryS = the fold
-// seed for M >= 32 (see fast_chunk), c = chunk index in the tile.  Interior tiles come
-// from the TMA ring; edge tiles go through the bounds-checked loader.
+// (window ends [J, J+32)), lb = the 32 bytes before J (0 < M < 32 only; M = 0: neither
+// lb nor the fold), carryS = the fold seed for M >= 32 (see fast_chunk), c = chunk index
+// in the tile.  Interior tiles come from the TMA ring; edge tiles go through the
+// bounds-checked loader.
 struct NoStageHook {
   __device__ __forceinline__ void operator()(const uint8_t*, int, int) const {}
 };
@@ -451,7 +452,7 @@ __device__ __forceinline__ void stream_tile(const TextGeom& g, WarpRingT<SC>* R,
 #pragma unroll(UNROLL ? SC : 1)
       for (int j = 0; j < SC; ++j) {
         const Vec32 v = lds32(st + 32 + j * kChunk + lane * kR);
-        if constexpr (M < 32) {
+        if constexpr (M > 0 && M < 32) {
           const Vec32 l = lds32(st + j * kChunk + lane * kR);
 #pragma unroll
           for (int i = 0; i < 8; ++i) lb[i] = l.w[i];
@@ -475,7 +476,7 @@ __device__ __forceinline__ void stream_tile(const TextGeom& g, WarpRingT<SC>* R,
     for (int c = 0; c < kTileChunks; ++c) {
       const int64_t J = ta + c * kChunk + lane * kR;
       const Vec32 v = load_edge(g, J);
-      if constexpr (M < 32) {
+      if constexpr (M > 0 && M < 32) {
         const Vec32 l = load_edge(g, J - 32);
 #pragma unroll
         for (int i = 0; i < 8; ++i) lb[i] = l.w[i];

@@ -207,7 +207,10 @@ template <int SS, int QW>
 __device__ __forceinline__ void qgram_tile(const MultiArgs& a, MultiRing* R, Stream& S,
                                            uint32_t t, int lane, const uint32_t* sfilter) {
   constexpr int q = 4 * QW;
-  stream_tile<31, RK_MULTI_UNROLL>(
+  // the anchored q-grams only reach into the 32 bytes before the lane's when a q-gram is
+  // longer than the sampling step (QW words > SS / 4): otherwise skip loading them
+  constexpr int kStreamM = QW > SS / 4 ? 31 : 0;
+  stream_tile<kStreamM, RK_MULTI_UNROLL>(
       a.g, R, S, t, lane,
       [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J, int) {
         const uint32_t qm = qgram_tests<SS, QW>(sfilter, v, lb);
