@@ -142,8 +142,14 @@ struct MultiGroup {
   uint32_t m, tsize, P;
 };
 constexpr int kMultiMaxGroups = 64;  // length groups per sweep (kernel parameter space)
-constexpr int kMultiWarps = 16;      // one 16-warp CTA per SM shares the 64 KiB q-gram filter
-constexpr int kMultiStageChunks = 4;  // 4 KiB TMA stages  // length groups per sweep (kernel parameter space)
+#ifndef RK_MULTI_WARPS
+#define RK_MULTI_WARPS 16
+#define RK_MULTI_STAGE 4
+#endif
+// one 16-warp CTA per SM shares the 64 KiB q-gram filter, 4 KiB TMA stages (measured
+// against 20/24/32 warps with 2 KiB stages: C3 5.23 against 3.64/5.20/4.52 TB/s)
+constexpr int kMultiWarps = RK_MULTI_WARPS;
+constexpr int kMultiStageChunks = RK_MULTI_STAGE;
 
 struct MultiArgs {
   TextGeom g;                 // q-gram mode: tiles cover the anchors (q-gram ends)
