@@ -46,7 +46,7 @@ def _slices_agree(text_host_fn, offs_host, pat, n, seed, samples=4, window=1 << 
         assert offs_host[lo:hi].tolist() == expect, (a, b)
 
 
-@pytest.mark.parametrize("m", [4, 8, 16, 25, 32, 64, 128, 256, 512, 1024])
+@pytest.mark.parametrize("m", [4, 5, 8, 12, 16, 20, 25, 32, 64, 128, 256, 512, 1024])
 def test_c2_1gib_ascii(gpu, m):
     import torch
 
