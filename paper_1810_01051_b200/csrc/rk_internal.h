@@ -1,4 +1,16 @@
 // rk_internal.h -- host-side declarations shared by the CUDA translation units.
+//
+// Build-time knobs (RK_*; defaults are the measured best on B200, and tools/ab.sh /
+// RK_DEFINES in paper_1810_01051_b200/_build.py build variants to A/B them):
+//   RK_PDL               programmatic dependent launch of scan and emit (1)
+//   RK_WIDE_FROM         first m with the wide 12-warp x 8 KiB-stage shape (15)
+//   RK_WIDE_W/S/B, RK_BASE_W/S/B   warps / stage chunks / CTAs per SM of the shapes
+//   RK_FOLD_FMA_BYTES    fold filter takes b0/b1 by dp4a instead of PRMT (0)
+//   RK_COOP_FROM         first m with the lane-flag + cooperative settle (5)
+//   RK_UNROLL_FROM       first m whose chunk loop is unrolled per stage (5)
+//   RK_EMIT_MIN_SMEM_KB  emit CTA shared-memory floor, one CTA per SM (116)
+//   RK_EMIT_MAX_GROUPS   groups of 256 tiles one emit block expands (4)
+//   RK_MULTI_WARPS/STAGE, RK_MULTI_UNROLL   q-gram / tiny multi-pattern kernel shape
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
