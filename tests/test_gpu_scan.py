@@ -102,8 +102,9 @@ def test_foreign_hx_semantics(gpu):
     """hx is a parameter (as in _scan_range): windows are hash-checked against it, then
     byte-verified against the pattern bytes."""
     rng = np.random.default_rng(5)
-    host = rng.integers(97, 100, 5000, dtype=np.uint8)
-    for m, hx_kind in [(1, "other"), (1, "big"), (2, "other"), (4, "other"), (8, "other"),
+    host = rng.integers(97, 100, 60000, dtype=np.uint8)  # edge and staged (interior) tiles
+    for m, hx_kind in [(1, "other"), (1, "big"), (2, "other"), (4, "other"), (5, "other"),
+                       (6, "other"), (8, "other"), (12, "other"), (16, "other"), (20, "other"),
                        (30, "other"), (40, "other"), (70, "other")]:
         pat = host[100 : 100 + m]
         other = host[200 : 200 + m] if m > 1 else np.array([98], dtype=np.uint8)
