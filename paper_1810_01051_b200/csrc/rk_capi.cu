@@ -774,8 +774,23 @@ int rk_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_pat
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
-  if (int r = enqueue_scan(c, d_text, n, h_pattern, m, hx, start, stop, d_out, cap, 0, s)) return r;
-  return read_counters(c, matches, collisions, hash_hits, s);
+  if (stop <= start || hash_unreachable(m, hx)) {
+    if (int r = enqueue_scan(c, d_text, n, h_pattern, m, hx, start, stop, d_out, cap, 0, s))
+      return r;
+    return read_counters(c, matches, collisions, hash_hits, s);
+  }
+  // The emit kernel writes {matches, hash_hits, collisions} straight into the pinned
+  // counter block (host memory mapped through UVA): no device-to-host copy sits between
+  // the last kernel and the wait (C1, 1 MiB: the synchronous call is launch-bound).
+  unsigned long long* hc = c->h_counters;
+  if (int r = enqueue_scan(c, d_text, n, h_pattern, m, hx, start, stop, d_out, cap, 0, s,
+                           (uint64_t*)hc))
+    return r;
+  RK_CUDA(cudaStreamSynchronize(s));
+  if (matches) *matches = hc[0];
+  if (hash_hits) *hash_hits = hc[1];
+  if (collisions) *collisions = hc[2];
+  return RK_OK;
 }
 
 int rk_scan_host(rk_ctx_t* c, const uint8_t* h_text, uint64_t n, const uint8_t* h_pattern,
