@@ -59,7 +59,7 @@ def c1(reps):
     offs, k, coll, hits = _scan.scan_counts(t, pat, hx, 0, t.numel() - 7)
     return {"config": "C1", "bytes": t.numel(), "m": 8, "ms": ms,
             "GBps": t.numel() / ms / 1e6, "matches": k, "collisions": coll,
-            "note": "includes the host round trip of the synchronous rk_scan (counts D2H)"}
+            "note": "includes the host round trip of the synchronous rk_scan (counters written to mapped pinned memory) and the Python wrapper"}
 
 
 def c3(reps, n=4 << 30, P=1024, m=16, alphabet=None, tag="C3"):
