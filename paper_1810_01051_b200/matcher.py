@@ -155,7 +155,7 @@ def multi_scan(t_dev, dev: int, pats: list[bytes]):
     lengths = np.array([len(p) for p in pats], dtype=np.uint32)
     hashes = np.array([hash_full(p) for p in pats], dtype=np.uint64)
     ctx = _lib.context(dev)
-    stream = torch.cuda.current_stream(dev).cuda_stream
+    stream = _scan._stream(dev)
     cap = 1 << 16
     pairs = _lib.u64ref()
     for _attempt in range(2):
