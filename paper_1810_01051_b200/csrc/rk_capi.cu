@@ -354,7 +354,14 @@ int launch_one(rk_ctx* c, const uint8_t* d_text, uint64_t n, uint32_t m, uint64_
   a.tile_info = c->d_tile_info;
   a.masks = c->d_masks;
   a.pw = pw;
-  RK_CUDA(launch_scan(a, grid_for(g.num_tiles, c->num_sms, scan_blocks_per_sm(m), scan_warps(m)),
+  // A scan with fewer tiles than the full grid has warps (e.g. C1, 1 MiB = 128 tiles
+  // against 148 x 20 warps at m = 8) spreads them: every CTA slot gets ceil(tiles / slots)
+  // warps, so a 1 MiB scan streams through ~128 SMs instead of 7 full CTAs.
+  const uint64_t slots = (uint64_t)c->num_sms * (uint64_t)scan_blocks_per_sm(m);
+  uint64_t warps = (uint64_t)scan_warps(m);
+  if (g.num_tiles < slots * warps) warps = std::max<uint64_t>(1, (g.num_tiles + slots - 1) / slots);
+  a.warps = (uint32_t)warps;
+  RK_CUDA(launch_scan(a, grid_for(g.num_tiles, c->num_sms, scan_blocks_per_sm(m), (int)warps),
                       s));
   ++c->launches;
   return RK_OK;

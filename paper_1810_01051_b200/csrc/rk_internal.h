@@ -29,6 +29,8 @@ struct ScanArgs {
   uint32_t* tile_info;            // per sequence number: matches | chunk bitmap << 16
   uint32_t* masks;                // per sequence number: kTileChunks x 32 lane hit masks
   PatWords pw;
+  uint32_t warps;                 // warps per CTA launched (<= scan_warps(m): small scans
+                                  // spread one or a few warps over every SM)
 };
 // Shape of the scan kernel per pattern length: m >= 15 (the running fold, the least work
 // per byte) streams 8 KiB stages -- one TMA copy and one ring hand-off per tile -- with 12

@@ -457,8 +457,8 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
       reinterpret_cast<uint32_t*>(smem + kWarps * sizeof(Ring)) + warp * kScratchWords;
   (void)scratch;
   ring_init(R, lane);
-  const uint64_t W = (uint64_t)gridDim.x * kWarps;
-  const uint64_t w = (uint64_t)blockIdx.x * kWarps + warp;
+  const uint64_t W = (uint64_t)gridDim.x * a.warps;
+  const uint64_t w = (uint64_t)blockIdx.x * a.warps + warp;
   const uint32_t T = (uint32_t)a.hx;
   const auto pred = [T](uint32_t L) { return L == T; };
   Stream S;
@@ -588,7 +588,7 @@ cudaError_t launch_m(const ScanArgs& a, int grid, cudaStream_t s) {
   // kernel waits for that grid's completion before touching memory (griddepcontrol.wait)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(32 * scan_warps(M));
+  cfg.blockDim = dim3(32 * a.warps);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
