@@ -14,8 +14,12 @@
  *   - Every function returns 0 on success, RK_EINVAL for argument errors (the Python
  *     layer maps it to ValueError), RK_ECUDA for CUDA failures (RuntimeError).
  *     rk_last_error() returns the calling thread's last message.
- *   - A context owns per-device scratch (look-back status, tickets, staging buffers).
- *     Calls on one context must not run concurrently; use one context per stream.
+ *   - A context owns per-device scratch (per-tile match counts and hit masks, counter
+ *     sets, the pattern cache, staging buffers).  Calls on one context are serialised by
+ *     its mutex, and the scratch is stream-ordered: a call on a different stream than the
+ *     previous one first makes its stream wait for the work already queued on that one
+ *     (so the previous call's stream must still exist at the next call).  For concurrent
+ *     scans use one context per stream.
  *   - Hash: h = sum b_i * 2^(m-1-i) mod 2^64 (rkhash.py:21-28).  Window x covers text
  *     bytes [x, x+m).  Offsets are 0-based int64, strictly ascending.
  */
@@ -54,9 +58,9 @@ int rk_ctx_destroy(rk_ctx_t* ctx);
  *   *matches    windows whose hash equals hx AND whose bytes equal the pattern
  *   *collisions windows whose hash equals hx but whose bytes differ
  *   *hash_hits  matches + collisions (ScanStats.hash_hits, matcher.py:45-55)
- * Requires stop + m - 1 <= n.  A caller seeing matches > cap may call again with a
- * larger buffer (the reference's overflow protocol, _scan.py:64-67).  Blocks the host
- * until the result is known.
+ * Requires stop + m - 1 <= n.  A caller seeing matches > cap fetches all of them with
+ * rk_scan_fetch into a larger buffer (the reference rescans instead, _scan.py:64-67).
+ * Blocks the host until the result is known.
  */
 int rk_scan(rk_ctx_t* ctx, const uint8_t* d_text, uint64_t n, const uint8_t* h_pattern,
             uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t* d_out,
@@ -75,6 +79,15 @@ int rk_scan_async(rk_ctx_t* ctx, const uint8_t* d_text, uint64_t n, const uint8_
                   uint64_t cap, int64_t out_bias, uint64_t* d_counts, void* stream);
 int rk_scan_result(rk_ctx_t* ctx, uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits,
                    void* stream);
+
+/*
+ * rk_scan_fetch -- the overflow protocol of scan (_scan.py:61-67) without the rescan:
+ * re-writes the ordered offsets of this context's last rk_scan / rk_scan_async (which
+ * must have been its last call) into d_out, now with room for cap of them, from the
+ * per-tile results the scan left on the device.  Asynchronous on `stream`; only the
+ * ordered-emission kernel runs.  RK_EINVAL if the last call was not a device scan.
+ */
+int rk_scan_fetch(rk_ctx_t* ctx, int64_t* d_out, uint64_t cap, void* stream);
 
 /*
  * rk_scan_bitmap -- MatchResult.to_bitmap (matcher.py:36-42) produced on the device:

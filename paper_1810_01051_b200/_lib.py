@@ -22,7 +22,7 @@ MULTI_MAX_PATTERNS = 4096
 EXPORTS = (
     "rk_version", "rk_last_error", "rk_device_count", "rk_ctx_create", "rk_ctx_destroy",
     "rk_scan", "rk_scan_async", "rk_scan_result", "rk_scan_bitmap", "rk_scan_host",
-    "rk_scan_host_fetch",
+    "rk_scan_host_fetch", "rk_scan_fetch",
     "rk_multi_scan", "rk_multi_scan_mixed", "rk_window_hashes", "rk_generate", "rk_launch_count",
 )
 
@@ -60,6 +60,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.rk_scan_host.argtypes = [vp, u8p, u64, u8p, u32, u64, u64, u64, vp, u64, pu64, pu64, pu64]
     lib.rk_scan_host_fetch.restype = ci
     lib.rk_scan_host_fetch.argtypes = [vp, vp, u64, u64]
+    lib.rk_scan_fetch.restype = ci
+    lib.rk_scan_fetch.argtypes = [vp, vp, u64, vp]
     lib.rk_multi_scan.restype = ci
     lib.rk_multi_scan.argtypes = [vp, u8p, u64, u8p, u32, u32, vp, vp, vp, u64, pu64, vp]
     lib.rk_multi_scan_mixed.restype = ci
@@ -100,7 +102,8 @@ def check(rc: int) -> None:
 
 
 class Context:
-    """One rk_ctx_t (per-device scratch: look-back status, tickets, staging rings)."""
+    """One rk_ctx_t (per-device scratch: per-tile results, counter sets, pattern cache,
+    staging rings); ``lock`` serialises the Python callers of a context."""
 
     def __init__(self, device: int):
         self.device = device

@@ -138,11 +138,11 @@ def scan_counts(text, pattern, hx: int, start: int, stop: int, *, out_bias: int 
                              out.data_ptr(), cap, ctypes.byref(mt), ctypes.byref(co),
                              ctypes.byref(hh), stream))
         k = int(mt.value)
-        if k > cap:  # the reference's overflow protocol: one more pass with exact room
+        if k > cap:
+            # the reference's overflow protocol (_scan.py:64-67) rescans with exact room;
+            # here only the ordered emission runs again, from the scan's per-tile results
             out = torch.empty(k, dtype=torch.int64, device=text.device)
-            _lib.check(L.rk_scan(ctx.handle, text.data_ptr(), n, _ptr(p), m, hx, start, stop,
-                                 out.data_ptr(), k, ctypes.byref(mt), ctypes.byref(co),
-                                 ctypes.byref(hh), stream))
+            _lib.check(L.rk_scan_fetch(ctx.handle, out.data_ptr(), k, stream))
     out = out[:k]
     if out_bias:
         out += out_bias

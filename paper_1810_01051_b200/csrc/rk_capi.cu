@@ -174,6 +174,8 @@ struct rk_ctx {
     std::vector<uint8_t> bytes;
     uint8_t* d = nullptr;
     uint64_t cap = 0;
+    uint8_t* h = nullptr;  // pinned source of the slot's upload (rewritten after a sync only)
+    uint64_t hcap = 0;
     uint64_t last_use = 0;
   };
   std::vector<PatSlot> pat_cache = std::vector<PatSlot>(64);
@@ -199,6 +201,19 @@ struct rk_ctx {
   uint64_t h_mstage_cap = 0;
   unsigned long long* h_mresult = nullptr;  // pinned: count, kMultiPrefix offsets, indices
   MultiPlan mplan;              // the last pattern set's plan (cache key + layout)
+  // The scratch above is ordered on the stream of the call that used it.  When a call
+  // arrives on another stream, that stream first waits for everything queued so far on
+  // the previous one (an event recorded lazily at the switch: an event between two
+  // launches on one stream would cost their programmatic-dependent-launch overlap).
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
+  cudaEvent_t ev_switch = nullptr;
+  // the last device scan's emission (rk_scan / rk_scan_async), for rk_scan_fetch
+  struct LastScan {
+    bool valid = false;
+    uint64_t tiles = 0, tile0 = 0;
+    int64_t start_bias = 0;
+  } last_scan;
   std::mutex mu;
 };
 
@@ -258,6 +273,17 @@ void select_set(rk_ctx* c, int k) {
   c->cur_set = k;
   c->d_counters = c->d_sets + (uint64_t)k * set_words(c);
   c->d_block_sums = c->d_counters + 4;
+}
+
+// Orders a call on stream s after all earlier work of the context (see rk_ctx::ev_switch).
+int enter(rk_ctx* c, cudaStream_t s) {
+  if (c->has_last && c->last_stream != s) {
+    RK_CUDA(cudaEventRecord(c->ev_switch, c->last_stream));
+    RK_CUDA(cudaStreamWaitEvent(s, c->ev_switch, 0));
+  }
+  c->last_stream = s;
+  c->has_last = true;
+  return RK_OK;
 }
 
 // Starts a logical scan of `tiles` tiles: per-tile buffers sized, and the next counter
@@ -387,7 +413,9 @@ bool hash_unreachable(uint32_t m, uint64_t hx) { return m <= 24 && (hx >> 32) !=
 // Device copy of the pattern from a small per-context cache (64 slots, LRU), so
 // repeated scans with the same patterns -- a length sweep, a service loop -- issue no
 // host-to-device copy and no synchronisation.  A slot is only overwritten after the
-// stream has drained, because an earlier kernel may still be reading it.
+// stream has drained (the context's earlier work on other streams is ordered before s,
+// see enter()), because an earlier kernel may still be reading it; the upload is an
+// asynchronous copy on s from the slot's pinned buffer, so the scan is ordered after it.
 int upload_pattern(rk_ctx* c, const uint8_t* h_pattern, uint32_t m, cudaStream_t s) {
   ++c->pat_clock;
   rk_ctx::PatSlot* victim = &c->pat_cache[0];
@@ -401,9 +429,17 @@ int upload_pattern(rk_ctx* c, const uint8_t* h_pattern, uint32_t m, cudaStream_t
   }
   RK_CUDA(cudaStreamSynchronize(s));
   if (int r = grow(&victim->d, &victim->cap, m, false, s)) return r;
+  if (victim->hcap < m) {
+    if (victim->h) RK_CUDA(cudaFreeHost(victim->h));
+    victim->h = nullptr;
+    victim->hcap = 0;
+    RK_CUDA(cudaMallocHost(&victim->h, std::max<uint64_t>(m, 64)));
+    victim->hcap = std::max<uint64_t>(m, 64);
+  }
   victim->bytes.assign(h_pattern, h_pattern + m);
   victim->last_use = c->pat_clock;
-  RK_CUDA(cudaMemcpy(victim->d, victim->bytes.data(), m, cudaMemcpyHostToDevice));
+  memcpy(victim->h, h_pattern, m);
+  RK_CUDA(cudaMemcpyAsync(victim->d, victim->h, m, cudaMemcpyHostToDevice, s));
   c->d_pattern = victim->d;
   return RK_OK;
 }
@@ -411,14 +447,18 @@ int upload_pattern(rk_ctx* c, const uint8_t* h_pattern, uint32_t m, cudaStream_t
 int enqueue_scan(rk_ctx* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_pattern,
                  uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t* d_out,
                  uint64_t cap, int64_t bias, cudaStream_t s, uint64_t* d_counts = nullptr) {
+  c->last_scan.valid = false;
   if (stop <= start || hash_unreachable(m, hx)) return zero_result(c, d_counts, s);
   if (int r = upload_pattern(c, h_pattern, m, s)) return r;
   const Geometry g = geometry(d_text, m, start, stop);
   if (int r = begin_scan(c, g.num_tiles, s)) return r;
   if (int r = launch_one(c, d_text, n, m, hx, start, stop, 0, pack_pattern(h_pattern, m), s))
     return r;
-  return emit(c, g.num_tiles, g.tile_first, bias - (int64_t)g.amis - (int64_t)m + 1, d_out, cap,
-              s, d_counts);
+  c->last_scan.valid = true;
+  c->last_scan.tiles = g.num_tiles;
+  c->last_scan.tile0 = g.tile_first;
+  c->last_scan.start_bias = bias - (int64_t)g.amis - (int64_t)m + 1;
+  return emit(c, g.num_tiles, g.tile_first, c->last_scan.start_bias, d_out, cap, s, d_counts);
 }
 
 int read_counters(rk_ctx* c, uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits,
@@ -699,6 +739,7 @@ int rk_ctx_create(int device, rk_ctx_t** out) {
   RK_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
   for (auto& e : c->ev_copied) RK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   RK_CUDA(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
+  RK_CUDA(cudaEventCreateWithFlags(&c->ev_switch, cudaEventDisableTiming));
   *out = c;
   return RK_OK;
 }
@@ -712,7 +753,11 @@ int rk_ctx_destroy(rk_ctx_t* c) {
   cudaFreeHost(c->h_counters);
   cudaFree(c->d_tile_info);
   cudaFree(c->d_masks);
-  for (auto& sl : c->pat_cache) cudaFree(sl.d);
+  for (auto& sl : c->pat_cache) {
+    cudaFree(sl.d);
+    cudaFreeHost(sl.h);
+  }
+  cudaEventDestroy(c->ev_switch);
   cudaFree(c->d_stage);
   cudaFree(c->d_out_stage);
   for (auto* h : c->h_ring) cudaFreeHost(h);
@@ -739,6 +784,7 @@ int rk_scan_async(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t*
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (int r = enter(c, s)) return r;
   return enqueue_scan(c, d_text, n, h_pattern, m, hx, start, stop, d_out, cap, out_bias, s,
                       d_counts);
 }
@@ -752,6 +798,8 @@ int rk_scan_bitmap(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (int r = enter(c, s)) return r;
+  c->last_scan.valid = false;
   if (stop > start)
     RK_CUDA(cudaMemsetAsync(d_bitmap, 0, ((stop - start + 31) / 32) * sizeof(uint32_t), s));
   if (stop <= start || hash_unreachable(m, hx)) return zero_result(c, d_counts, s);
@@ -770,6 +818,7 @@ int rk_scan_result(rk_ctx_t* c, uint64_t* matches, uint64_t* collisions, uint64_
   if (!c) return fail(RK_EINVAL, "context is NULL");
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
+  if (int r = enter(c, (cudaStream_t)stream)) return r;
   return read_counters(c, matches, collisions, hash_hits, (cudaStream_t)stream);
 }
 
@@ -781,6 +830,7 @@ int rk_scan(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_pat
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (int r = enter(c, s)) return r;
   if (stop <= start || hash_unreachable(m, hx)) {
     if (int r = enqueue_scan(c, d_text, n, h_pattern, m, hx, start, stop, d_out, cap, 0, s))
       return r;
@@ -808,7 +858,9 @@ int rk_scan_host(rk_ctx_t* c, const uint8_t* h_text, uint64_t n, const uint8_t* 
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
   cudaStream_t sc = c->s_comp, sk = c->s_copy;
+  if (int r = enter(c, sc)) return r;
   c->host_last = 0;
+  c->last_scan.valid = false;
   if (stop <= start || hash_unreachable(m, hx)) {
     if (int r = zero_result(c, nullptr, sc)) return r;
     return read_counters(c, matches, collisions, hash_hits, sc);
@@ -880,7 +932,6 @@ int rk_scan_host(rk_ctx_t* c, const uint8_t* h_text, uint64_t n, const uint8_t* 
   uint64_t mt = 0, co = 0, hh = 0;
   if (int r = read_counters(c, &mt, &co, &hh, sc)) return r;
   if (mt > icap) {
-    // more offsets than the staging output held: rescan the staged text on the device
     // more offsets than the staging output held: re-emit from the kept masks (no rescan)
     if (int r = grow(&c->d_out_stage, &c->out_stage_cap, mt, false, sc)) return r;
     if (int r = emit(c, gall.num_tiles, gall.tile_first, start_bias, c->d_out_stage, mt, sc))
@@ -902,18 +953,34 @@ int rk_scan_host(rk_ctx_t* c, const uint8_t* h_text, uint64_t n, const uint8_t* 
 
 int rk_scan_host_fetch(rk_ctx_t* c, int64_t* h_out, uint64_t first, uint64_t count) {
   if (!c) return fail(RK_EINVAL, "context is NULL");
+  std::lock_guard<std::mutex> lk(c->mu);
   if (first > c->host_last || count > c->host_last - first)
     return fail(RK_EINVAL, "fetch [%llu, %llu) beyond the %llu offsets of the last host scan",
                 (unsigned long long)first, (unsigned long long)(first + count),
                 (unsigned long long)c->host_last);
   if (!count) return RK_OK;
   if (!h_out) return fail(RK_EINVAL, "NULL output");
-  std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
+  if (int r = enter(c, c->s_comp)) return r;
   RK_CUDA(cudaMemcpyAsync(h_out, c->d_out_stage + first, count * sizeof(int64_t),
                           cudaMemcpyDeviceToHost, c->s_comp));
   RK_CUDA(cudaStreamSynchronize(c->s_comp));
   return RK_OK;
+}
+
+int rk_scan_fetch(rk_ctx_t* c, int64_t* d_out, uint64_t cap, void* stream) {
+  if (!c) return fail(RK_EINVAL, "context is NULL");
+  if (cap && !d_out) return fail(RK_EINVAL, "output pointer is NULL with cap > 0");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->last_scan.valid)
+    return fail(RK_EINVAL, "rk_scan_fetch: the context's last call was not a device scan "
+                "with matches to re-emit");
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int r = enter(c, s)) return r;
+  // the scan's per-tile results and block sums are still in the current counter set: the
+  // emit alone writes the ordered offsets again, now with room for cap of them
+  return emit(c, c->last_scan.tiles, c->last_scan.tile0, c->last_scan.start_bias, d_out, cap, s);
 }
 
 int rk_window_hashes(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, uint32_t m, uint64_t start,
@@ -972,6 +1039,7 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
   DeviceGuard dg(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   *pairs = 0;
+  if (int r = enter(c, s)) return r;
   uint64_t max_len = 0, min_len = ~0ull;
   for (uint32_t i = 0; i < P; ++i) {
     max_len = std::max<uint64_t>(max_len, h_lengths[i]);

@@ -147,10 +147,14 @@ def search_multi_sharded(shard, patterns, start_lo: int, start_hi: int, byte_lo:
             t_dev, dev = _device_text(_scan.as_u8(t))
             return multi_scan(t_dev, dev, pats)
 
+    from .matcher import PatternSet
+
+    # pair indices are PatternSet indices (deduplicated, first occurrence), as search_multi's
+    ps = patterns if isinstance(patterns, PatternSet) else PatternSet(patterns)
     dev = shard.device if isinstance(shard, torch.Tensor) else "cpu"
     idx_parts, off_parts = [], []
     if start_hi > start_lo:
-        per = multi_fn(shard, list(patterns))
+        per = multi_fn(shard, list(ps.patterns))
         lo, hi = start_lo - byte_lo, start_hi - byte_lo
         for i, offs in enumerate(per):
             offs = torch.as_tensor(np.asarray(offs, dtype=np.int64))

@@ -57,6 +57,14 @@ def main(rep, out, note="", launch=0):
         cnt = collections.Counter()
         data = [r for r in data
                 if len(r) >= len(hdr) and (r[idx["Instructions Executed"]] or "0").isdigit()]
+        # ncu may print a kernel's SASS listing more than once (one section per source
+        # view); every address counts once
+        seen, uniq = set(), []
+        for r in data:
+            if r[idx["Address"]] not in seen:
+                seen.add(r[idx["Address"]])
+                uniq.append(r)
+        data = uniq
         for r in data:
             toks = r[idx["Source"]].strip().split()
             if not toks:
