@@ -297,6 +297,14 @@ def load():
     lib.ro_search_multi.argtypes = [p, u64, p, p, ctypes.c_uint32, u64, p, p, u64, p]
     lib.ro_splitmix64_fill.restype = None
     lib.ro_splitmix64_fill.argtypes = [u64, u64, u64, p, ctypes.c_uint32, p]
+    lib.ro_scan_roll_mt.restype = u64
+    lib.ro_scan_roll_mt.argtypes = [p, p, u64, u64, u64, u64, ctypes.c_int, p, u64,
+                                    ctypes.POINTER(u64)]
+    lib.ro_fill_mt.restype = None
+    lib.ro_fill_mt.argtypes = [u64, u64, u64, p, ctypes.c_uint32, p, ctypes.c_int]
+    lib.ro_search_multi_mt.restype = u64
+    lib.ro_search_multi_mt.argtypes = [p, u64, p, p, ctypes.c_uint32, u64, ctypes.c_int, p, p,
+                                       u64, p]
     _lib = lib
     return lib
 
@@ -383,3 +391,98 @@ def cpu_threads() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------------------- full sizes
+def c_scan_mt(text: np.ndarray, pattern, start: int = 0, stop: int | None = None,
+              threads: int | None = None):
+    """_scan.py:28-50 over windows [start, stop) with the reference's exact rolling update
+    (rkhash.py:48-60) on pthreads: the checker for the 1-16 GiB configs.  `text` must hold
+    the bytes [0, stop + m - 1).  Returns (offsets int64[], collisions)."""
+    lib = load()
+    text = np.ascontiguousarray(text, dtype=np.uint8)
+    pat = np.frombuffer(bytes(pattern), dtype=np.uint8)
+    m = pat.size
+    if stop is None:
+        stop = text.size - m + 1
+    assert stop + m - 1 <= text.size
+    threads = threads or cpu_threads()
+    hx = hash_full(pat.tobytes())
+    coll = ctypes.c_uint64(0)
+    cap = 1 << 16
+    out = np.empty(cap, dtype=np.int64)
+    k = lib.ro_scan_roll_mt(text.ctypes.data, pat.ctypes.data, m, hx, start, stop, threads,
+                            out.ctypes.data, cap, ctypes.byref(coll))
+    if k > cap:
+        out = np.empty(k, dtype=np.int64)
+        k = lib.ro_scan_roll_mt(text.ctypes.data, pat.ctypes.data, m, hx, start, stop, threads,
+                                out.ctypes.data, k, ctypes.byref(coll))
+    return out[:k].copy(), int(coll.value)
+
+
+def c_fill(seed: int, skip: int, count: int, alphabet: bytes = b"ACGT",
+           threads: int | None = None) -> np.ndarray:
+    """Bytes [skip, skip + count) of generate(seed, ..., alphabet) (datagen.py:68-77)."""
+    lib = load()
+    out = np.empty(count, dtype=np.uint8)
+    if count:
+        alpha = np.frombuffer(alphabet, dtype=np.uint8)
+        lib.ro_fill_mt(ctypes.c_uint64(seed & MASK64), ctypes.c_uint64(skip),
+                       ctypes.c_uint64(count), alpha.ctypes.data, ctypes.c_uint32(len(alphabet)),
+                       out.ctypes.data, threads or cpu_threads())
+    return out
+
+
+def c_scan_generated(seed: int, n: int, alphabet: bytes, pattern, plants=(),
+                     piece: int = 1 << 30, threads: int | None = None):
+    """Scan the corpus generate(seed, n, alphabet) with `pattern` copied in at every
+    offset of `plants` (datagen.py:80-102 semantics) WITHOUT materialising it: the corpus
+    is regenerated on the host piece by piece (each piece carries the m - 1 bytes its last
+    windows need) and scanned with c_scan_mt.  Returns (offsets int64[], collisions)."""
+    pat = bytes(pattern)
+    m = len(pat)
+    parr = np.frombuffer(pat, dtype=np.uint8)
+    nw = n - m + 1
+    offs, coll = [], 0
+    for a in range(0, nw, piece):
+        b = min(a + piece, nw)
+        buf = c_fill(seed, a, b - a + m - 1, alphabet, threads)
+        for x in plants:
+            lo, hi = max(x, a), min(x + m, a + buf.size)
+            if lo < hi:
+                buf[lo - a: hi - a] = parr[lo - x: hi - x]
+        o, c = c_scan_mt(buf, pat, 0, b - a, threads)
+        offs.append(o + a)
+        coll += c
+    return (np.concatenate(offs) if offs else np.empty(0, np.int64)), coll
+
+
+def c_search_multi_mt(text: np.ndarray, pats: list[bytes], threads: int | None = None):
+    """One equal-length group of search_multi (matcher.py:139-153) on pthreads.  Returns
+    [(idx, offsets int64[])] in index order."""
+    lib = load()
+    text = np.ascontiguousarray(text, dtype=np.uint8)
+    P = len(pats)
+    m = len(pats[0])
+    buf = np.frombuffer(b"".join(pats), dtype=np.uint8)
+    ph = np.array([hash_full(p) for p in pats], dtype=np.uint64)
+    counts = np.zeros(P, dtype=np.uint64)
+    cap = 1 << 16
+    offs = np.empty(cap, dtype=np.int64)
+    idx = np.empty(cap, dtype=np.uint32)
+    th = threads or cpu_threads()
+    k = lib.ro_search_multi_mt(text.ctypes.data, text.size, buf.ctypes.data, ph.ctypes.data, P,
+                               m, th, offs.ctypes.data, idx.ctypes.data, cap, counts.ctypes.data)
+    if k > cap:
+        offs = np.empty(k, dtype=np.int64)
+        idx = np.empty(k, dtype=np.uint32)
+        k = lib.ro_search_multi_mt(text.ctypes.data, text.size, buf.ctypes.data, ph.ctypes.data,
+                                   P, m, th, offs.ctypes.data, idx.ctypes.data, k,
+                                   counts.ctypes.data)
+    out = []
+    base = 0
+    for i in range(P):
+        c = int(counts[i])
+        out.append((i, offs[base: base + c].copy()))
+        base += c
+    return out

@@ -18,6 +18,9 @@
  *   ro_window_hashes    _scan.py:71-91       batched u64 hash of windows [start, stop)
  *   ro_search_multi     matcher.py:125-157   per-length hash sweep, lookup, verify
  *   ro_splitmix64_fill  datagen.py:37-77     counter-based splitmix64 corpus bytes
+ *   ro_scan_roll_mt     _scan.py:28-50 with rkhash.py:48-60 `roll`, on pthreads (full sizes)
+ *   ro_fill_mt          ro_splitmix64_fill on pthreads
+ *   ro_search_multi_mt  matcher.py:139-153 per length group, rolled, on pthreads
  *
  * Parity is pinned by tests/test_oracle.py against golden vectors produced by the
  * reference itself (tests/golden/make_golden.py).
@@ -226,8 +229,228 @@ static inline uint64_t ro_mix(uint64_t z) {
 
 void ro_splitmix64_fill(uint64_t seed, uint64_t skip, uint64_t count, const uint8_t* alphabet,
                         uint32_t k, uint8_t* out) {
+    if ((k & (k - 1)) == 0) { /* z mod k == z & (k - 1) for a power of two */
+        for (uint64_t i = 0; i < count; ++i)
+            out[i] = alphabet[ro_mix(seed + 0x9E3779B97F4A7C15ull * (skip + i + 1)) & (k - 1)];
+        return;
+    }
     for (uint64_t i = 0; i < count; ++i) {
         uint64_t z = ro_mix(seed + 0x9E3779B97F4A7C15ull * (skip + i + 1));
         out[i] = alphabet[z % (uint64_t)k];
     }
+}
+
+/* ------------------------------------------------------------------------------------
+ * Full-size checkers (still TEST INFRASTRUCTURE ONLY).  The same per-window decisions as
+ * ro_scan_range (_scan.py:35-49), but the window hash is carried by the reference's own
+ * exact rolling update (rkhash.py:48-60, `roll`: h' = ((h - out * 2^(m-1)) * 2 + in)
+ * mod 2^64) instead of being refolded per window, so a 16 GiB scan finishes in seconds
+ * on the host cores.  The range split is parallel.py:155-161's contiguous partition;
+ * results are concatenated in range order (parallel.py:168-172).
+ */
+typedef struct {
+    const uint8_t* text;
+    const uint8_t* pattern;
+    uint64_t m, hx, start, stop;
+    int64_t* offs;
+    uint64_t n, cap, coll;
+} ro_roll_job;
+
+static void ro_push(int64_t** v, uint64_t* n, uint64_t* cap, int64_t x) {
+    if (*n == *cap) {
+        *cap = *cap ? 2 * *cap : 1024;
+        *v = (int64_t*)realloc(*v, *cap * sizeof(int64_t));
+    }
+    (*v)[(*n)++] = x;
+}
+
+static void* ro_roll_run(void* arg) {
+    ro_roll_job* j = (ro_roll_job*)arg;
+    const uint8_t* t = j->text;
+    const uint64_t m = j->m;
+    const uint64_t top = m - 1 < 64 ? m - 1 : 64; /* out * 2^(m-1) vanishes for m > 64 */
+    uint64_t h = ro_hash_full(t + j->start, m);
+    for (uint64_t x = j->start; x < j->stop; ++x) {
+        if (h == j->hx) {
+            if (memcmp(t + x, j->pattern, m) == 0)
+                ro_push(&j->offs, &j->n, &j->cap, (int64_t)x);
+            else
+                ++j->coll;
+        }
+        if (x + 1 < j->stop) {
+            const uint64_t out = top < 64 ? ((uint64_t)t[x] << top) : 0;
+            h = ((h - out) << 1) + (uint64_t)t[x + m];
+        }
+    }
+    return NULL;
+}
+
+/* Windows [start, stop) of text (which holds at least stop + m - 1 bytes) on `threads`
+ * pthreads.  Writes up to cap offsets (ascending), returns the match count; *collisions
+ * receives the hash-equal-but-bytes-differ count. */
+uint64_t ro_scan_roll_mt(const uint8_t* text, const uint8_t* pattern, uint64_t m, uint64_t hx,
+                         uint64_t start, uint64_t stop, int threads, int64_t* out, uint64_t cap,
+                         uint64_t* collisions) {
+    *collisions = 0;
+    if (m == 0 || stop <= start) return 0;
+    if (threads < 1) threads = 1;
+    const uint64_t total = stop - start;
+    const uint64_t chunk = (total + (uint64_t)threads - 1) / (uint64_t)threads;
+    ro_roll_job* jobs = (ro_roll_job*)calloc((size_t)threads, sizeof(ro_roll_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    int nj = 0;
+    for (int w = 0; w < threads; ++w) {
+        uint64_t s = start + (uint64_t)w * chunk, e = s + chunk;
+        if (e > stop) e = stop;
+        if (s >= e) break;
+        ro_roll_job* j = &jobs[nj++];
+        j->text = text; j->pattern = pattern; j->m = m; j->hx = hx; j->start = s; j->stop = e;
+    }
+    for (int i = 0; i < nj; ++i) pthread_create(&th[i], NULL, ro_roll_run, &jobs[i]);
+    for (int i = 0; i < nj; ++i) pthread_join(th[i], NULL);
+    uint64_t k = 0;
+    for (int i = 0; i < nj; ++i) {
+        for (uint64_t q = 0; q < jobs[i].n; ++q, ++k)
+            if (k < cap) out[k] = jobs[i].offs[q];
+        *collisions += jobs[i].coll;
+        free(jobs[i].offs);
+    }
+    free(jobs);
+    free(th);
+    return k;
+}
+
+typedef struct {
+    uint64_t seed, skip, count;
+    const uint8_t* alphabet;
+    uint32_t k;
+    uint8_t* out;
+} ro_fill_job;
+
+static void* ro_fill_run(void* arg) {
+    ro_fill_job* j = (ro_fill_job*)arg;
+    ro_splitmix64_fill(j->seed, j->skip, j->count, j->alphabet, j->k, j->out);
+    return NULL;
+}
+
+/* ro_splitmix64_fill split over `threads` pthreads (counter-based: byte i depends only
+ * on skip + i). */
+void ro_fill_mt(uint64_t seed, uint64_t skip, uint64_t count, const uint8_t* alphabet, uint32_t k,
+                uint8_t* out, int threads) {
+    if (threads < 1) threads = 1;
+    const uint64_t chunk = (count + (uint64_t)threads - 1) / (uint64_t)threads;
+    ro_fill_job* jobs = (ro_fill_job*)calloc((size_t)threads, sizeof(ro_fill_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    int nj = 0;
+    for (int w = 0; w < threads; ++w) {
+        uint64_t s = (uint64_t)w * chunk, e = s + chunk;
+        if (e > count) e = count;
+        if (s >= e) break;
+        ro_fill_job* j = &jobs[nj++];
+        j->seed = seed; j->skip = skip + s; j->count = e - s; j->alphabet = alphabet; j->k = k;
+        j->out = out + s;
+    }
+    for (int i = 0; i < nj; ++i) pthread_create(&th[i], NULL, ro_fill_run, &jobs[i]);
+    for (int i = 0; i < nj; ++i) pthread_join(th[i], NULL);
+    free(jobs);
+    free(th);
+}
+
+/* matcher.py:139-153 for one equal-length group, over windows [start, stop), on pthreads:
+ * each window's hash (rolled, as above) is looked up among the sorted pattern hashes
+ * (the reference compares it with every indexed hash, :147-148 -- same hit set) and
+ * every pattern carrying it is byte-compared (:149-153).  Output as ro_search_multi:
+ * pairs grouped per pattern index, ascending offsets; counts[P] per-pattern totals. */
+typedef struct {
+    const uint8_t* text;
+    const uint8_t* pats;
+    const ro_key* keys;
+    const uint8_t* filt; /* 2^16-bit presence filter over the low 16 hash bits */
+    uint32_t P;
+    uint64_t m, start, stop;
+    int64_t* offs; /* interleaved (offset, index) pairs */
+    uint64_t n, cap;
+} ro_multi_job;
+
+static void* ro_multi_run(void* arg) {
+    ro_multi_job* j = (ro_multi_job*)arg;
+    const uint8_t* t = j->text;
+    const uint64_t m = j->m;
+    const uint64_t top = m - 1 < 64 ? m - 1 : 64;
+    uint64_t h = ro_hash_full(t + j->start, m);
+    for (uint64_t x = j->start; x < j->stop; ++x) {
+        const uint32_t lo = (uint32_t)(h & 0xffff);
+        if (j->filt[lo >> 3] & (1u << (lo & 7))) {
+            uint32_t a = 0, b = j->P;
+            while (a < b) {
+                uint32_t mid = (a + b) >> 1;
+                if (j->keys[mid].h < h) a = mid + 1; else b = mid;
+            }
+            for (uint32_t q = a; q < j->P && j->keys[q].h == h; ++q) {
+                const uint32_t i = j->keys[q].idx;
+                if (memcmp(t + x, j->pats + (uint64_t)i * m, m) == 0) {
+                    ro_push(&j->offs, &j->n, &j->cap, (int64_t)x);
+                    ro_push(&j->offs, &j->n, &j->cap, (int64_t)i);
+                }
+            }
+        }
+        if (x + 1 < j->stop) {
+            const uint64_t out = top < 64 ? ((uint64_t)t[x] << top) : 0;
+            h = ((h - out) << 1) + (uint64_t)t[x + m];
+        }
+    }
+    return NULL;
+}
+
+uint64_t ro_search_multi_mt(const uint8_t* text, uint64_t n, const uint8_t* pats,
+                            const uint64_t* phash, uint32_t P, uint64_t m, int threads,
+                            int64_t* out_off, uint32_t* out_idx, uint64_t cap, uint64_t* counts) {
+    for (uint32_t i = 0; i < P; ++i) counts[i] = 0;
+    if (m == 0 || m > n || P == 0) return 0;
+    if (threads < 1) threads = 1;
+    const uint64_t nw = n - m + 1;
+    ro_key* keys = (ro_key*)malloc(sizeof(ro_key) * P);
+    uint8_t* filt = (uint8_t*)calloc(1 << 13, 1);
+    for (uint32_t i = 0; i < P; ++i) {
+        keys[i].h = phash[i];
+        keys[i].idx = i;
+        const uint32_t lo = (uint32_t)(phash[i] & 0xffff);
+        filt[lo >> 3] |= (uint8_t)(1u << (lo & 7));
+    }
+    qsort(keys, P, sizeof(ro_key), ro_key_cmp);
+    const uint64_t chunk = (nw + (uint64_t)threads - 1) / (uint64_t)threads;
+    ro_multi_job* jobs = (ro_multi_job*)calloc((size_t)threads, sizeof(ro_multi_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    int nj = 0;
+    for (int w = 0; w < threads; ++w) {
+        uint64_t s = (uint64_t)w * chunk, e = s + chunk;
+        if (e > nw) e = nw;
+        if (s >= e) break;
+        ro_multi_job* j = &jobs[nj++];
+        j->text = text; j->pats = pats; j->keys = keys; j->filt = filt; j->P = P; j->m = m;
+        j->start = s; j->stop = e;
+    }
+    for (int i = 0; i < nj; ++i) pthread_create(&th[i], NULL, ro_multi_run, &jobs[i]);
+    for (int i = 0; i < nj; ++i) pthread_join(th[i], NULL);
+    for (int i = 0; i < nj; ++i)
+        for (uint64_t q = 0; q < jobs[i].n; q += 2) counts[jobs[i].offs[q + 1]]++;
+    uint64_t* base = (uint64_t*)calloc(P + 1, sizeof(uint64_t));
+    for (uint32_t i = 0; i < P; ++i) base[i + 1] = base[i] + counts[i];
+    /* ranges are ascending, so filling in range order keeps every pattern's offsets sorted */
+    for (int i = 0; i < nj; ++i) {
+        for (uint64_t q = 0; q < jobs[i].n; q += 2) {
+            const uint32_t idx = (uint32_t)jobs[i].offs[q + 1];
+            const uint64_t pos = base[idx]++;
+            if (pos < cap) { out_off[pos] = jobs[i].offs[q]; out_idx[pos] = idx; }
+        }
+        free(jobs[i].offs);
+    }
+    uint64_t total = 0;
+    for (uint32_t i = 0; i < P; ++i) total += counts[i];
+    free(base);
+    free(jobs);
+    free(th);
+    free(keys);
+    free(filt);
+    return total;
 }

@@ -55,3 +55,55 @@ def launch():
 
 
 ASCII = bytes(range(32, 127))
+
+
+def acceptance():
+    return load("acceptance.json")
+
+
+def criterion1_cases():
+    """The 10,008 cases of the reference's criterion 1
+    (/root/reference/pkg/tests/test_acceptance.py:49-85), regenerated from the same seed
+    and draw sequence, each with the reference's recorded answer:
+    yields (case, text, pattern, workers, block_dim, expected) with expected =
+    [n, m, k, matches, collisions, sha1-16 of the int64 offsets]."""
+    import numpy as np
+
+    rng = np.random.default_rng(20240810)
+    workers_grid, block_grid = (1, 2, 4, 8), (32, 256, 1024)
+    for case, exp in enumerate(acceptance()["criterion1"]):
+        k = (2, 4, 256)[case % 3]
+        n = int(rng.integers(1, 4097))
+        m = int(rng.integers(1, 65))
+        text = rng.integers(0, k, size=n, dtype=np.uint8).tobytes()
+        if m <= n and rng.random() < 0.5:
+            x = int(rng.integers(0, n - m + 1))
+            pattern = text[x: x + m]
+        else:
+            pattern = rng.integers(0, k, size=m, dtype=np.uint8).tobytes()
+        assert exp[:3] == [n, m, k], (case, exp[:3], (n, m, k))  # draw sequence in step
+        yield (case, text, pattern, workers_grid[case % 4], block_grid[(case // 4) % 3], exp)
+
+
+def criterion5_texts():
+    """The 1,000 texts of criterion 5 (test_acceptance.py:156-182): yields (text, m,
+    sha1-16 of the reference's uint64 window hashes)."""
+    import numpy as np
+
+    rng = np.random.default_rng(5150)
+    for exp in acceptance()["criterion5"]:
+        n = int(rng.integers(2, 4097))
+        m = int(rng.integers(1, 65))
+        if m >= n:
+            m = n - 1 or 1
+        text = rng.integers(0, 256, size=n, dtype=np.uint8).tobytes()
+        assert exp[:2] == [n, m]
+        yield text, m, exp[2]
+
+
+def digest(values, dtype) -> str:
+    import hashlib
+
+    import numpy as np
+
+    return hashlib.sha1(np.asarray(values, dtype=dtype).tobytes()).hexdigest()[:16]

@@ -18,6 +18,8 @@ Output files (JSON; texts are zlib+base64 encoded):
   corpus.json      splitmix64 chains, corpus sha256s, C1/C2-at-1MiB/DNA goldens
   multi_cases.json search_multi cases
   launch.json      plan_launch / offset_of known answers
+  acceptance.json  the reference's acceptance criteria 1, 4, 5 case by case (answers only;
+                   inputs are regenerated from the same seeds in tests/_golden.py)
 """
 
 from __future__ import annotations
@@ -305,7 +307,77 @@ def main() -> None:
         launch["offset_of"].append({"block_idx": [bx, by, bz], "thread": t, "grid": list(dims),
                                     "block": b, "offset": x})
     (OUT / "launch.json").write_text(json.dumps(launch))
+
+    # ------------------------------------------------------------------ acceptance suite
+    acceptance(rk, _scan)
     print("golden fixtures written to", OUT)
+
+
+def _digest(values, dtype) -> str:
+    return hashlib.sha1(np.asarray(values, dtype=dtype).tobytes()).hexdigest()[:16]
+
+
+def acceptance(rk, _scan) -> None:
+    """acceptance.json: the reference's own acceptance criteria 1, 4 and 5
+    (/root/reference/pkg/tests/test_acceptance.py:49-85, :124-153, :156-182) recorded
+    case by case.  The inputs are NOT stored: tests regenerate them from the same numpy
+    seeds and draw sequence (tests/_golden.acceptance_cases), so only the reference's
+    answers are kept -- per case (n, m, k, match count, collisions, sha1 of the int64
+    offsets)."""
+    acc = {}
+    rng = np.random.default_rng(20240810)
+    crit1 = []
+    for case in range(10_008):
+        k = (2, 4, 256)[case % 3]
+        n = int(rng.integers(1, 4097))
+        m = int(rng.integers(1, 65))
+        text = rng.integers(0, k, size=n, dtype=np.uint8).tobytes()
+        if m <= n and rng.random() < 0.5:
+            x = int(rng.integers(0, n - m + 1))
+            pattern = text[x: x + m]
+        else:
+            pattern = rng.integers(0, k, size=m, dtype=np.uint8).tobytes()
+        st = rk.ScanStats()
+        res = rk.search_sequential(text, pattern, stats=st)
+        if case % 50 == 0:  # the reference's own equivalences, spot-checked here
+            assert res == rk.search_naive(text, pattern)
+            cfg = rk.plan_launch(n, m, 32) if m <= n else rk.LaunchConfig((1, 1, 1), 32)
+            assert rk.search_parallel(text, pattern, cfg, 4) == res
+        crit1.append([n, m, k, len(res.offsets), st.collisions, _digest(res.offsets, np.int64)])
+    acc["criterion1"] = crit1
+
+    filler = rk.generate(rk.DnaSpec(seed=11, length=5000))
+    texts = [b"ac" + b"Xba" * 300, rk.plant(filler, b"ba", list(range(0, 4000, 13))),
+             b"ba" * 64 + b"ac" + b"ba" * 64]
+    crit4 = []
+    for ti, text in enumerate(texts):
+        for pattern in (b"ac", b"ba"):
+            st = rk.ScanStats()
+            res = rk.search_sequential(text, pattern, stats=st)
+            multi = dict(rk.search_multi(text, rk.PatternSet([pattern])))
+            assert multi[0] == res
+            crit4.append({"text": ti, "pattern": pattern.decode(), "offsets": res.offsets,
+                          "collisions": st.collisions, "hash_hits": st.hash_hits})
+    acc["criterion4"] = crit4
+
+    rng = np.random.default_rng(5150)
+    crit5 = []
+    for _ in range(1000):
+        n = int(rng.integers(2, 4097))
+        m = int(rng.integers(1, 65))
+        if m >= n:
+            m = n - 1 or 1
+        text = rng.integers(0, 256, size=n, dtype=np.uint8).tobytes()
+        h = _scan.window_hashes(_scan.as_u8(text), m, 0, n - m + 1)
+        roll = [rk.hash_window(text, 0, m)]
+        for x in range(n - m):
+            roll.append(rk.roll(roll[-1], text[x], text[x + m], m))
+        assert [int(v) for v in h] == roll
+        crit5.append([n, m, _digest(h, np.uint64)])
+    base = bytes(rng.integers(0, 256, size=80, dtype=np.uint8))
+    acc["criterion5"] = crit5
+    acc["criterion5_m65"] = {"base": enc(base), "h": str(rk.hash_window(base, 0, 65))}
+    (OUT / "acceptance.json").write_text(json.dumps(acc, separators=(",", ":")))
 
 
 if __name__ == "__main__":

@@ -205,3 +205,28 @@ def test_shard_ranges_cover_exactly_once():
             r = shard_ranges(W, G_)
             covered = [x for a, b in r for x in range(a, b)]
             assert covered == list(range(W))
+
+
+def test_acceptance_criterion5_host_roll(golden):
+    """The reference's criterion 5 (test_acceptance.py:156-182) on the host hash
+    functions: rolling every window of the 1,000 texts with rk.roll tracks
+    rk.hash_window, and the chain's digest is the reference's."""
+    import numpy as np
+
+    for j, (text, m, dig) in enumerate(golden.criterion5_texts()):
+        h = rk.hash_window(text, 0, m)
+        chain = [h]
+        for x in range(len(text) - m):
+            h = rk.roll(h, text[x], text[x + m], m)
+            chain.append(h)
+        if j % 25 == 0:
+            assert chain[-1] == rk.hash_window(text, len(text) - m, m)
+        assert golden.digest(chain, np.uint64) == dig
+    c = golden.acceptance()["criterion5_m65"]
+    base = golden.dec(c["base"])
+    variant = bytes([base[0] ^ 0xFF]) + base[1:]
+    assert rk.hash_window(base, 0, 65) == rk.hash_window(variant, 0, 65) == int(c["h"])
+    h = rk.hash_window(base, 0, 65)
+    for x in range(len(base) - 65):
+        h = rk.roll(h, base[x], base[x + 65], 65)
+        assert h == rk.hash_window(base, x + 1, 65)

@@ -152,3 +152,59 @@ def test_roll_matches_window_hashes(m):
     for x in range(t.size - m):
         cur = oracle.roll(cur, int(t[x]), int(t[x + m]), m)
         assert cur == int(h[x + 1])
+
+
+# --------------------------------------------------------------------------- acceptance
+def test_acceptance_criterion1_c_oracle(golden):
+    """All 10,008 cases of the reference's criterion 1 (test_acceptance.py:49-85): the C
+    oracle (per-window and rolled, parallel partition included) gives the reference's
+    recorded offsets and collision counts."""
+    import numpy as np
+
+    n_cases = 0
+    for case, text, pattern, workers, block, exp in golden.criterion1_cases():
+        n, m = len(text), len(pattern)
+        t = np.frombuffer(text, dtype=np.uint8)
+        p = np.frombuffer(pattern, dtype=np.uint8)
+        if m > n:
+            assert exp[3] == 0 and exp[4] == 0
+            continue
+        eo, ec = oracle.c_scan(t, p)
+        assert (eo.size, ec, golden.digest(eo, np.int64)) == tuple(exp[3:]), case
+        if case % 4 == 0:
+            ro, rc = oracle.c_scan_mt(t, pattern, threads=workers)
+            assert ro.size == eo.size and (ro == eo).all() and rc == ec, case
+        n_cases += 1
+    assert n_cases > 9000
+
+
+def test_acceptance_criterion4_collision_family(golden):
+    """Criterion 4 (test_acceptance.py:124-153) with the oracle: byte-true offsets and the
+    reference's collision counts; the verify-fail branch is taken."""
+    import numpy as np
+
+    filler = oracle.generate(11, 5000)
+    texts = [b"ac" + b"Xba" * 300, oracle.plant(filler, b"ba", list(range(0, 4000, 13))),
+             b"ba" * 64 + b"ac" + b"ba" * 64]
+    total = 0
+    for c in golden.acceptance()["criterion4"]:
+        text, pat = texts[c["text"]], c["pattern"].encode()
+        eo, ec = oracle.c_scan(np.frombuffer(text, np.uint8), np.frombuffer(pat, np.uint8))
+        assert eo.tolist() == c["offsets"] == oracle.search_naive(text, pat)
+        assert ec == c["collisions"] and c["hash_hits"] == len(c["offsets"]) + ec
+        total += ec
+    assert total > 0
+
+
+def test_acceptance_criterion5_rolling(golden):
+    """Criterion 5 (test_acceptance.py:156-182): the oracle's batched window hashes give
+    the reference's recorded digests for all 1,000 texts, and the m = 65 horizon case."""
+    import numpy as np
+
+    for text, m, dig in golden.criterion5_texts():
+        t = np.frombuffer(text, dtype=np.uint8)
+        assert golden.digest(oracle.c_window_hashes(t, m, 0, t.size - m + 1), np.uint64) == dig
+    c = golden.acceptance()["criterion5_m65"]
+    base = golden.dec(c["base"])
+    variant = bytes([base[0] ^ 0xFF]) + base[1:]
+    assert oracle.hash_window(base, 0, 65) == oracle.hash_window(variant, 0, 65) == int(c["h"])
