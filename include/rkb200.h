@@ -12,7 +12,8 @@
  *     device, `h_` pointers are host memory (pinned or pageable).
  *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
  *   - Every function returns 0 on success, RK_EINVAL for argument errors (the Python
- *     layer maps it to ValueError), RK_ECUDA for CUDA failures (RuntimeError).
+ *     layer maps it to ValueError), RK_ECUDA for CUDA failures and RK_ENCCL for NCCL
+ *     failures (RuntimeError).
  *     rk_last_error() returns the calling thread's last message.
  *   - A context owns per-device scratch (per-tile match counts and hit masks, counter
  *     sets, the pattern cache, staging buffers).  Calls on one context are serialised by
@@ -35,6 +36,7 @@ extern "C" {
 #define RK_OK 0
 #define RK_EINVAL 1
 #define RK_ECUDA 2
+#define RK_ENCCL 3
 
 typedef struct rk_ctx rk_ctx_t;
 
@@ -153,6 +155,53 @@ int rk_window_hashes(rk_ctx_t* ctx, const uint8_t* d_text, uint64_t n, uint32_t 
  */
 int rk_generate(rk_ctx_t* ctx, uint8_t* d_out, uint64_t count, uint64_t seed, uint64_t skip,
                 const uint8_t* h_alphabet, uint32_t k, void* stream);
+
+/*
+ * Multi-GPU (one process per GPU) -- the range partition and ordered merge of
+ * search_parallel (parallel.py:155-172) across GPUs.  NCCL is loaded at run time
+ * (libnccl.so.2, or $RKB200_NCCL_LIB); where it is absent these return RK_ENCCL.
+ *
+ * rk_comm_get_unique_id writes the 128-byte NCCL unique id (on one rank; the caller ships
+ * it to the others, e.g. through torch.distributed's store).  rk_comm_init creates this
+ * rank's communicator over the context's device (collective over all ranks).
+ * $RKB200_COMM_LOG=1 logs each rank's init to stderr.
+ */
+#define RK_COMM_ID_BYTES 128
+typedef struct rk_comm rk_comm_t;
+int rk_comm_get_unique_id(uint8_t* id);
+int rk_comm_init(rk_ctx_t* ctx, const uint8_t* id, int nranks, int rank, rk_comm_t** out);
+int rk_comm_destroy(rk_comm_t* comm);
+int rk_comm_info(rk_comm_t* comm, int* nranks, int* rank, int* nccl_version);
+
+/*
+ * rk_shard_range -- rank's part of the strong partition of an n-byte text for m-byte
+ * windows (parallel.py:155-161: ceil(W / G) contiguous windows per rank, W = n - m + 1):
+ * global windows [win_lo, win_hi) and the bytes [byte_lo, byte_hi) they read (the
+ * shard plus its (m-1)-byte halo).
+ */
+int rk_shard_range(uint64_t n, uint32_t m, int nranks, int rank, uint64_t* win_lo,
+                   uint64_t* win_hi, uint64_t* byte_lo, uint64_t* byte_hi);
+
+/*
+ * rk_scan_sharded -- collective over the communicator's ranks.  Each rank passes the bytes
+ * it holds, text = global bytes [byte_lo, byte_lo + len) (device memory of the context's
+ * device, or host memory: then staged into HBM chunk by chunk as in rk_scan_host), and
+ * its global windows [win_lo, win_hi) (which must lie in those bytes).  Every rank scans
+ * its own windows with no inter-GPU traffic; then the ranks' counters are all-gathered
+ * and every rank's ordered offsets are broadcast into every rank's d_out at the rank's
+ * prefix (an allgather-v: ranks in order = globally ascending).  d_out receives the first
+ * min(total, cap) GLOBAL offsets (stream-ordered on `stream`); *matches / *collisions /
+ * *hash_hits are the totals over all ranks, known to the host on return.
+ */
+int rk_scan_sharded(rk_comm_t* comm, const uint8_t* text, uint64_t len, uint64_t byte_lo,
+                    const uint8_t* h_pattern, uint32_t m, uint64_t hx, uint64_t win_lo,
+                    uint64_t win_hi, int64_t* d_out, uint64_t cap, uint64_t* matches,
+                    uint64_t* collisions, uint64_t* hash_hits, void* stream);
+
+/* Copies offsets [first, first + count) of the last rk_scan_sharded on this communicator
+ * whose total exceeded its cap (every rank keeps the whole gathered list, so a caller
+ * whose cap was too small never rescans).  Stream-ordered on `stream`. */
+int rk_comm_fetch(rk_comm_t* comm, int64_t* d_out, uint64_t first, uint64_t count, void* stream);
 
 /* Number of kernel launches issued by this context so far (bench accounting). */
 uint64_t rk_launch_count(rk_ctx_t* ctx);

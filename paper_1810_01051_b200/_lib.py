@@ -15,7 +15,8 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "librkb200.so"
 
-RK_OK, RK_EINVAL, RK_ECUDA = 0, 1, 2
+RK_OK, RK_EINVAL, RK_ECUDA, RK_ENCCL = 0, 1, 2, 3
+COMM_ID_BYTES = 128
 MULTI_MAX_PATTERNS = 4096
 
 # every symbol include/rkb200.h declares (checked by tests/test_capi.py)
@@ -24,6 +25,8 @@ EXPORTS = (
     "rk_scan", "rk_scan_async", "rk_scan_result", "rk_scan_bitmap", "rk_scan_host",
     "rk_scan_host_fetch", "rk_scan_fetch",
     "rk_multi_scan", "rk_multi_scan_mixed", "rk_window_hashes", "rk_generate", "rk_launch_count",
+    "rk_comm_get_unique_id", "rk_comm_init", "rk_comm_destroy", "rk_comm_info", "rk_shard_range",
+    "rk_scan_sharded", "rk_comm_fetch",
 )
 
 _lib = None
@@ -72,6 +75,22 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.rk_generate.argtypes = [vp, vp, u64, u64, u64, u8p, u32, vp]
     lib.rk_launch_count.restype = u64
     lib.rk_launch_count.argtypes = [vp]
+    pi = ctypes.POINTER(ci)
+    lib.rk_comm_get_unique_id.restype = ci
+    lib.rk_comm_get_unique_id.argtypes = [vp]
+    lib.rk_comm_init.restype = ci
+    lib.rk_comm_init.argtypes = [vp, vp, ci, ci, ctypes.POINTER(vp)]
+    lib.rk_comm_destroy.restype = ci
+    lib.rk_comm_destroy.argtypes = [vp]
+    lib.rk_comm_info.restype = ci
+    lib.rk_comm_info.argtypes = [vp, pi, pi, pi]
+    lib.rk_shard_range.restype = ci
+    lib.rk_shard_range.argtypes = [u64, u32, ci, ci, pu64, pu64, pu64, pu64]
+    lib.rk_comm_fetch.restype = ci
+    lib.rk_comm_fetch.argtypes = [vp, vp, u64, u64, vp]
+    lib.rk_scan_sharded.restype = ci
+    lib.rk_scan_sharded.argtypes = [vp, u8p, u64, u64, u8p, u32, u64, u64, u64, vp, u64, pu64,
+                                    pu64, pu64, vp]
 
 
 def lib() -> ctypes.CDLL:
@@ -98,6 +117,8 @@ def check(rc: int) -> None:
     msg = lib().rk_last_error().decode("utf-8", "replace")
     if rc == RK_EINVAL:
         raise ValueError(msg)
+    if rc == RK_ENCCL:
+        raise RuntimeError(f"librkb200 (NCCL): {msg}")
     raise RuntimeError(f"librkb200: {msg}")
 
 
@@ -151,14 +172,53 @@ def context(device: int | None = None) -> Context:
         return c
 
 
+_spare: dict[int, list[Context]] = {}
+
+
+class _Held:
+    def __init__(self, ctx: Context, spare: bool):
+        self.ctx, self.spare = ctx, spare
+
+    def __enter__(self) -> Context:
+        return self.ctx
+
+    def __exit__(self, *exc) -> None:
+        self.ctx.lock.release()
+        if self.spare:
+            with _ctx_lock:
+                _spare.setdefault(self.ctx.device, []).append(self.ctx)
+
+
+def acquire(device: int | None = None) -> _Held:
+    """A context of ``device`` held for one call (``with acquire(dev) as ctx: ...``).
+
+    The device's primary context when it is free, else a spare one from a per-device pool
+    (created on demand): concurrent callers -- the reference runs range scans concurrently
+    on a thread pool (parallel.py:111-121, :162-167) -- each get their own scratch and
+    staging streams and run in parallel instead of queueing on one context."""
+    if device is None:
+        device = default_device()
+    primary = context(device)
+    if primary.lock.acquire(blocking=False):
+        return _Held(primary, False)
+    with _ctx_lock:
+        pool = _spare.get(device)
+        c = pool.pop() if pool else None
+    if c is None:
+        c = Context(device)
+    c.lock.acquire()
+    return _Held(c, True)
+
+
 @atexit.register
 def _close_all() -> None:  # pragma: no cover
-    for c in list(_ctx.values()):
+    for c in list(_ctx.values()) + [x for v in _spare.values() for x in v]:
         try:
             c.close()
         except Exception:
             pass
     _ctx.clear()
+    _spare.clear()
 
 
 def u64ref(v: int = 0):

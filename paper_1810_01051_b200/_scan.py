@@ -112,10 +112,9 @@ def scan_counts(text, pattern, hx: int, start: int, stop: int, *, out_bias: int 
     dev = _device_of(text)
     if dev is None:
         t = _host_bytes(text)
-        ctx = _lib.context()
         cap = max(0, min(stop - start, _INITIAL_CAPACITY))
         out = np.empty(max(cap, 1), dtype=np.int64)
-        with ctx.lock:
+        with _lib.acquire() as ctx:
             _lib.check(L.rk_scan_host(ctx.handle, _ptr(t), n, _ptr(p), m, hx, start, stop,
                                       out.ctypes.data, cap, ctypes.byref(mt), ctypes.byref(co),
                                       ctypes.byref(hh)))
@@ -129,11 +128,10 @@ def scan_counts(text, pattern, hx: int, start: int, stop: int, *, out_bias: int 
         return out, k, int(co.value), int(hh.value)
 
     torch = _torch()
-    ctx = _lib.context(dev)
     stream = _stream(dev)
     cap = max(0, min(stop - start, _INITIAL_CAPACITY))
     out = torch.empty(max(cap, 1), dtype=torch.int64, device=text.device)
-    with ctx.lock:
+    with _lib.acquire(dev) as ctx:
         _lib.check(L.rk_scan(ctx.handle, text.data_ptr(), n, _ptr(p), m, hx, start, stop,
                              out.data_ptr(), cap, ctypes.byref(mt), ctypes.byref(co),
                              ctypes.byref(hh), stream))
@@ -182,11 +180,10 @@ def scan_bitmap(text, pattern, hx: int, start: int, stop: int, *, packed: bool =
         t = torch.from_numpy(np.array(_host_bytes(text), copy=True)).to(f"cuda:{dev}")
     else:
         t = text
-    ctx = _lib.context(dev)
     words = torch.zeros(max((count + 31) // 32, 1), dtype=torch.int32, device=t.device)
     counts = torch.zeros(3, dtype=torch.int64, device=t.device)
     stream = _stream(dev)
-    with ctx.lock:
+    with _lib.acquire(dev) as ctx:
         _lib.check(L.rk_scan_bitmap(ctx.handle, t.data_ptr() if n else 0, n, _ptr(p), m,
                                     int(hx) & ((1 << 64) - 1), start, max(stop, start),
                                     words.data_ptr(), counts.data_ptr(), stream))
@@ -224,10 +221,9 @@ def window_hashes(text, m: int, start: int, stop: int):
         t = torch.from_numpy(np.ascontiguousarray(text)).to(f"cuda:{dev}")
     else:
         t = text
-    ctx = _lib.context(dev)
     out = torch.empty(stop - start, dtype=torch.uint64, device=t.device)
     stream = _stream(dev)
-    with ctx.lock:
+    with _lib.acquire(dev) as ctx:
         _lib.check(_lib.lib().rk_window_hashes(ctx.handle, t.data_ptr(), n, m, start, stop,
                                                out.data_ptr(), stream))
     if on_host:

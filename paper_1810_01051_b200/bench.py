@@ -148,7 +148,6 @@ def time_device(text_dev, pattern: bytes, reps: int = 3) -> tuple[float, int]:
     nw = n - m + 1
     pat = np.frombuffer(pattern, dtype=np.uint8)
     hx = hash_full(pattern)
-    ctx = _lib.context(dev)
     L = _lib.lib()
     counts = torch.zeros(3, dtype=torch.int64, device=text_dev.device)
     cap = 1 << 16
@@ -156,7 +155,7 @@ def time_device(text_dev, pattern: bytes, reps: int = 3) -> tuple[float, int]:
     stream = torch.cuda.current_stream(dev)
 
     def launch():
-        with ctx.lock:
+        with _lib.acquire(dev) as ctx:
             _lib.check(L.rk_scan_async(ctx.handle, text_dev.data_ptr(), n, pat.ctypes.data, m,
                                        hx, 0, nw, out.data_ptr(), cap, 0, counts.data_ptr(),
                                        stream.cuda_stream))

@@ -15,15 +15,15 @@
 #include <vector>
 
 #include "../../include/rkb200.h"
-#include "rk_internal.h"
+#include "rk_ctx.h"
 
 using namespace rkb;
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
 
-int fail(int code, const char* fmt, ...) {
+int rkb::fail(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -33,29 +33,7 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
-#define RK_CUDA(call)                                                                   \
-  do {                                                                                  \
-    cudaError_t e_ = (call);                                                            \
-    if (e_ != cudaSuccess)                                                              \
-      return fail(RK_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
-                  __FILE__, __LINE__);                                                  \
-  } while (0)
-
-struct DeviceGuard {
-  int prev = -1;
-  bool ok = false;
-  explicit DeviceGuard(int dev) {
-    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    ok = cudaSetDevice(dev) == cudaSuccess;
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
-constexpr uint64_t kStageChunk = 64ull << 20;  // host staging granularity (multiple of kTile)
-constexpr int kRing = 3;                        // pinned staging slots for pageable texts
-constexpr uint64_t kRingSlot = 32ull << 20;     // bytes per pinned slot
+namespace rkb {
 
 // Persistent host threads for the pageable -> pinned staging copy (CPU-bound: one
 // thread moves ~10-14 GB/s, the DMA ~55 GB/s).
@@ -128,111 +106,9 @@ class CopyPool {
   uint64_t len_ = 0;
 };
 
-}  // namespace
+}  // namespace rkb
 
-// A pattern set's device layout (offsets into the context's blob) and its sweeps.
-struct MultiPlan {
-  struct Group {
-    uint32_t m, P, tsize;
-    uint64_t pats, phash, order, gidx, table, filter;
-    uint64_t tiny = 0;  // m < 7: cuckoo table of the packed patterns
-    TinyHash tiny_hash{};
-  };
-  struct Sweep {
-    std::vector<uint32_t> groups;  // ascending lengths
-    uint32_t qmode = 0, qwords = 0;
-    uint64_t qfilter = 0;  // blob offset of the sweep's q-gram filter (qmode > 0)
-    uint64_t qmap = 0;     // blob offset of its q-gram -> group-mask table
-    uint32_t qmap_size = 0;
-  };
-  std::vector<uint8_t> key;  // P, lengths, hashes, pattern bytes
-  std::vector<Group> groups;
-  std::vector<Sweep> sweeps;
-};
-constexpr uint64_t kMultiPrefix = 4096;  // pairs fetched with the count in one round trip
-
-struct rk_ctx {
-  int device = 0;
-  int num_sms = 0;
-  // Two alternating "sets" of {counters[4], block_sums[block_sums_cap]}: a scan uses
-  // the current set, and its emit kernel zeroes the other one for the next scan, so a
-  // scan is exactly two kernel launches (no memsets).  counters: [0] matches,
-  // [1] hash_hits, [2] collisions.
-  unsigned long long* d_sets = nullptr;
-  unsigned long long* d_counters = nullptr;  // counters of the current set
-  int cur_set = 0;
-  unsigned long long* d_mcount = nullptr;    // multi-pattern pair counter
-  unsigned long long* h_counters = nullptr;  // pinned mirror
-  uint32_t* d_tile_info = nullptr;  // per tile: matches | chunk bitmap << 16
-  uint64_t tile_info_cap = 0;
-  uint32_t* d_masks = nullptr;      // per tile: kTileChunks x 32 lane hit masks
-  uint64_t masks_cap = 0;
-  unsigned long long* d_block_sums = nullptr;  // block sums of the current set
-  uint64_t block_sums_cap = 0;
-  uint8_t* d_pattern = nullptr;  // pattern of the current scan (points into a cache slot)
-  struct PatSlot {
-    std::vector<uint8_t> bytes;
-    uint8_t* d = nullptr;
-    uint64_t cap = 0;
-    uint8_t* h = nullptr;  // pinned source of the slot's upload (rewritten after a sync only)
-    uint64_t hcap = 0;
-    uint64_t last_use = 0;
-  };
-  std::vector<PatSlot> pat_cache = std::vector<PatSlot>(64);
-  uint64_t pat_clock = 0;
-  uint64_t launches = 0;
-  // host staging
-  uint8_t* d_stage = nullptr;
-  uint64_t stage_cap = 0;
-  uint8_t* h_ring[kRing] = {};
-  CopyPool* copier = nullptr;  // created on the first pageable host scan
-  int64_t* d_out_stage = nullptr;
-  uint64_t out_stage_cap = 0;
-  uint64_t host_last = 0;  // offsets held in d_out_stage by the last rk_scan_host
-  cudaStream_t s_copy = nullptr, s_comp = nullptr;
-  cudaEvent_t ev_copied[kRing] = {};  // ring slot free again
-  cudaEvent_t ev_ready = nullptr;                 // bytes of the current chunk landed
-  // multi-pattern tables
-  uint8_t* d_sort = nullptr;   // scratch of the device pair sort
-  uint64_t sort_cap = 0;
-  uint8_t* d_mblob = nullptr;  // every length group's patterns, hashes and tables
-  uint64_t mblob_cap = 0;
-  uint8_t* h_mstage = nullptr;  // pinned staging of the blob
-  uint64_t h_mstage_cap = 0;
-  unsigned long long* h_mresult = nullptr;  // pinned: count, kMultiPrefix offsets, indices
-  MultiPlan mplan;              // the last pattern set's plan (cache key + layout)
-  // The scratch above is ordered on the stream of the call that used it.  When a call
-  // arrives on another stream, that stream first waits for everything queued so far on
-  // the previous one (an event recorded lazily at the switch: an event between two
-  // launches on one stream would cost their programmatic-dependent-launch overlap).
-  cudaStream_t last_stream = nullptr;
-  bool has_last = false;
-  cudaEvent_t ev_switch = nullptr;
-  // the last device scan's emission (rk_scan / rk_scan_async), for rk_scan_fetch
-  struct LastScan {
-    bool valid = false;
-    uint64_t tiles = 0, tile0 = 0;
-    int64_t start_bias = 0;
-  } last_scan;
-  std::mutex mu;
-};
-
-namespace {
-
-template <class T>
-int grow(T** p, uint64_t* cap, uint64_t need, bool zero, cudaStream_t s) {
-  if (*cap >= need && *p) return RK_OK;
-  if (*p) {
-    RK_CUDA(cudaStreamSynchronize(s));
-    RK_CUDA(cudaFree(*p));
-    *p = nullptr;
-  }
-  uint64_t c = std::max<uint64_t>(need, 64);
-  RK_CUDA(cudaMalloc((void**)p, c * sizeof(T)));
-  if (zero) RK_CUDA(cudaMemsetAsync(*p, 0, c * sizeof(T), s));
-  *cap = c;
-  return RK_OK;
-}
+namespace rkb {
 
 PatWords pack_pattern(const uint8_t* h, uint32_t m) {
   PatWords pw{};
@@ -446,7 +322,7 @@ int upload_pattern(rk_ctx* c, const uint8_t* h_pattern, uint32_t m, cudaStream_t
 
 int enqueue_scan(rk_ctx* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_pattern,
                  uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t* d_out,
-                 uint64_t cap, int64_t bias, cudaStream_t s, uint64_t* d_counts = nullptr) {
+                 uint64_t cap, int64_t bias, cudaStream_t s, uint64_t* d_counts) {
   c->last_scan.valid = false;
   if (stop <= start || hash_unreachable(m, hx)) return zero_result(c, d_counts, s);
   if (int r = upload_pattern(c, h_pattern, m, s)) return r;
@@ -455,6 +331,7 @@ int enqueue_scan(rk_ctx* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_
   if (int r = launch_one(c, d_text, n, m, hx, start, stop, 0, pack_pattern(h_pattern, m), s))
     return r;
   c->last_scan.valid = true;
+  c->last_scan.host = false;
   c->last_scan.tiles = g.num_tiles;
   c->last_scan.tile0 = g.tile_first;
   c->last_scan.start_bias = bias - (int64_t)g.amis - (int64_t)m + 1;
@@ -472,7 +349,105 @@ int read_counters(rk_ctx* c, uint64_t* matches, uint64_t* collisions, uint64_t* 
   return RK_OK;
 }
 
-}  // namespace
+// Re-runs the ordered emission of the context's last scan (device or staged host text)
+// into d_out with room for cap offsets: the scan's per-tile results and block sums are
+// still in the current counter set (nothing rescans).
+int emit_last(rk_ctx* c, int64_t* d_out, uint64_t cap, cudaStream_t s) {
+  if (!c->last_scan.valid) return fail(RK_EINVAL, "no scan to re-emit");
+  return emit(c, c->last_scan.tiles, c->last_scan.tile0, c->last_scan.start_bias, d_out, cap, s);
+}
+
+bool is_device_pointer(const void* p, int device) {
+  cudaPointerAttributes attr;
+  const bool dev = cudaPointerGetAttributes(&attr, p) == cudaSuccess &&
+                   (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) &&
+                   attr.device == device;
+  cudaGetLastError();
+  return dev;
+}
+
+// The staging pipeline of a HOST text (rk_scan_host, rk_scan_sharded): windows [start,
+// stop) of h_text (n bytes) are scanned as their bytes land in HBM.  The bytes [start,
+// stop + m - 1) go to c->d_stage in kStageChunk pieces by cudaMemcpyAsync on s_copy
+// (pinned text: straight from it; pageable: through the pinned ring, filled by the copy
+// threads), and the windows ending in each piece are scanned on s_comp as soon as it has
+// landed, while the next piece is in flight.  The ordered offsets (+ bias) go to
+// c->d_out_stage (first out_stage_cap of them; emit_last re-emits more), the counters
+// to c->d_counters (and d_counts if given).  Enqueued only: the caller holds c->mu, has
+// entered s_comp, and has sized d_out_stage.
+int host_scan_enqueue(rk_ctx* c, const uint8_t* h_text, uint64_t n, const uint8_t* h_pattern,
+                      uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t bias,
+                      uint64_t* d_counts) {
+  cudaStream_t sc = c->s_comp, sk = c->s_copy;
+  c->last_scan.valid = false;
+  if (stop <= start || hash_unreachable(m, hx)) return zero_result(c, d_counts, sc);
+  // bytes the windows need: [start, stop + m - 1)
+  const uint64_t b_lo = start, b_hi = stop + m - 1;
+  if (int r = grow(&c->d_stage, &c->stage_cap, n, false, sc)) return r;
+  if (int r = upload_pattern(c, h_pattern, m, sc)) return r;
+
+  cudaPointerAttributes attr;
+  const bool pinned = cudaPointerGetAttributes(&attr, h_text) == cudaSuccess &&
+                      attr.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (!pinned && !c->h_ring[0]) {
+    for (auto& h : c->h_ring) RK_CUDA(cudaMallocHost(&h, kRingSlot));
+    c->copier = new CopyPool();
+  }
+
+  // The staging buffer is cudaMalloc'ed (256-byte aligned), so a-space == text index.
+  const Geometry gall = geometry(c->d_stage, m, start, stop);
+  if (int r = begin_scan(c, gall.num_tiles, sc)) return r;
+  const PatWords pw = pack_pattern(h_pattern, m);
+
+  // chunk k covers end positions [k*C, (k+1)*C) and needs bytes < (k+1)*C; its copy on
+  // s_copy overlaps the scan of chunk k-1 on s_comp.
+  const uint64_t ja_lo = gall.ja_lo, ja_hi = gall.ja_hi;
+  const uint64_t k0 = ja_lo / kStageChunk, k1 = (ja_hi - 1) / kStageChunk;
+  uint64_t copied = b_lo;  // bytes [b_lo, copied) are enqueued
+  int slot = 0;
+  for (uint64_t k = k0; k <= k1; ++k) {
+    const uint64_t e_lo = std::max(ja_lo, k * kStageChunk);
+    const uint64_t e_hi = std::min(ja_hi, (k + 1) * kStageChunk);
+    const uint64_t need = std::min(b_hi, (k + 1) * kStageChunk);
+    if (need > copied) {
+      const uint64_t len = need - copied;
+      if (pinned) {
+        RK_CUDA(cudaMemcpyAsync(c->d_stage + copied, h_text + copied, len,
+                                cudaMemcpyHostToDevice, sk));
+      } else {
+        // pageable: multi-threaded CPU copy into a pinned ring slot, then DMA; a slot
+        // is reused only after the DMA issued from it kRing steps ago has finished
+        for (uint64_t off = 0; off < len; off += kRingSlot) {
+          const uint64_t l = std::min<uint64_t>(kRingSlot, len - off);
+          RK_CUDA(cudaEventSynchronize(c->ev_copied[slot]));
+          c->copier->copy(c->h_ring[slot], h_text + copied + off, l);
+          RK_CUDA(cudaMemcpyAsync(c->d_stage + copied + off, c->h_ring[slot], l,
+                                  cudaMemcpyHostToDevice, sk));
+          RK_CUDA(cudaEventRecord(c->ev_copied[slot], sk));
+          slot = (slot + 1) % kRing;
+        }
+      }
+      copied = need;
+      RK_CUDA(cudaEventRecord(c->ev_ready, sk));
+      RK_CUDA(cudaStreamWaitEvent(sc, c->ev_ready, 0));
+    }
+    const uint64_t ws = e_lo - (m - 1), we = e_hi - (m - 1);  // windows ending in the chunk
+    const Geometry gk = geometry(c->d_stage, m, ws, we);
+    if (int r = launch_one(c, c->d_stage, n, m, hx, ws, we, gk.tile_first - gall.tile_first, pw,
+                           sc))
+      return r;
+  }
+  c->last_scan.valid = true;
+  c->last_scan.host = true;
+  c->last_scan.tiles = gall.num_tiles;
+  c->last_scan.tile0 = gall.tile_first;
+  c->last_scan.start_bias = bias - (int64_t)m + 1;  // staging buffer: a-space == text index
+  return emit(c, gall.num_tiles, gall.tile_first, c->last_scan.start_bias, c->d_out_stage,
+              c->out_stage_cap, sc, d_counts);
+}
+
+}  // namespace rkb
 
 // Builds (or reuses) the device tables of a pattern set: every length group's patterns,
 // hashes, key table and filter, plus one q-gram filter per sweep, in one device blob.
@@ -857,86 +832,24 @@ int rk_scan_host(rk_ctx_t* c, const uint8_t* h_text, uint64_t n, const uint8_t* 
   if (int r = check_scan_args(h_text, n, h_pattern, m, start, stop, h_out, cap)) return r;
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
-  cudaStream_t sc = c->s_comp, sk = c->s_copy;
+  cudaStream_t sc = c->s_comp;
   if (int r = enter(c, sc)) return r;
   c->host_last = 0;
-  c->last_scan.valid = false;
   if (stop <= start || hash_unreachable(m, hx)) {
+    c->last_scan.valid = false;
     if (int r = zero_result(c, nullptr, sc)) return r;
     return read_counters(c, matches, collisions, hash_hits, sc);
   }
-  // bytes the windows need: [start, stop + m - 1)
-  const uint64_t b_lo = start, b_hi = stop + m - 1;
-  if (int r = grow(&c->d_stage, &c->stage_cap, n, false, sc)) return r;
   if (int r = grow(&c->d_out_stage, &c->out_stage_cap, std::max<uint64_t>(cap, 1ull << 16), false,
                    sc))
     return r;
-  if (int r = upload_pattern(c, h_pattern, m, sc)) return r;
-
-  cudaPointerAttributes attr;
-  const bool pinned = cudaPointerGetAttributes(&attr, h_text) == cudaSuccess &&
-                      attr.type == cudaMemoryTypeHost;
-  cudaGetLastError();
-  if (!pinned && !c->h_ring[0]) {
-    for (auto& h : c->h_ring) RK_CUDA(cudaMallocHost(&h, kRingSlot));
-    c->copier = new CopyPool();
-  }
-
-  // The staging buffer is cudaMalloc'ed (256-byte aligned), so a-space == text index.
-  const Geometry gall = geometry(c->d_stage, m, start, stop);
-  if (int r = begin_scan(c, gall.num_tiles, sc)) return r;
-  const PatWords pw = pack_pattern(h_pattern, m);
-  const uint64_t icap = c->out_stage_cap;
-
-  // chunk k covers end positions [k*C, (k+1)*C) and needs bytes < (k+1)*C; its copy on
-  // s_copy overlaps the scan of chunk k-1 on s_comp.
-  const uint64_t ja_lo = gall.ja_lo, ja_hi = gall.ja_hi;
-  const uint64_t k0 = ja_lo / kStageChunk, k1 = (ja_hi - 1) / kStageChunk;
-  uint64_t copied = b_lo;  // bytes [b_lo, copied) are enqueued
-  int slot = 0;
-  for (uint64_t k = k0; k <= k1; ++k) {
-    const uint64_t e_lo = std::max(ja_lo, k * kStageChunk);
-    const uint64_t e_hi = std::min(ja_hi, (k + 1) * kStageChunk);
-    const uint64_t need = std::min(b_hi, (k + 1) * kStageChunk);
-    if (need > copied) {
-      const uint64_t len = need - copied;
-      if (pinned) {
-        RK_CUDA(cudaMemcpyAsync(c->d_stage + copied, h_text + copied, len,
-                                cudaMemcpyHostToDevice, sk));
-      } else {
-        // pageable: multi-threaded CPU copy into a pinned ring slot, then DMA; a slot
-        // is reused only after the DMA issued from it kRing steps ago has finished
-        for (uint64_t off = 0; off < len; off += kRingSlot) {
-          const uint64_t l = std::min<uint64_t>(kRingSlot, len - off);
-          RK_CUDA(cudaEventSynchronize(c->ev_copied[slot]));
-          c->copier->copy(c->h_ring[slot], h_text + copied + off, l);
-          RK_CUDA(cudaMemcpyAsync(c->d_stage + copied + off, c->h_ring[slot], l,
-                                  cudaMemcpyHostToDevice, sk));
-          RK_CUDA(cudaEventRecord(c->ev_copied[slot], sk));
-          slot = (slot + 1) % kRing;
-        }
-      }
-      copied = need;
-      RK_CUDA(cudaEventRecord(c->ev_ready, sk));
-      RK_CUDA(cudaStreamWaitEvent(sc, c->ev_ready, 0));
-    }
-    const uint64_t ws = e_lo - (m - 1), we = e_hi - (m - 1);  // windows ending in the chunk
-    const Geometry gk = geometry(c->d_stage, m, ws, we);
-    if (int r = launch_one(c, c->d_stage, n, m, hx, ws, we, gk.tile_first - gall.tile_first, pw,
-                           sc))
-      return r;
-  }
-  const int64_t start_bias = -(int64_t)m + 1;  // staging buffer: a-space == text index
-  if (int r = emit(c, gall.num_tiles, gall.tile_first, start_bias, c->d_out_stage, icap, sc))
-    return r;
+  if (int r = host_scan_enqueue(c, h_text, n, h_pattern, m, hx, start, stop, 0, nullptr)) return r;
   uint64_t mt = 0, co = 0, hh = 0;
   if (int r = read_counters(c, &mt, &co, &hh, sc)) return r;
-  if (mt > icap) {
+  if (mt > c->out_stage_cap) {
     // more offsets than the staging output held: re-emit from the kept masks (no rescan)
     if (int r = grow(&c->d_out_stage, &c->out_stage_cap, mt, false, sc)) return r;
-    if (int r = emit(c, gall.num_tiles, gall.tile_first, start_bias, c->d_out_stage, mt, sc))
-      return r;
-    if (int r = read_counters(c, &mt, nullptr, nullptr, sc)) return r;
+    if (int r = emit_last(c, c->d_out_stage, mt, sc)) return r;
   }
   c->host_last = mt;
   const uint64_t nout = std::min(mt, cap);
@@ -972,15 +885,13 @@ int rk_scan_fetch(rk_ctx_t* c, int64_t* d_out, uint64_t cap, void* stream) {
   if (!c) return fail(RK_EINVAL, "context is NULL");
   if (cap && !d_out) return fail(RK_EINVAL, "output pointer is NULL with cap > 0");
   std::lock_guard<std::mutex> lk(c->mu);
-  if (!c->last_scan.valid)
+  if (!c->last_scan.valid || c->last_scan.host)
     return fail(RK_EINVAL, "rk_scan_fetch: the context's last call was not a device scan "
                 "with matches to re-emit");
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   if (int r = enter(c, s)) return r;
-  // the scan's per-tile results and block sums are still in the current counter set: the
-  // emit alone writes the ordered offsets again, now with room for cap of them
-  return emit(c, c->last_scan.tiles, c->last_scan.tile0, c->last_scan.start_bias, d_out, cap, s);
+  return emit_last(c, d_out, cap, s);
 }
 
 int rk_window_hashes(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, uint32_t m, uint64_t start,

@@ -1,0 +1,321 @@
+// rk_comm.cu -- the multi-GPU data plane behind the C ABI: NCCL communicators and the
+// sharded scan (include/rkb200.h, "Multi-GPU").
+//
+// The reference splits the window range into contiguous ranges, scans them independently
+// and concatenates the per-range lists in range order
+// (/root/reference/pkg/src/rkmatch/parallel.py:155-172).  Here a range is a GPU (one
+// process per GPU): each rank scans its shard -- its windows plus the (m-1)-byte halo
+// their last bytes need -- with no traffic during the scan, and the one exchange is the
+// final gather, an allgather-v over NVLink/NVSwitch:
+//   1. ncclAllGather of every rank's {matches, hash_hits, collisions} (32 bytes per rank);
+//   2. one grouped ncclBroadcast per rank with matches, rooted at that rank, whose receive
+//      buffer on every rank is the output at the rank's prefix offset -- the positions
+//      land in place, already globally ascending (rank order = range order), with no
+//      padding to the largest count and no copy after the collective.
+// NCCL is loaded at run time (dlopen of libnccl.so.2, i.e. the one torch already mapped
+// when it is loaded), so the library still loads where NCCL is absent and only the
+// rk_comm_* entry points report RK_ENCCL there.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "rk_ctx.h"
+
+using namespace rkb;
+
+namespace {
+
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  int version = 0;
+  ncclResult_t (*GetVersion)(int*) = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* path = getenv("RKB200_NCCL_LIB");
+    void* h = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      api.err = std::string("cannot load NCCL: ") + dlerror();
+      return;
+    }
+    bool all = true;
+    auto sym = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      all = all && fn != nullptr;
+    };
+    sym(api.GetVersion, "ncclGetVersion");
+    sym(api.GetUniqueId, "ncclGetUniqueId");
+    sym(api.CommInitRank, "ncclCommInitRank");
+    sym(api.CommDestroy, "ncclCommDestroy");
+    sym(api.CommAbort, "ncclCommAbort");
+    sym(api.AllGather, "ncclAllGather");
+    sym(api.Broadcast, "ncclBroadcast");
+    sym(api.GroupStart, "ncclGroupStart");
+    sym(api.GroupEnd, "ncclGroupEnd");
+    sym(api.GetErrorString, "ncclGetErrorString");
+    if (!all) {
+      api.err = "NCCL library lacks a required symbol";
+      return;
+    }
+    api.GetVersion(&api.version);
+    api.ok = true;
+  });
+  return api;
+}
+
+#define RK_NCCL(call)                                                                       \
+  do {                                                                                      \
+    ncclResult_t r_ = (call);                                                               \
+    if (r_ != ncclSuccess)                                                                  \
+      return fail(RK_ENCCL, "%s failed: %s (%s:%d)", #call, nccl().GetErrorString(r_),      \
+                  __FILE__, __LINE__);                                                      \
+  } while (0)
+
+}  // namespace
+
+struct rk_comm {
+  rk_ctx* ctx = nullptr;
+  ncclComm_t comm = nullptr;
+  int nranks = 0, rank = 0;
+  unsigned long long* d_cnt = nullptr;     // this rank's {matches, hash_hits, collisions, 0}
+  unsigned long long* d_allcnt = nullptr;  // every rank's, rank-major
+  unsigned long long* h_allcnt = nullptr;  // pinned mirror
+  int64_t* d_local = nullptr;              // this rank's ordered offsets (device texts)
+  uint64_t local_cap = 0;
+  int64_t* d_gather = nullptr;             // whole gathered list when the caller's cap < total
+  uint64_t gather_cap = 0;
+  uint64_t gathered = 0;                   // offsets of the last sharded scan in d_gather
+};
+
+extern "C" {
+
+int rk_comm_get_unique_id(uint8_t* id) {
+  if (!id) return fail(RK_EINVAL, "id is NULL");
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(RK_ENCCL, "%s", api.err.c_str());
+  ncclUniqueId u;
+  RK_NCCL(api.GetUniqueId(&u));
+  static_assert(sizeof(u) == RK_COMM_ID_BYTES, "NCCL unique id size");
+  memcpy(id, &u, sizeof u);
+  return RK_OK;
+}
+
+int rk_comm_init(rk_ctx_t* c, const uint8_t* id, int nranks, int rank, rk_comm_t** out) {
+  if (!out) return fail(RK_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!c || !id) return fail(RK_EINVAL, "context or id is NULL");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(RK_EINVAL, "rank %d outside [0, %d)", rank, nranks);
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(RK_ENCCL, "%s", api.err.c_str());
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  rk_comm* k = new rk_comm();
+  k->ctx = c;
+  k->nranks = nranks;
+  k->rank = rank;
+  ncclUniqueId u;
+  memcpy(&u, id, sizeof u);
+  ncclResult_t r = api.CommInitRank(&k->comm, nranks, u, rank);
+  if (r != ncclSuccess) {
+    delete k;
+    return fail(RK_ENCCL, "ncclCommInitRank(rank %d of %d) failed: %s", rank, nranks,
+                api.GetErrorString(r));
+  }
+  cudaError_t e = cudaMalloc(&k->d_cnt, 4 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&k->d_allcnt, 4ull * nranks * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMallocHost(&k->h_allcnt, 4ull * nranks * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(k->d_cnt, 0, 4 * sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    api.CommDestroy(k->comm);
+    cudaFree(k->d_cnt);
+    cudaFree(k->d_allcnt);
+    delete k;
+    return fail(RK_ECUDA, "comm scratch: %s", cudaGetErrorString(e));
+  }
+  const char* log = getenv("RKB200_COMM_LOG");
+  if (log && *log && *log != '0')
+    fprintf(stderr, "[rkb200] comm rank %d/%d on device %d, NCCL %d\n", rank, nranks, c->device,
+            api.version);
+  *out = k;
+  return RK_OK;
+}
+
+int rk_comm_destroy(rk_comm_t* k) {
+  if (!k) return RK_OK;
+  DeviceGuard g(k->ctx->device);
+  cudaDeviceSynchronize();
+  if (k->comm) nccl().CommDestroy(k->comm);
+  cudaFree(k->d_cnt);
+  cudaFree(k->d_allcnt);
+  cudaFreeHost(k->h_allcnt);
+  cudaFree(k->d_local);
+  cudaFree(k->d_gather);
+  delete k;
+  return RK_OK;
+}
+
+int rk_comm_info(rk_comm_t* k, int* nranks, int* rank, int* nccl_version) {
+  if (!k) return fail(RK_EINVAL, "communicator is NULL");
+  if (nranks) *nranks = k->nranks;
+  if (rank) *rank = k->rank;
+  if (nccl_version) *nccl_version = nccl().version;
+  return RK_OK;
+}
+
+int rk_shard_range(uint64_t n, uint32_t m, int nranks, int rank, uint64_t* win_lo,
+                   uint64_t* win_hi, uint64_t* byte_lo, uint64_t* byte_hi) {
+  if (m < 1) return fail(RK_EINVAL, "pattern must be non-empty");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(RK_EINVAL, "rank %d outside [0, %d)", rank, nranks);
+  // parallel.py:155-161: ceil(W / G) windows per range, capped at W
+  const uint64_t W = n >= m ? n - m + 1 : 0;
+  const uint64_t chunk = (W + (uint64_t)nranks - 1) / (uint64_t)nranks;
+  const uint64_t a = std::min<uint64_t>((uint64_t)rank * chunk, W);
+  const uint64_t b = std::min<uint64_t>(a + chunk, W);
+  if (win_lo) *win_lo = a;
+  if (win_hi) *win_hi = b;
+  if (byte_lo) *byte_lo = a;
+  if (byte_hi) *byte_hi = b > a ? std::min<uint64_t>(b + m - 1, n) : a;
+  return RK_OK;
+}
+
+int rk_scan_sharded(rk_comm_t* k, const uint8_t* text, uint64_t len, uint64_t byte_lo,
+                    const uint8_t* h_pattern, uint32_t m, uint64_t hx, uint64_t win_lo,
+                    uint64_t win_hi, int64_t* d_out, uint64_t cap, uint64_t* matches,
+                    uint64_t* collisions, uint64_t* hash_hits, void* stream) {
+  if (!k) return fail(RK_EINVAL, "communicator is NULL");
+  if (!h_pattern || m < 1) return fail(RK_EINVAL, "pattern must be non-empty");
+  if (win_hi > win_lo) {
+    if (win_lo < byte_lo || win_hi - byte_lo + m - 1 > len)
+      return fail(RK_EINVAL, "windows [%llu, %llu) of length %u need bytes the shard [%llu, "
+                  "%llu) does not hold", (unsigned long long)win_lo,
+                  (unsigned long long)win_hi, m, (unsigned long long)byte_lo,
+                  (unsigned long long)(byte_lo + len));
+    if (!text) return fail(RK_EINVAL, "text pointer is NULL");
+  }
+  if (cap && !d_out) return fail(RK_EINVAL, "output pointer is NULL with cap > 0");
+  rk_ctx* c = k->ctx;
+  NcclApi& api = nccl();
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t start = win_hi > win_lo ? win_lo - byte_lo : 0;
+  const uint64_t stop = win_hi > win_lo ? win_hi - byte_lo : 0;
+  const bool on_device = stop > start && is_device_pointer(text, c->device);
+
+  // 1. the local scan: ordered offsets (biased to global positions) + counters in d_cnt
+  int64_t** local = &k->d_local;
+  uint64_t* local_cap = &k->local_cap;
+  if (stop > start && !on_device) {
+    // host shard: staged into HBM chunk by chunk on the context's streams
+    if (int r = enter(c, c->s_comp)) return r;
+    if (int r = grow(&c->d_out_stage, &c->out_stage_cap, 1ull << 16, false, c->s_comp)) return r;
+    if (int r = host_scan_enqueue(c, text, len, h_pattern, m, hx, start, stop, (int64_t)byte_lo,
+                                  (uint64_t*)k->d_cnt))
+      return r;
+    local = &c->d_out_stage;
+    local_cap = &c->out_stage_cap;
+    if (int r = enter(c, s)) return r;  // s waits for the staged scan
+  } else {
+    if (int r = enter(c, s)) return r;
+    if (int r = grow(&k->d_local, &k->local_cap, 1ull << 16, false, s)) return r;
+    if (int r = enqueue_scan(c, text, len, h_pattern, m, hx, start, stop, k->d_local,
+                             k->local_cap, (int64_t)byte_lo, s, (uint64_t*)k->d_cnt))
+      return r;
+  }
+
+  // 2. every rank's counters (32 bytes per rank) to every rank
+  RK_NCCL(api.AllGather(k->d_cnt, k->d_allcnt, 4, ncclUint64, k->comm, s));
+  RK_CUDA(cudaMemcpyAsync(k->h_allcnt, k->d_allcnt, 4ull * k->nranks * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, s));
+  RK_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint64_t> cnt(k->nranks), prefix(k->nranks + 1, 0);
+  uint64_t hits = 0, coll = 0;
+  for (int r = 0; r < k->nranks; ++r) {
+    cnt[r] = k->h_allcnt[4 * r];
+    hits += k->h_allcnt[4 * r + 1];
+    coll += k->h_allcnt[4 * r + 2];
+    prefix[r + 1] = prefix[r] + cnt[r];
+  }
+  const uint64_t total = prefix[k->nranks];
+  const uint64_t mine = cnt[k->rank];
+  if (mine > *local_cap) {
+    // more local matches than the first emission held: re-emit from the kept per-tile
+    // results (never a rescan)
+    if (int r = grow(local, local_cap, mine, false, s)) return r;
+    if (int r = emit_last(c, *local, mine, s)) return r;
+  }
+
+  // 3. allgather-v: rank r's list broadcast from r into every rank's output at prefix[r]
+  k->gathered = 0;
+  if (total) {
+    int64_t* recv = d_out;
+    if (cap < total) {
+      if (int r = grow(&k->d_gather, &k->gather_cap, total, false, s)) return r;
+      recv = k->d_gather;
+    }
+    RK_NCCL(api.GroupStart());
+    for (int r = 0; r < k->nranks; ++r) {
+      if (!cnt[r]) continue;
+      const void* send = r == k->rank ? (const void*)*local : (const void*)(recv + prefix[r]);
+      ncclResult_t e = api.Broadcast(send, recv + prefix[r], cnt[r], ncclInt64, r, k->comm, s);
+      if (e != ncclSuccess) {
+        api.GroupEnd();
+        return fail(RK_ENCCL, "ncclBroadcast(root %d) failed: %s", r, api.GetErrorString(e));
+      }
+    }
+    RK_NCCL(api.GroupEnd());
+    if (recv != d_out) {
+      k->gathered = total;
+      if (cap)
+        RK_CUDA(cudaMemcpyAsync(d_out, recv, cap * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  if (matches) *matches = total;
+  if (hash_hits) *hash_hits = hits;
+  if (collisions) *collisions = coll;
+  return RK_OK;
+}
+
+int rk_comm_fetch(rk_comm_t* k, int64_t* d_out, uint64_t first, uint64_t count, void* stream) {
+  if (!k) return fail(RK_EINVAL, "communicator is NULL");
+  std::lock_guard<std::mutex> lk(k->ctx->mu);
+  if (first > k->gathered || count > k->gathered - first)
+    return fail(RK_EINVAL, "fetch [%llu, %llu) beyond the %llu offsets kept from the last "
+                "sharded scan", (unsigned long long)first, (unsigned long long)(first + count),
+                (unsigned long long)k->gathered);
+  if (!count) return RK_OK;
+  if (!d_out) return fail(RK_EINVAL, "NULL output");
+  DeviceGuard g(k->ctx->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int r = enter(k->ctx, s)) return r;
+  RK_CUDA(cudaMemcpyAsync(d_out, k->d_gather + first, count * sizeof(int64_t),
+                          cudaMemcpyDeviceToDevice, s));
+  return RK_OK;
+}
+
+}  // extern "C"

@@ -66,10 +66,9 @@ def generate_into(out, spec: DnaSpec, skip: int = 0, stream=None) -> None:
     import torch
 
     dev = out.device.index if out.device.index is not None else torch.cuda.current_device()
-    ctx = _lib.context(dev)
     alpha = np.frombuffer(spec.alphabet, dtype=np.uint8)
     s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
-    with ctx.lock:
+    with _lib.acquire(dev) as ctx:
         _lib.check(_lib.lib().rk_generate(ctx.handle, out.data_ptr(), int(out.numel()),
                                           spec.seed & MASK64, skip, alpha.ctypes.data,
                                           len(spec.alphabet), s))

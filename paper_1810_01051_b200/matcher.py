@@ -154,14 +154,13 @@ def multi_scan(t_dev, dev: int, pats: list[bytes]):
     flat = np.frombuffer(b"".join(pats), dtype=np.uint8)
     lengths = np.array([len(p) for p in pats], dtype=np.uint32)
     hashes = np.array([hash_full(p) for p in pats], dtype=np.uint64)
-    ctx = _lib.context(dev)
     stream = _scan._stream(dev)
     cap = 1 << 16
     pairs = _lib.u64ref()
     for _attempt in range(2):
         off = torch.empty(cap, dtype=torch.int64, device=t_dev.device)
         idx = torch.empty(cap, dtype=torch.int32, device=t_dev.device)
-        with ctx.lock:
+        with _lib.acquire(dev) as ctx:
             _lib.check(L.rk_multi_scan_mixed(ctx.handle, t_dev.data_ptr(), n, flat.ctypes.data,
                                              lengths.ctypes.data, P, hashes.ctypes.data,
                                              off.data_ptr(), idx.data_ptr(), cap,

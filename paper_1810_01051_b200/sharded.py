@@ -7,15 +7,27 @@ The same partition becomes the GPU shard map:
 * rank r owns windows [a_r, b_r) and holds text bytes [a_r, b_r + m - 1) -- its shard
   plus an (m-1)-byte halo (the hash needs min(m,32)-1 of them, verification m-1);
 * each rank scans its shard with no inter-GPU traffic;
-* the only exchange is the final gather: per-rank counts, then the positions padded to
-  the largest count, with NCCL all_gather over NVLink; concatenating in rank order is
-  already the globally ascending list.
+* the only exchange is the final gather: per-rank counts, then every rank's positions
+  over NVLink; concatenating in rank order is already the globally ascending list.
 
-The functions take a ``torch.distributed`` process group, so the host logic is tested
-with ``gloo`` on CPU (tests/test_sharded.py) and runs with ``nccl`` on B200s.
+Two layers:
+
+* ``Communicator`` -- the data plane behind the C ABI (rk_comm_init / rk_scan_sharded in
+  librkb200.so, NCCL called from C++): each rank scans its shard (device tensor, or host
+  memory staged chunk by chunk), then the counters are all-gathered and every rank's
+  ordered positions are broadcast into every rank's output at its prefix -- an exact
+  allgather-v, whatever the match density.  ``torch.distributed`` only ships the 128-byte
+  NCCL unique id at setup.
+* the ``torch.distributed`` helpers below (``search_sharded``, ``gather_offsets``, the
+  multi-pattern gather), which take a process group, so the partition / halo / ordering
+  logic is tested with ``gloo`` on CPU (tests/test_sharded.py).
 """
 
 from __future__ import annotations
+
+import ctypes
+
+from . import _lib
 
 
 def weak_shard(rank: int, per_rank: int, n_total: int, m: int) -> tuple[int, int, int, int]:
@@ -47,7 +59,7 @@ def gather_offsets(local, group=None):
     k = torch.tensor([local.numel()], dtype=torch.int64, device=dev)
     counts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(counts, k, group=group)
-    counts = [int(c.item()) for c in counts]
+    counts = [int(c) for c in torch.cat(counts).tolist()]  # one host round trip
     kmax = max(counts)
     if kmax == 0:
         return torch.empty(0, dtype=torch.int64, device=dev), counts
@@ -164,3 +176,122 @@ def search_multi_sharded(shard, patterns, start_lo: int, start_hi: int, byte_lo:
     idx = torch.cat(idx_parts) if idx_parts else torch.empty(0, dtype=torch.int32)
     off = torch.cat(off_parts) if off_parts else torch.empty(0, dtype=torch.int64)
     return gather_pairs(idx.to(dev), off.to(dev), group)
+
+
+def shard_range(n_total: int, m: int, world: int, rank: int) -> tuple[int, int, int, int]:
+    """rk_shard_range (the C ABI's strong partition, parallel.py:155-161): (win_lo, win_hi,
+    byte_lo, byte_hi) of ``rank``; equal to strong_shard."""
+    v = [_lib.u64ref() for _ in range(4)]
+    _lib.check(_lib.lib().rk_shard_range(n_total, m, world, rank, *(ctypes.byref(x) for x in v)))
+    return tuple(int(x.value) for x in v)
+
+
+class Communicator:
+    """This rank's NCCL communicator behind the C ABI (rk_comm_init).
+
+    Collective: every rank of ``group`` (default: the default process group; none
+    initialised = a single rank) constructs one.  Rank 0 draws the NCCL unique id
+    (rk_comm_get_unique_id) and torch.distributed broadcasts those 128 bytes; nothing
+    else goes through torch.distributed."""
+
+    def __init__(self, group=None, device: int | None = None):
+        import torch
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            self.rank = dist.get_rank(group)
+            self.world = dist.get_world_size(group)
+        else:
+            self.rank, self.world = 0, 1
+        self.device = _lib.default_device() if device is None else device
+        torch.cuda.set_device(self.device)
+        L = _lib.lib()
+        uid = (ctypes.c_uint8 * _lib.COMM_ID_BYTES)()
+        if self.rank == 0:
+            _lib.check(L.rk_comm_get_unique_id(uid))
+        if self.world > 1:
+            box = [bytes(uid) if self.rank == 0 else None]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(box, src=src, group=group)
+            uid = (ctypes.c_uint8 * _lib.COMM_ID_BYTES).from_buffer_copy(box[0])
+        # a context of its own: the sharded scans' scratch never interleaves with other
+        # callers' scans on the device's shared context
+        self.ctx = _lib.Context(self.device)
+        h = ctypes.c_void_p()
+        _lib.check(L.rk_comm_init(self.ctx.handle, uid, self.world, self.rank, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self) -> None:
+        if self.handle:
+            _lib.lib().rk_comm_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+            self.ctx.close()
+
+    def info(self) -> dict:
+        n, r, v = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _lib.check(_lib.lib().rk_comm_info(self.handle, ctypes.byref(n), ctypes.byref(r),
+                                           ctypes.byref(v)))
+        return {"nranks": n.value, "rank": r.value, "nccl_version": v.value}
+
+    def scan(self, text, pattern, win_lo: int, win_hi: int, byte_lo: int, *,
+             cap: int = 1 << 16, out=None, stream=None):
+        """rk_scan_sharded: this rank's windows [win_lo, win_hi) of the global text, whose
+        bytes [byte_lo, byte_lo + len(text)) it holds (CUDA tensor on this device, or host
+        bytes / ndarray / pinned tensor).  Returns (global offsets as a CUDA int64 tensor,
+        matches, collisions, hash_hits), totals over all ranks, on every rank."""
+        import numpy as np
+        import torch
+
+        from . import _scan
+        from .rkhash import hash_full
+
+        L = _lib.lib()
+        p = _scan._host_bytes(pattern)
+        m = int(p.size)
+        if m == 0:
+            raise ValueError("empty pattern")
+        t = _scan.as_u8(text)
+        if isinstance(t, torch.Tensor) and not t.is_cuda:
+            t = t.numpy()
+        n = _scan._size(t)
+        ptr = (t.data_ptr() if isinstance(t, torch.Tensor) else _scan._ptr(np.asarray(t))) if n else 0
+        s = _scan._stream(self.device) if stream is None else stream
+        if out is None:
+            out = torch.empty(max(cap, 1), dtype=torch.int64, device=f"cuda:{self.device}")
+        cap = min(cap, int(out.numel()))
+        mt, co, hh = _lib.u64ref(), _lib.u64ref(), _lib.u64ref()
+        with self.ctx.lock:
+            _lib.check(L.rk_scan_sharded(self.handle, ptr, n, byte_lo, _scan._ptr(p), m,
+                                         hash_full(p.tobytes()), win_lo, win_hi, out.data_ptr(),
+                                         cap, ctypes.byref(mt), ctypes.byref(co),
+                                         ctypes.byref(hh), s))
+            k = int(mt.value)
+            if k > cap:
+                full = torch.empty(k, dtype=torch.int64, device=out.device)
+                _lib.check(L.rk_comm_fetch(self.handle, full.data_ptr(), 0, k, s))
+                out = full
+        return out[:k], k, int(co.value), int(hh.value)
+
+    def search(self, shard, pattern, n_total: int, stats=None):
+        """search_parallel's result over a text sharded across the ranks (strong partition,
+        rk_shard_range): ``shard`` is this rank's bytes [byte_lo, byte_hi) -- or the whole
+        text, which is then sliced.  Returns the global MatchResult on every rank."""
+        from . import _scan
+        from .matcher import MatchResult
+
+        p = _scan._host_bytes(pattern)
+        m = int(p.size)
+        if m == 0:
+            raise ValueError("empty pattern")
+        if m > n_total:
+            return MatchResult(n_total, m, [])
+        a, b, blo, bhi = shard_range(n_total, m, self.world, self.rank)
+        t = _scan.as_u8(shard)
+        if _scan._size(t) == n_total and (blo, bhi) != (0, n_total):
+            t = t[blo:bhi]
+        offs, k, coll, hits = self.scan(t, p, a, b, blo)
+        if stats is not None:
+            stats.windows += n_total - m + 1
+            stats.hash_hits += hits
+            stats.collisions += coll
+        return MatchResult(n_total, m, offs.cpu().tolist())

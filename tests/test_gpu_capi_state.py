@@ -128,3 +128,40 @@ def test_scans_on_alternating_streams(gpu):
         k = int(c[i, 0])
         assert k == len(exp) and int(c[i, 2]) == ecoll and int(c[i, 1]) == k + ecoll, i
         assert o[i, : min(k, cap)].tolist() == exp[:cap].tolist(), i
+
+
+def test_concurrent_callers_get_their_own_contexts(gpu):
+    """The reference runs range scans concurrently on a thread pool
+    (parallel.py:111-121, :162-167).  Concurrent Python callers here each hold their own
+    context (_lib.acquire: the primary one if free, else a pooled spare), so host-text
+    and device-text scans from 6 threads run side by side and all stay exact."""
+    import threading
+
+    import oracle
+
+    torch = _torch()
+    rng = np.random.default_rng(31)
+    texts = [rng.integers(0, 4, (1 << 20) + 977 * i, dtype=np.uint8) for i in range(6)]
+    pats = [t[4000:4000 + m].tobytes() for t, m in zip(texts, (4, 8, 13, 32, 64, 200))]
+    expect = [oracle.c_scan(t, np.frombuffer(p, np.uint8)) for t, p in zip(texts, pats)]
+    errors = []
+
+    def work(i):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for rep in range(20):
+                    src = texts[i] if rep % 2 else torch.from_numpy(texts[i]).cuda()
+                    st = rk.ScanStats()
+                    r = rk.search_sequential(src, pats[i], stats=st)
+                    assert r.offsets == expect[i][0].tolist() and st.collisions == expect[i][1]
+        except Exception as e:  # noqa: BLE001
+            errors.append((i, repr(e)))
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(6)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors

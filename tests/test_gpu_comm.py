@@ -1,0 +1,120 @@
+"""The multi-GPU data plane behind the C ABI (rk_comm_init / rk_scan_sharded / rk_comm_fetch,
+NCCL called from librkb200) on the one GPU of the test box: a single-rank communicator,
+so every collective is real NCCL but no rank waits on another GPU.  The partition and the
+rank-order merge across several ranks are covered by tests/test_sharded.py (gloo) and by
+tests/test_gpu_fullsize.py::test_c4_16gib_shard_map (every shard's scan on this GPU)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1810_01051_b200 as rk
+from paper_1810_01051_b200 import _scan, sharded
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def comm(gpu):
+    c = sharded.Communicator(device=0)
+    yield c
+    c.close()
+
+
+def test_comm_info(comm):
+    info = comm.info()
+    assert info["nranks"] == 1 and info["rank"] == 0 and info["nccl_version"] >= 21000
+
+
+def test_sharded_scan_device_text(comm):
+    import torch
+
+    spec = rk.DnaSpec(42, 64 << 20)
+    t = rk.generate_tensor(spec)
+    pat = rk.datagen.make_pattern(t, spec, 12, "sampled")
+    n, m = t.numel(), len(pat)
+    offs, k, coll, hits = comm.scan(t, pat, 0, n - m + 1, 0)
+    eo, ec = oracle.c_scan_mt(t.cpu().numpy(), pat)
+    assert offs.cpu().numpy().tolist() == eo.tolist() and coll == ec and hits == k + coll
+    # a window range inside a shard held from byte 1000 on (global offsets come back)
+    a, b = 5000, (40 << 20)
+    shard = t[1000: b + m - 1]
+    offs2, k2, coll2, _ = comm.scan(shard, pat, a, b, 1000)
+    sel = eo[(eo >= a) & (eo < b)]
+    assert offs2.cpu().numpy().tolist() == sel.tolist()
+
+
+def test_sharded_scan_host_text_and_fetch(comm):
+    """A host shard is staged into HBM chunk by chunk; more matches than cap: the rest is
+    fetched from the kept gather (no rescan)."""
+    import torch
+
+    n = 48 << 20
+    host = np.full(n, 97, dtype=np.uint8)
+    host[::1000] = 98
+    offs, k, coll, hits = comm.scan(host, b"aaaa", 0, n - 3, 0, cap=1000)
+    eo, ec = oracle.c_scan_mt(host, b"aaaa")
+    assert k == eo.size and coll == ec == 0 and hits == k
+    assert torch.equal(offs.cpu(), torch.from_numpy(eo))
+    pinned = torch.from_numpy(host).pin_memory()
+    offs, k, _, _ = comm.scan(pinned, b"aab", 0, n - 2, 0)
+    assert offs.cpu().numpy().tolist() == oracle.c_scan_mt(host, b"aab")[0].tolist()
+
+
+def test_sharded_dense_all_a(comm):
+    """C5 density through the exact allgather-v: 256 MiB of 'a', every window matches."""
+    import torch
+
+    n = 1 << 28
+    t = torch.full((n,), 97, dtype=torch.uint8, device="cuda")
+    offs, k, coll, hits = comm.scan(t, b"aaaa", 0, n - 3, 0, cap=n)
+    assert k == n - 3 and coll == 0
+    assert torch.equal(offs, torch.arange(n - 3, device="cuda"))
+
+
+def test_sharded_edge_cases(comm):
+    import torch
+
+    t = torch.frombuffer(bytearray(b"acXba" * 10), dtype=torch.uint8).cuda()
+    offs, k, coll, hits = comm.scan(t, b"ac", 0, t.numel() - 1, 0)
+    assert offs.cpu().tolist() == list(range(0, 50, 5)) and coll == 10 and hits == 20
+    offs, k, coll, hits = comm.scan(t, b"ac", 3, 3, 0)  # this rank owns no windows
+    assert k == coll == hits == 0
+    with pytest.raises(ValueError):
+        comm.scan(t[10:], b"ac", 0, 30, 10)  # windows before the held bytes
+    with pytest.raises(ValueError):
+        comm.scan(t, b"ac", 0, t.numel(), 0)  # last window runs past the held bytes
+
+
+def test_search_matches_search_sequential(comm):
+    text = rk.generate(rk.DnaSpec(7, 1 << 20))
+    for pat in (text[100:108], text[5000:5040], b"ACGTACGTAC"):
+        st = rk.ScanStats()
+        r = comm.search(text, pat, len(text), stats=st)
+        st2 = rk.ScanStats()
+        assert r == rk.search_sequential(text, pat, stats=st2)
+        assert (st.windows, st.hash_hits, st.collisions) == \
+            (st2.windows, st2.hash_hits, st2.collisions)
+
+
+def test_communicator_over_torch_distributed(gpu):
+    """The unique id shipped through a torch.distributed group (NCCL backend, 1 rank)."""
+    import torch.distributed as dist
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        c = sharded.Communicator()
+        text = rk.generate(rk.DnaSpec(3, 1 << 16))
+        assert c.search(text, text[77:90], len(text)) == rk.search_naive(text, text[77:90])
+        c.close()
+    finally:
+        dist.destroy_process_group()

@@ -194,3 +194,69 @@ def test_sharded_multi_gpu_single_rank(gpu):
             assert off[idx == j].cpu().tolist() == exp
     finally:
         dist.destroy_process_group()
+
+
+def test_c_abi_shard_range_is_the_strong_partition():
+    """rk_shard_range (C ABI, no GPU needed) == strong_shard (the partition of
+    parallel.py:155-161) for every rank, including empty tails and m > n."""
+    for n in (0, 1, 5, 31, 1000, 4097, 16 << 30):
+        for m in (1, 3, 32, 1024):
+            for world in (1, 2, 3, 4, 8):
+                for r in range(world):
+                    assert sharded.shard_range(n, m, world, r) == \
+                        sharded.strong_shard(r, world, n, m), (n, m, world, r)
+
+
+def _c4_worker(rank, world, port, seed, n, m, plants, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, b, blo, bhi = sharded.shard_range(n, m, world, rank)
+        # the rank builds ONLY its bytes [blo, bhi): corpus slice + the planted copies
+        # that intersect it (a copy straddling the cut lands half in each shard)
+        buf = oracle.c_fill(seed, blo, bhi - blo, b"ACGT", threads=1)
+        full_pat = plants["pattern"]
+        for x in plants["at"]:
+            lo, hi = max(x, blo), min(x + m, bhi)
+            if lo < hi:
+                buf[lo - blo: hi - blo] = np.frombuffer(full_pat[lo - x: hi - x], dtype=np.uint8)
+        shard = torch.from_numpy(buf)
+        offs, tot = sharded.search_sharded(shard, full_pat, a, b, blo, scan_fn=_oracle_scan)
+        q.put((rank, offs.tolist(), tot))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_c4_shape_sharded_gloo(world):
+    """BASELINE configs[3] at 4 MiB: DNA (seed 42), a sampled 32-byte pattern, copies
+    planted across every 2/4/8-way shard cut; each rank regenerates only its shard + halo
+    and the gathered list equals the oracle's scan of the whole text, on every rank."""
+    n, m, seed = 4 << 20, 32, 42
+    text = np.frombuffer(oracle.generate(seed, n), dtype=np.uint8)
+    pat = oracle.make_pattern(text.tobytes(), seed, b"ACGT", m, "sampled")
+    cuts = sorted({sharded.strong_shard(r, w, n, m)[0] for w in (2, 4, 8) for r in range(1, w)})
+    at = []
+    for x in [c - m // 2 for c in cuts]:
+        if not at or x >= at[-1] + m:
+            at.append(x)
+    full = oracle.plant(text.tobytes(), pat, at)
+    expect, coll = oracle.c_scan(np.frombuffer(full, dtype=np.uint8),
+                                 np.frombuffer(pat, dtype=np.uint8))
+    assert set(at) <= set(expect.tolist())
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_c4_worker,
+                         args=(r, world, port, seed, n, m, {"pattern": pat, "at": at}, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, offs, tot in out:
+        assert offs == expect.tolist(), rank
+        assert tot == [len(expect), len(expect) + coll, coll]
