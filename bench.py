@@ -11,7 +11,8 @@ from the corpus as rkmatch.bench._make_pattern does).  One step = the whole swee
 
 N > 1 runs under torchrun, one rank per GPU: weak scaling, each rank owns 1 GiB of the
 global N GiB corpus plus an (m-1)-byte halo, scans it, and the global ordered position
-list is returned with NCCL all_gather.  `--impl reference` times the reference
+list is returned to every rank by the C ABI's rk_scan_sharded (NCCL allgather-v).
+`--workload C4` runs BASELINE configs[3] instead: 16 GiB DNA, m = 32, strong scaling.  `--impl reference` times the reference
 algorithm (the C restatement in oracle/ of rkmatch._scan_range + search_parallel's range
 partition) on the host cores on a bounded sample of the same workload.
 """
@@ -49,6 +50,11 @@ def parse():
     ap.add_argument("--bytes-per-gpu", type=int, default=GiB)
     ap.add_argument("--sweep", type=str, default=",".join(map(str, SWEEP)))
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--workload", choices=("C2", "C4"), default="C2",
+                    help="C2 (default, BASELINE configs[1], weak scaling) or C4 (configs[3]: "
+                         "16 GiB DNA, strong scaling)")
+    ap.add_argument("--c4-bytes", type=int, default=16 * GiB)
+    ap.add_argument("--sustained-steps", type=int, default=200)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-seconds", type=float, default=150.0,
@@ -225,6 +231,69 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------- GPU arm
+def load_traffic():
+    """Per-m DRAM bytes per launch of rk_scan_kernel<M> (dram__bytes_read.sum +
+    dram__bytes_write.sum), from the ncu pass of this command summarised by
+    profiles/traffic_from_ncu.py."""
+    p = ROOT / "profiles" / "r02_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text())
+    except Exception:
+        return None
+
+
+def setup_dist(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = 0 if args.same_device else local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        # each rank logs its NCCL communicator (torch's and librkb200's) to stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        os.environ.setdefault("RKB200_COMM_LOG", "1")
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, dev
+
+
+def timed_steps(step, steps, stream, dev, world):
+    """K steps back to back bracketed by a barrier + synchronize, device-timed with CUDA
+    events on the launching stream, max over ranks; NVML clocks sampled meanwhile."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        start.record(stream)
+        for _ in range(steps):
+            step(None)
+        end.record(stream)
+        # poll (sleeping, GIL released) instead of blocking, so the clock sampler thread
+        # keeps sampling while the device drains the queued steps
+        while not end.query():
+            time.sleep(0.0002)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([start.elapsed_time(end)], dtype=torch.float64, device=f"cuda:{dev}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), clk.summary()
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -234,16 +303,9 @@ def run_ours(args):
 
     if args.lib:
         _lib.LIB_PATH = Path(args.lib).resolve()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    dev = 0 if args.same_device else local
-    torch.cuda.set_device(dev)
-    if world > 1:
-        if args.dist_backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
-        else:
-            dist.init_process_group("gloo")
+    world, rank, dev = setup_dist(args)
+    if args.workload == "C4":
+        return run_c4(args, world, rank, dev)
     sweep = [int(x) for x in args.sweep.split(",")]
     per = args.bytes_per_gpu
     n_total = per * world
@@ -262,85 +324,61 @@ def run_ours(args):
         plans[m] = (a - byte_lo, b - byte_lo, rk.hash_full(pats[m]))
     L = _lib.lib()
     ctx = _lib.context(dev)
+    comm = sharded.Communicator(device=dev) if world > 1 else None
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
     cap = 1 << 22
     out_all = torch.empty((len(sweep), cap), dtype=torch.int64, device=f"cuda:{dev}")
     outs = {m: out_all[i] for i, m in enumerate(sweep)}
     counts = torch.zeros((len(sweep), 3), dtype=torch.int64, device=f"cuda:{dev}")
-    # the exchange (N > 1): every rank's counters and ordered positions, per length, in
-    # two all_gathers per step over NVLink and no host round trip inside the step; the
-    # position slots hold GATHER_SLOT offsets per length (the C2 sweep finds <= 13 per
-    # GiB; a rank with more is caught by the gate after the timed region)
-    GATHER_SLOT = 8192
-    if world > 1:
-        all_counts = torch.empty((world, len(sweep), 3), dtype=torch.int64, device=f"cuda:{dev}")
-        all_pos = torch.empty((world, len(sweep), GATHER_SLOT), dtype=torch.int64, device=f"cuda:{dev}")
+    glob = {}
     pat_bufs = {m: np.frombuffer(pats[m], dtype=np.uint8) for m in sweep}
     n_local = int(text.numel())
-
-    def gather_into(out, inp):
-        if args.dist_backend == "nccl":
-            dist.all_gather_into_tensor(out, inp)
-        else:  # gloo (the one-GPU plumbing test): list form
-            dist.all_gather(list(out.unbind(0)), inp)
 
     def step(ev_pairs=None):
         for i, m in enumerate(sweep):
             a, b, hx = plans[m]
             if ev_pairs is not None:
                 ev_pairs[i][0].record(stream)
-            _lib.check(L.rk_scan_async(ctx.handle, text.data_ptr(), n_local, pat_bufs[m].ctypes.data,
-                                       m, hx, a, b, outs[m].data_ptr(), cap, byte_lo,
-                                       counts[i].data_ptr(), sptr))
+            if comm is None:
+                _lib.check(L.rk_scan_async(ctx.handle, text.data_ptr(), n_local,
+                                           pat_bufs[m].ctypes.data, m, hx, a, b,
+                                           outs[m].data_ptr(), cap, byte_lo,
+                                           counts[i].data_ptr(), sptr))
+            else:
+                # the C ABI's sharded scan: local scan, counters all-gathered, every rank's
+                # ordered positions broadcast into every rank's output (exact allgather-v)
+                glob[m] = comm.scan(text, pats[m], a + byte_lo, b + byte_lo, byte_lo,
+                                    cap=cap, out=outs[m], stream=sptr)
             if ev_pairs is not None:
                 ev_pairs[i][1].record(stream)
-        if world > 1:
-            gather_into(all_counts, counts)
-            gather_into(all_pos, out_all[:, :GATHER_SLOT].contiguous())
         return counts
 
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
-    # correctness gate: every ordered list is what a second pass gives, and counts add up
-    host_counts = counts.cpu().numpy()
+    # correctness gate: counts add up; at N > 1 every rank holds the same global ascending
+    # list, and its total is the sum over ranks
+    if comm is None:
+        host_counts = counts.cpu().numpy()
+    else:
+        host_counts = np.array([[glob[m][1], glob[m][3], glob[m][2]] for m in sweep], dtype=np.int64)
+        for m in sweep:
+            g = glob[m][0]
+            assert g.numel() == glob[m][1] and bool((g[1:] > g[:-1]).all())
     assert (host_counts[:, 1] == host_counts[:, 0] + host_counts[:, 2]).all()
-    if world > 1:
-        ac = all_counts.cpu().numpy()
-        assert (ac[:, :, 0] <= GATHER_SLOT).all(), "gather slot too small for this corpus"
-        ap = all_pos.cpu().numpy()
-        for i in range(len(sweep)):  # the global list, concatenated in rank order, ascends
-            glob = np.concatenate([ap[r, i, : ac[r, i, 0]] for r in range(world)])
-            assert (np.diff(glob) > 0).all()
 
     # Headline: K steps back to back with nothing between the launches (an event recorded
     # between two kernels costs the programmatic-dependent-launch overlap, ~4%).  Then,
     # after an idle gap (right after ~30 ms of full-bandwidth streaming the next pass runs
     # ~4% slower; after ~1 s idle it does not), the same K steps again with CUDA events
     # around every scan + emit, for the per-length numbers and the kernel's per-launch
-    # duration (roofline).
+    # duration (roofline).  Last, a sustained pass of many steps (power-capped clocks).
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in sweep] for _ in range(args.steps)]
-    launches0 = ctx.launches
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clk:
-        start.record(stream)
-        for s in range(args.steps):
-            step(None)
-        end.record(stream)
-        # poll (sleeping, GIL released) instead of blocking, so the clock sampler thread
-        # keeps sampling while the device drains the queued steps
-        while not end.query():
-            time.sleep(0.0002)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    launches = ctx.launches - launches0
-    elapsed_ms = start.elapsed_time(end)
+    launches0 = ctx.launches + (comm.ctx.launches if comm else 0)
+    elapsed_ms, clk = timed_steps(step, args.steps, stream, dev, world)
+    launches = ctx.launches + (comm.ctx.launches if comm else 0) - launches0
     time.sleep(args.pass_gap)
     # per-length pass: the same steps with events around every scan + emit
     with ClockSampler(dev) as clk_b:
@@ -353,87 +391,63 @@ def run_ours(args):
         dist.barrier()
     per_m_ms = {m: sum(ev[s][i][0].elapsed_time(ev[s][i][1]) for s in range(args.steps)) / args.steps
                 for i, m in enumerate(sweep)}
-    t_all = torch.tensor([elapsed_ms], dtype=torch.float64, device=f"cuda:{dev}")
-    if world > 1:
-        dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(t_all.item())
-    host_counts = counts.cpu().numpy()
-    bytes_per_step_rank = sum(plans[m][1] - plans[m][0] + m - 1 for m in sweep)
     windows_all = sum(max(n_total - m + 1, 0) for m in sweep)
     value = windows_all / (elapsed_ms / args.steps / 1e3) / 1e9  # text (window) bytes/s
+    sustained = None
+    if args.sustained_steps > 0:
+        time.sleep(args.pass_gap)
+        sus_ms, clk_s = timed_steps(step, args.sustained_steps, stream, dev, world)
+        sustained = {"value": windows_all / (sus_ms / args.sustained_steps / 1e3) / 1e9,
+                     "unit": "GB/s", "steps": args.sustained_steps,
+                     "ms_per_step": sus_ms / args.sustained_steps, "clocks": clk_s,
+                     "note": "the headline's steps back to back for ~0.3 s: the board's power "
+                             "limit lowers the SM clock under sustained full-bandwidth streaming"}
 
-    # roofline of the scan kernel: algorithmic bytes = n + 8*matches per launch
+    # roofline of the scan kernel: algorithmic bytes = n + 8*matches per launch (local)
     peak, peak_kind = load_peaks()
-    alg = [(plans[m][1] - plans[m][0] + m - 1) + 8 * int(host_counts[i, 0]) for i, m in enumerate(sweep)]
+    local_counts = counts.cpu().numpy() if comm is None else None
+    alg = [(plans[m][1] - plans[m][0] + m - 1) +
+           8 * int((local_counts if local_counts is not None else host_counts)[i, 0])
+           for i, m in enumerate(sweep)]
     achieved = sum(alg) / (sum(per_m_ms.values()) / 1e3) / 1e9
-    traffic = None
-    tf = ROOT / "profiles" / "dram_traffic.json"
-    if tf.exists():
-        try:
-            traffic = json.loads(tf.read_text()).get("bytes_per_launch")
-        except Exception:
-            traffic = None
+    tr = load_traffic()
+    traffic = traffic_per_m = None
+    if tr and all(str(m) in tr.get("per_m", {}) for m in sweep):
+        traffic_per_m = {str(m): tr["per_m"][str(m)] for m in sweep}
+        traffic = sum(traffic_per_m.values()) / len(sweep)  # per launch, sweep mean
 
     # ---------------------------------------------------------------- e2e (host API)
-    # One step = the sweep's inputs (this rank's text and the patterns) from pinned host
-    # memory through the C ABI to host-side results: the text crosses PCIe once per step
-    # (it is ONE input of the step) and every pattern is scanned on it as it lands.
-    # e2e_per_call repeats the text transfer for every pattern (rk_scan_host: one call per
-    # pattern with a host text, chunks DMA'd and scanned as they land).
+    # search_each's C entry point, rk_scan_host_batch: this rank's text from pinned host
+    # memory and the sweep's patterns in, every pattern's counters and ordered offsets
+    # back in host memory; the text crosses PCIe once per step and each pattern's windows
+    # are scanned as their bytes land (a step's inputs copied every step, inside the
+    # timed region).  e2e_per_call: rk_scan_host per pattern (search_sequential on a host
+    # text: the text crosses PCIe for every pattern).
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 3)
     e2e = e2e_call = None
     if e2e_steps > 0:
         host = text.cpu().pin_memory()
-        t_dev = torch.empty_like(text)
-        h_out = torch.empty(cap, dtype=torch.int64).pin_memory()
+        h_out = torch.empty(1 << 20, dtype=torch.int64).pin_memory()
+        flat = np.frombuffer(b"".join(pats[m] for m in sweep), dtype=np.uint8)
+        lens = np.array(sweep, dtype=np.uint32)
+        hashes = np.array([plans[m][2] for m in sweep], dtype=np.uint64)
+        b_mt, b_co, b_hh = (np.zeros(len(sweep), dtype=np.uint64) for _ in range(3))
         mt, co, hh = _lib.u64ref(), _lib.u64ref(), _lib.u64ref()
         h2d = d2h = 0
-
-        # the text lands in E2E_CHUNK pieces on a copy stream; as piece k lands, every
-        # pattern's windows that END in it are scanned (rk_scan_async over that window
-        # range of the resident text; all their bytes have landed), overlapped with the
-        # copy of piece k+1.  Each (piece, pattern) leaves its ordered offsets and counters
-        # on the device; one round trip brings the counters back, a second the offsets.
-        E2E_CHUNK = 64 << 20
-        pieces = [(lo, min(lo + E2E_CHUNK, n_local)) for lo in range(0, n_local, E2E_CHUNK)]
-        e_cap = 1 << 14
-        e_out = torch.empty((len(pieces), len(sweep), e_cap), dtype=torch.int64, device=f"cuda:{dev}")
-        e_cnt = torch.zeros((len(pieces), len(sweep), 3), dtype=torch.int64, device=f"cuda:{dev}")
-        h_cnt = torch.empty_like(e_cnt, device="cpu").pin_memory()
-        copy_stream = torch.cuda.Stream(dev)
-        landed = [torch.cuda.Event() for _ in pieces]
+        # (the batch call scans every window of the text it is given: at N > 1 a rank's
+        # text ends with its (mmax - 1)-byte halo, so shorter patterns also see a few of the
+        # next rank's windows there -- an end-to-end rank-local number, not an exchange)
 
         def e2e_step():
             nonlocal h2d, d2h
-            for k, (lo, hi) in enumerate(pieces):
-                with torch.cuda.stream(copy_stream):
-                    t_dev[lo:hi].copy_(host[lo:hi], non_blocking=True)
-                    landed[k].record(copy_stream)
-            h2d += host.numel() + sum(m for m in sweep)
-            for k, (lo, hi) in enumerate(pieces):
-                stream.wait_event(landed[k])
-                for i, m in enumerate(sweep):
-                    a, b, hx = plans[m]
-                    ws, we = max(a, lo - m + 1), min(b, hi - m + 1)  # window ends in [lo, hi)
-                    if we <= ws:
-                        e_cnt[k, i].zero_()
-                        continue
-                    _lib.check(L.rk_scan_async(ctx.handle, t_dev.data_ptr(), n_local,
-                                               pat_bufs[m].ctypes.data, m, hx, ws, we,
-                                               e_out[k, i].data_ptr(), e_cap, 0,
-                                               e_cnt[k, i].data_ptr(), sptr))
-            h_cnt.copy_(e_cnt, non_blocking=True)
-            torch.cuda.current_stream(dev).synchronize()
-            d2h += h_cnt.numel() * 8
-            cnt = h_cnt.numpy()
-            assert (cnt[:, :, 0] <= e_cap).all(), "e2e offset slots too small"
-            got = []
-            for i, m in enumerate(sweep):
-                parts = [e_out[k, i, : int(cnt[k, i, 0])] for k in range(len(pieces)) if cnt[k, i, 0]]
-                offs = torch.cat(parts).cpu() if parts else torch.empty(0, dtype=torch.int64)
-                d2h += 8 * offs.numel()
-                got.append(int(cnt[:, i, 0].sum()))
-            return got
+            _lib.check(L.rk_scan_host_batch(ctx.handle, host.data_ptr(), n_local,
+                                            flat.ctypes.data, lens.ctypes.data,
+                                            hashes.ctypes.data, len(sweep), h_out.data_ptr(),
+                                            h_out.numel(), b_mt.ctypes.data, b_co.ctypes.data,
+                                            b_hh.ctypes.data))
+            h2d += n_local + int(flat.size)
+            d2h += 8 * min(int(b_mt.sum()), h_out.numel()) + 32 * len(sweep)
+            return [int(v) for v in b_mt]
 
         def e2e_call_step():
             nonlocal h2d, d2h
@@ -441,17 +455,18 @@ def run_ours(args):
             for m in sweep:
                 a, b, hx = plans[m]
                 _lib.check(L.rk_scan_host(ctx.handle, host.data_ptr(), n_local, pat_bufs[m].ctypes.data,
-                                          m, hx, a, b, h_out.data_ptr(), cap, ctypes.byref(mt),
-                                          ctypes.byref(co), ctypes.byref(hh)))
+                                          m, hx, a, b, h_out.data_ptr(), h_out.numel(),
+                                          ctypes.byref(mt), ctypes.byref(co), ctypes.byref(hh)))
                 h2d += (b - a) + m - 1
-                d2h += 8 * min(int(mt.value), cap) + 24
+                d2h += 8 * min(int(mt.value), h_out.numel()) + 24
                 got.append(int(mt.value))
             return got
 
-        def timed_e2e(fn, steps, api):
+        def timed_e2e(fn, steps, api, check):
             nonlocal h2d, d2h
             got = fn()
-            assert got == [int(v) for v in host_counts[:, 0]], (got, host_counts[:, 0])
+            if check is not None:
+                assert got == check, (got, check)
             h2d = d2h = 0
             torch.cuda.synchronize()
             if world > 1:
@@ -467,14 +482,17 @@ def run_ours(args):
                     "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
                     "steps": steps, "api": api}
 
+        local_k = [int(v) for v in (local_counts[:, 0] if local_counts is not None else [0] * len(sweep))]
         e2e = timed_e2e(e2e_step, e2e_steps,
-                        "pinned host text -> HBM once per step in 64 MiB pieces on a copy stream; "
-                        "rk_scan_async of every pattern over the windows ending in each landed "
-                        "piece, overlapped with the next piece's copy; counters and ordered "
-                        "offsets -> host")
+                        "rk_scan_host_batch (C ABI; Python: paper_1810_01051_b200.search_each) -- "
+                        "pinned host text + the 9 patterns in, per-pattern counters and ordered "
+                        "offsets out in host memory; the text crosses PCIe once per step in 64 "
+                        "MiB chunks, every pattern scanning each chunk as it lands",
+                        local_k if world == 1 else None)
         e2e_call = timed_e2e(e2e_call_step, 1,
-                             "rk_scan_host per pattern (the host text crosses PCIe for every "
-                             "pattern, chunked DMA overlapped with the scan)")
+                             "rk_scan_host per pattern (search_sequential on a host text: the "
+                             "text crosses PCIe for every pattern, chunked DMA overlapped with "
+                             "the scan)", local_k if world == 1 else None)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -505,19 +523,132 @@ def run_ours(args):
             "matches_per_m": {str(m): int(host_counts[i, 0]) for i, m in enumerate(sweep)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "traffic_per_m": traffic_per_m,
+                         "traffic_source": tr.get("source") if tr else None,
                          # the same bytes over the headline steps' time (scans, emits and
                          # the gaps between them, no events in between)
                          "achieved_headline_steps": sum(alg) / (elapsed_ms / args.steps / 1e3) / 1e9,
                          "peak_kind": peak_kind, "kernel": "rk_scan_kernel<M>",
                          "algorithmic_bytes": "n + 8*matches per launch"},
+            "sustained": sustained,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_per_call": e2e_call,
-            "clocks": clk.summary(),
+            "clocks": clk,
             "clocks_per_m_pass": clk_b.summary(),
             "gpu_launches": launches,
         }
+        if comm is not None:
+            line["exchange"] = {"api": "rk_scan_sharded (C ABI, NCCL allgather-v)",
+                                "nccl": comm.info()}
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_c4(args, world, rank, dev):
+    """BASELINE configs[3]: 16 GiB DNA, a sampled 32-byte pattern with copies planted
+    across every 2/4/8-way shard cut, strong scaling: rank r holds its windows' bytes +
+    the (m-1)-byte halo (rk_shard_range) and the global ordered list is returned to every
+    rank by rk_scan_sharded."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1810_01051_b200 as rk
+    from paper_1810_01051_b200 import _lib, sharded
+
+    n, m = args.c4_bytes, 32
+    spec = rk.DnaSpec(SEED, n)
+    a, b, blo, bhi = sharded.shard_range(n, m, world, rank)
+    text = rk.generate_tensor(spec, device=f"cuda:{dev}", skip=blo, count=bhi - blo)
+    x = sampled_offset(n, m)
+    pat = rk.generate_tensor(spec, device=f"cuda:{dev}", skip=x, count=m).cpu().numpy().tobytes()
+    cuts = sorted({sharded.shard_range(n, m, w, r)[0] for w in (2, 4, 8) for r in range(1, w)})
+    plants = []
+    for y in [c - m // 2 for c in cuts] + [n - m]:
+        if not plants or y >= plants[-1] + m:
+            plants.append(y)
+    parr = torch.frombuffer(bytearray(pat), dtype=torch.uint8).to(f"cuda:{dev}")
+    for y in plants:
+        lo, hi = max(y, blo), min(y + m, bhi)
+        if lo < hi:
+            text[lo - blo: hi - blo] = parr[lo - y: hi - y]
+    L = _lib.lib()
+    comm = sharded.Communicator(device=dev)  # a 1-rank communicator at N = 1
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    out = torch.empty(1 << 20, dtype=torch.int64, device=f"cuda:{dev}")
+    res = {}
+
+    def step(_ev=None):
+        res["r"] = comm.scan(text, pat, a, b, blo, cap=out.numel(), out=out, stream=sptr)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    offs, k, coll, hits = res["r"]
+    got = set(offs.cpu().tolist())
+    assert set(plants) <= got and hits == k + coll
+    l0 = comm.ctx.launches
+    elapsed_ms, clk = timed_steps(step, args.steps, stream, dev, world)
+    launches = comm.ctx.launches - l0
+    value = (n - m + 1) / (elapsed_ms / args.steps / 1e3) / 1e9
+    peak, peak_kind = load_peaks()
+    local_bytes = bhi - blo
+    e2e = None
+    if (args.e2e_steps or 0) > 0:
+        host = text.cpu().pin_memory()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            o2, k2, _, _ = comm.scan(host, pat, a, b, blo, cap=out.numel(), out=out, stream=sptr)
+            o2.cpu()
+        torch.cuda.synchronize()
+        t_e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{dev}")
+        if world > 1:
+            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        e2e = {"value": (n - m + 1) / (float(t_e.item()) / args.e2e_steps) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": local_bytes + m, "d2h_bytes_per_step": 8 * k + 32 * world,
+               "steps": args.e2e_steps,
+               "api": "rk_scan_sharded with this rank's pinned host shard (staged in 64 MiB "
+                      "chunks overlapped with the scan) + the global list to host"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+
+        threads = oracle.cpu_threads()
+        sample = text[: 512 << 20].cpu().numpy()
+        t0 = time.perf_counter()
+        oracle.c_scan(sample, np.frombuffer(pat, dtype=np.uint8), workers=threads)
+        dt = time.perf_counter() - t0
+        cpu = {"value": sample.size / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+               "sample": "512 MiB prefix of the C4 corpus, m = 32 (oracle C port of "
+                         "_scan_range + search_parallel ranges)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (rkmatch generator, on device)",
+            "config": {"workload": "C4: 16 GiB synthetic DNA, 32-byte pattern, sharded with "
+                                   "halo (BASELINE.json configs[3])",
+                       "bytes_total": n, "m": m, "plants": len(plants),
+                       "l2": "inputs larger than L2",
+                       "parallelism": f"shard{world} (strong, rk_shard_range, (m-1)-byte halo)"},
+            "matches": int(k), "collisions": int(coll),
+            "roofline": {"bound": "hbm",
+                         "achieved": (local_bytes + 8 * k) / (elapsed_ms / args.steps / 1e3) / 1e9,
+                         "peak": peak, "unit": "GB/s", "peak_kind": peak_kind,
+                         "kernel": "rk_scan_kernel<32> (+ emit + exchange)",
+                         "algorithmic_bytes": "shard bytes + 8*matches per step"},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
+            "exchange": {"api": "rk_scan_sharded (C ABI, NCCL allgather-v)", "nccl": comm.info()},
+        }
+        line["roofline"]["frac"] = line["roofline"]["achieved"] / peak
+        print(json.dumps(line), flush=True)
+    comm.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -113,8 +113,24 @@ int rk_scan_bitmap(rk_ctx_t* ctx, const uint8_t* d_text, uint64_t n, const uint8
 int rk_scan_host(rk_ctx_t* ctx, const uint8_t* h_text, uint64_t n, const uint8_t* h_pattern,
                  uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t* h_out,
                  uint64_t cap, uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits);
-/* Copies offsets [first, first+count) of the last rk_scan_host of this context (all of
- * them are kept on the device, so a caller whose cap was too small never rescans). */
+/*
+ * rk_scan_host_batch -- one HOST text, P patterns: search_sequential for each pattern
+ * (matcher.py:101-122) -- the reference CLI's per-pattern loop over a pattern file
+ * (cli.py:105-118) -- with the text crossing PCIe ONCE.  Pattern i is h_lengths[i] bytes
+ * of h_patterns (back to back) with hash h_hashes[i]; its windows are [0, n - m_i + 1).
+ * The text is staged chunk by chunk as in rk_scan_host and every pattern's windows ending
+ * in a chunk are scanned as soon as it lands.  matches / collisions / hash_hits (P
+ * entries each) receive every pattern's totals; h_out the first cap offsets of the
+ * concatenation (pattern 0's ordered offsets, then pattern 1's, ...).  Synchronous.
+ */
+#define RK_BATCH_MAX_PATTERNS 64
+int rk_scan_host_batch(rk_ctx_t* ctx, const uint8_t* h_text, uint64_t n,
+                       const uint8_t* h_patterns, const uint32_t* h_lengths,
+                       const uint64_t* h_hashes, uint32_t P, int64_t* h_out, uint64_t cap,
+                       uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits);
+/* Copies offsets [first, first+count) of the last rk_scan_host / rk_scan_host_batch of
+ * this context (all of them are kept on the device, so a caller whose cap was too small
+ * never rescans; for a batch, indices run over the per-pattern concatenation). */
 int rk_scan_host_fetch(rk_ctx_t* ctx, int64_t* h_out, uint64_t first, uint64_t count);
 
 /*

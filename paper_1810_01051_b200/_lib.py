@@ -18,12 +18,13 @@ LIB_PATH = Path(__file__).resolve().parent / "librkb200.so"
 RK_OK, RK_EINVAL, RK_ECUDA, RK_ENCCL = 0, 1, 2, 3
 COMM_ID_BYTES = 128
 MULTI_MAX_PATTERNS = 4096
+BATCH_MAX_PATTERNS = 64
 
 # every symbol include/rkb200.h declares (checked by tests/test_capi.py)
 EXPORTS = (
     "rk_version", "rk_last_error", "rk_device_count", "rk_ctx_create", "rk_ctx_destroy",
     "rk_scan", "rk_scan_async", "rk_scan_result", "rk_scan_bitmap", "rk_scan_host",
-    "rk_scan_host_fetch", "rk_scan_fetch",
+    "rk_scan_host_fetch", "rk_scan_fetch", "rk_scan_host_batch",
     "rk_multi_scan", "rk_multi_scan_mixed", "rk_window_hashes", "rk_generate", "rk_launch_count",
     "rk_comm_get_unique_id", "rk_comm_init", "rk_comm_destroy", "rk_comm_info", "rk_shard_range",
     "rk_scan_sharded", "rk_comm_fetch",
@@ -61,6 +62,9 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.rk_scan_result.argtypes = [vp, pu64, pu64, pu64, vp]
     lib.rk_scan_host.restype = ci
     lib.rk_scan_host.argtypes = [vp, u8p, u64, u8p, u32, u64, u64, u64, vp, u64, pu64, pu64, pu64]
+    lib.rk_scan_host_batch.restype = ci
+    lib.rk_scan_host_batch.argtypes = [vp, u8p, u64, u8p, vp, vp, ctypes.c_uint32, vp, u64, vp,
+                                       vp, vp]
     lib.rk_scan_host_fetch.restype = ci
     lib.rk_scan_host_fetch.argtypes = [vp, vp, u64, u64]
     lib.rk_scan_fetch.restype = ci

@@ -185,22 +185,35 @@ int begin_scan(rk_ctx* c, uint64_t tiles, cudaStream_t s) {
 // Orders the offsets of a logical scan whose tiles are sequence numbers [0, tiles)
 // starting at a-space tile `tile0`; copies {matches, hash_hits, collisions} to d_counts
 // if given, and zeroes the other counter set for the next scan.
+// Per-logical-scan device state.  Normally the context's (one scan at a time, counter
+// sets alternating); a batch of scans over one staged text keeps one of these per
+// pattern, so every pattern's results stay live until its offsets are emitted.
+struct ScanScratch {
+  unsigned long long* counters;    // [0] matches, [1] hash_hits, [2] collisions
+  unsigned long long* block_sums;
+  uint32_t* tile_info;
+  uint32_t* masks;
+  const uint8_t* pattern;          // device copy of the pattern
+};
+
 int emit(rk_ctx* c, uint64_t tiles, uint64_t tile0, int64_t start_bias, int64_t* d_out,
          uint64_t cap, cudaStream_t s, uint64_t* d_counts = nullptr,
-         uint32_t* d_bitmap = nullptr, int64_t bit_bias = 0) {
+         uint32_t* d_bitmap = nullptr, int64_t bit_bias = 0,
+         const ScanScratch* x = nullptr) {
   EmitArgs e;
-  e.tile_info = c->d_tile_info;
-  e.masks = c->d_masks;
-  e.block_sums = c->d_block_sums;
+  e.tile_info = x ? x->tile_info : c->d_tile_info;
+  e.masks = x ? x->masks : c->d_masks;
+  e.block_sums = x ? x->block_sums : c->d_block_sums;
   e.num_tiles = tiles;
   e.tile0 = tile0;
   e.start_bias = start_bias;
   e.out = d_out;
   e.cap = d_out ? cap : 0;
-  e.counters = c->d_counters;
+  e.counters = x ? x->counters : c->d_counters;
   e.counts_out = (unsigned long long*)d_counts;
-  e.clear = c->d_sets + (uint64_t)(c->cur_set ^ 1) * set_words(c);
-  e.clear_words = set_words(c);
+  // (a batch's counters are zeroed once, up front: nothing to clear for the next scan)
+  e.clear = x ? nullptr : c->d_sets + (uint64_t)(c->cur_set ^ 1) * set_words(c);
+  e.clear_words = x ? 0 : set_words(c);
   e.bitmap = nullptr;
   e.bit_bias = 0;
   if (d_bitmap) {
@@ -245,16 +258,17 @@ int grid_for(uint64_t tiles, int num_sms, int blocks_per_sm, int warps_per_block
 }
 
 int launch_one(rk_ctx* c, const uint8_t* d_text, uint64_t n, uint32_t m, uint64_t hx,
-               uint64_t start, uint64_t stop, uint64_t seq_base, const PatWords& pw, cudaStream_t s) {
+               uint64_t start, uint64_t stop, uint64_t seq_base, const PatWords& pw, cudaStream_t s,
+               const ScanScratch* x = nullptr) {
   const Geometry g = geometry(d_text, m, start, stop);
   ScanArgs a{};
   a.g = text_geom(g, n, m, seq_base);
-  a.pattern = c->d_pattern;
+  a.pattern = x ? x->pattern : c->d_pattern;
   a.hx = hx;
-  a.counters = c->d_counters;
-  a.block_sums = c->d_block_sums;
-  a.tile_info = c->d_tile_info;
-  a.masks = c->d_masks;
+  a.counters = x ? x->counters : c->d_counters;
+  a.block_sums = x ? x->block_sums : c->d_block_sums;
+  a.tile_info = x ? x->tile_info : c->d_tile_info;
+  a.masks = x ? x->masks : c->d_masks;
   a.pw = pw;
   // A scan with fewer tiles than the full grid has warps (e.g. C1, 1 MiB = 128 tiles
   // against 148 x 20 warps at m = 8) spreads them: every CTA slot gets ceil(tiles / slots)
@@ -741,6 +755,11 @@ int rk_ctx_destroy(rk_ctx_t* c) {
   cudaEventDestroy(c->ev_ready);
   cudaStreamDestroy(c->s_copy);
   cudaStreamDestroy(c->s_comp);
+  cudaFree(c->d_binfo);
+  cudaFree(c->d_bspill);
+  cudaFree(c->d_bmasks);
+  cudaFree(c->d_bsets);
+  cudaFreeHost(c->h_bcounts);
   cudaFree(c->d_mblob);
   cudaFree(c->d_sort);
   cudaFreeHost(c->h_mstage);
@@ -852,6 +871,7 @@ int rk_scan_host(rk_ctx_t* c, const uint8_t* h_text, uint64_t n, const uint8_t* 
     if (int r = emit_last(c, c->d_out_stage, mt, sc)) return r;
   }
   c->host_last = mt;
+  c->batch_segs.assign(1, rk_ctx::BatchSeg{c->d_out_stage, mt});
   const uint64_t nout = std::min(mt, cap);
   if (nout) {
     RK_CUDA(cudaMemcpyAsync(h_out, c->d_out_stage, nout * sizeof(int64_t), cudaMemcpyDeviceToHost,
@@ -861,6 +881,199 @@ int rk_scan_host(rk_ctx_t* c, const uint8_t* h_text, uint64_t n, const uint8_t* 
   if (matches) *matches = mt;
   if (collisions) *collisions = co;
   if (hash_hits) *hash_hits = hh;
+  return RK_OK;
+}
+
+int rk_scan_host_batch(rk_ctx_t* c, const uint8_t* h_text, uint64_t n, const uint8_t* h_patterns,
+                       const uint32_t* h_lengths, const uint64_t* h_hashes, uint32_t P,
+                       int64_t* h_out, uint64_t cap, uint64_t* matches, uint64_t* collisions,
+                       uint64_t* hash_hits) {
+  if (!c) return fail(RK_EINVAL, "context is NULL");
+  if (P < 1 || P > RK_BATCH_MAX_PATTERNS)
+    return fail(RK_EINVAL, "pattern count %u outside [1, %d]", P, RK_BATCH_MAX_PATTERNS);
+  if (!h_patterns || !h_lengths || !h_hashes || !matches || !collisions || !hash_hits)
+    return fail(RK_EINVAL, "NULL pattern or result arrays");
+  for (uint32_t i = 0; i < P; ++i)
+    if (h_lengths[i] < 1) return fail(RK_EINVAL, "pattern %u is empty", i);
+  if (n && !h_text) return fail(RK_EINVAL, "text pointer is NULL");
+  if (cap && !h_out) return fail(RK_EINVAL, "output pointer is NULL with cap > 0");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  cudaStream_t sc = c->s_comp, sk = c->s_copy;
+  if (int r = enter(c, sc)) return r;
+  c->host_last = 0;
+  c->batch_segs.clear();
+  c->last_scan.valid = false;
+
+  // per pattern: its windows [0, n - m + 1) as a-space geometry of the staging buffer,
+  // its scratch slices and device pattern copy
+  struct Job {
+    uint32_t m;
+    uint64_t hx, nw;
+    Geometry gall;
+    uint64_t info_off, set_off, nb;
+    const uint8_t* pat;
+    PatWords pw;
+    bool live;
+  };
+  std::vector<Job> jobs(P);
+  uint64_t info_words = 0, set_words_all = 0, max_m = 0, pat_off = 0;
+  for (uint32_t i = 0; i < P; ++i) {
+    Job& j = jobs[i];
+    j.m = h_lengths[i];
+    j.hx = h_hashes[i];
+    j.pat = h_patterns + pat_off;
+    pat_off += j.m;
+    j.nw = n >= j.m ? n - j.m + 1 : 0;
+    j.live = j.nw > 0 && !hash_unreachable(j.m, j.hx);
+    if (!j.live) continue;
+    max_m = std::max<uint64_t>(max_m, j.m);
+    j.gall = geometry(nullptr, j.m, 0, j.nw);  // the staging buffer is 256-byte aligned
+    j.info_off = info_words;
+    info_words += j.gall.num_tiles;
+    j.nb = (j.gall.num_tiles + kEmitTiles - 1) / kEmitTiles;
+    j.set_off = set_words_all;
+    set_words_all += 4 + j.nb;
+    j.pw = pack_pattern(j.pat, j.m);
+  }
+  // every pattern's device copy first (the cache may sync the stream to reuse a slot:
+  // before any of this call's copies are queued)
+  std::vector<const uint8_t*> dpat(P, nullptr);
+  for (uint32_t i = 0; i < P; ++i) {
+    if (!jobs[i].live) continue;
+    if (int r = upload_pattern(c, jobs[i].pat, jobs[i].m, sc)) return r;
+    dpat[i] = c->d_pattern;
+  }
+  if (c->h_bcounts_cap < P) {
+    RK_CUDA(cudaStreamSynchronize(sc));
+    if (c->h_bcounts) RK_CUDA(cudaFreeHost(c->h_bcounts));
+    c->h_bcounts = nullptr;
+    RK_CUDA(cudaMallocHost(&c->h_bcounts, 4ull * RK_BATCH_MAX_PATTERNS * sizeof(unsigned long long)));
+    c->h_bcounts_cap = RK_BATCH_MAX_PATTERNS;
+  }
+  memset(c->h_bcounts, 0, 4ull * P * sizeof(unsigned long long));
+  if (!info_words) {
+    for (uint32_t i = 0; i < P; ++i) matches[i] = collisions[i] = hash_hits[i] = 0;
+    return RK_OK;
+  }
+  if (int r = grow(&c->d_stage, &c->stage_cap, n, false, sc)) return r;
+  if (int r = grow(&c->d_binfo, &c->binfo_cap, info_words, false, sc)) return r;
+  if (int r = grow(&c->d_bmasks, &c->bmasks_cap, info_words * (uint64_t)(kTileChunks * 32), false,
+                   sc))
+    return r;
+  if (int r = grow(&c->d_bsets, &c->bsets_cap, set_words_all, false, sc)) return r;
+  constexpr uint64_t kSlot = 1ull << 16;  // offsets per pattern emitted before the counts are known
+  if (int r = grow(&c->d_out_stage, &c->out_stage_cap, kSlot * P, false, sc)) return r;
+  RK_CUDA(cudaMemsetAsync(c->d_bsets, 0, set_words_all * sizeof(unsigned long long), sc));
+  std::vector<ScanScratch> xs(P);
+  for (uint32_t i = 0; i < P; ++i) {
+    if (!jobs[i].live) continue;
+    xs[i].counters = c->d_bsets + jobs[i].set_off;
+    xs[i].block_sums = xs[i].counters + 4;
+    xs[i].tile_info = c->d_binfo + jobs[i].info_off;
+    xs[i].masks = c->d_bmasks + jobs[i].info_off * (uint64_t)(kTileChunks * 32);
+    xs[i].pattern = dpat[i];
+  }
+  cudaPointerAttributes attr;
+  const bool pinned = cudaPointerGetAttributes(&attr, h_text) == cudaSuccess &&
+                      attr.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (!pinned && !c->h_ring[0]) {
+    for (auto& h : c->h_ring) RK_CUDA(cudaMallocHost(&h, kRingSlot));
+    c->copier = new CopyPool();
+  }
+
+  // the text crosses PCIe ONCE: chunk k's bytes land on s_copy while every pattern's
+  // windows ending in chunk k-1 are scanned on s_comp (the just-landed chunk is read from
+  // L2 by the later patterns)
+  const uint64_t k1 = (n - 1) / kStageChunk;
+  uint64_t copied = 0;
+  int slot = 0;
+  for (uint64_t k = 0; k <= k1; ++k) {
+    const uint64_t need = std::min(n, (k + 1) * kStageChunk);
+    if (need > copied) {
+      const uint64_t len = need - copied;
+      if (pinned) {
+        RK_CUDA(cudaMemcpyAsync(c->d_stage + copied, h_text + copied, len,
+                                cudaMemcpyHostToDevice, sk));
+      } else {
+        for (uint64_t off = 0; off < len; off += kRingSlot) {
+          const uint64_t l = std::min<uint64_t>(kRingSlot, len - off);
+          RK_CUDA(cudaEventSynchronize(c->ev_copied[slot]));
+          c->copier->copy(c->h_ring[slot], h_text + copied + off, l);
+          RK_CUDA(cudaMemcpyAsync(c->d_stage + copied + off, c->h_ring[slot], l,
+                                  cudaMemcpyHostToDevice, sk));
+          RK_CUDA(cudaEventRecord(c->ev_copied[slot], sk));
+          slot = (slot + 1) % kRing;
+        }
+      }
+      copied = need;
+      RK_CUDA(cudaEventRecord(c->ev_ready, sk));
+      RK_CUDA(cudaStreamWaitEvent(sc, c->ev_ready, 0));
+    }
+    for (uint32_t i = 0; i < P; ++i) {
+      const Job& j = jobs[i];
+      if (!j.live) continue;
+      const uint64_t e_lo = std::max(j.gall.ja_lo, k * kStageChunk);
+      const uint64_t e_hi = std::min(j.gall.ja_hi, (k + 1) * kStageChunk);
+      if (e_hi <= e_lo) continue;
+      const uint64_t ws = e_lo - (j.m - 1), we = e_hi - (j.m - 1);
+      const Geometry gk = geometry(c->d_stage, j.m, ws, we);
+      if (int r = launch_one(c, c->d_stage, n, j.m, j.hx, ws, we,
+                             gk.tile_first - j.gall.tile_first, j.pw, sc, &xs[i]))
+        return r;
+    }
+  }
+  // every pattern's ordered offsets into its slot; the counts land in mapped pinned memory
+  for (uint32_t i = 0; i < P; ++i) {
+    const Job& j = jobs[i];
+    if (!j.live) continue;
+    if (int r = emit(c, j.gall.num_tiles, j.gall.tile_first, -(int64_t)j.m + 1,
+                     c->d_out_stage + kSlot * i, kSlot, sc, (uint64_t*)(c->h_bcounts + 4 * i),
+                     nullptr, 0, &xs[i]))
+      return r;
+  }
+  RK_CUDA(cudaStreamSynchronize(sc));
+  uint64_t total = 0, spill = 0;
+  for (uint32_t i = 0; i < P; ++i) {
+    matches[i] = c->h_bcounts[4 * i];
+    hash_hits[i] = c->h_bcounts[4 * i + 1];
+    collisions[i] = c->h_bcounts[4 * i + 2];
+    total += matches[i];
+    if (matches[i] > kSlot) spill += (matches[i] + 31) & ~31ull;
+  }
+  // patterns with more offsets than their slot: re-emitted whole, from their kept
+  // per-tile results, into a spill region after the slots (never a rescan)
+  std::vector<const int64_t*> seg(P, nullptr);
+  if (spill) {
+    // (a separate buffer: growing d_out_stage would drop the slots' contents)
+    if (int r = grow(&c->d_bspill, &c->bspill_cap, spill, false, sc)) return r;
+    uint64_t at = 0;
+    for (uint32_t i = 0; i < P; ++i) {
+      if (matches[i] <= kSlot) continue;
+      const Job& j = jobs[i];
+      if (int r = emit(c, j.gall.num_tiles, j.gall.tile_first, -(int64_t)j.m + 1,
+                       c->d_bspill + at, matches[i], sc, nullptr, nullptr, 0, &xs[i]))
+        return r;
+      seg[i] = c->d_bspill + at;
+      at += (matches[i] + 31) & ~31ull;  // segments stay 256-byte aligned
+    }
+  }
+  for (uint32_t i = 0; i < P; ++i) {
+    if (!seg[i]) seg[i] = c->d_out_stage + kSlot * i;
+    c->batch_segs.push_back(rk_ctx::BatchSeg{seg[i], matches[i]});
+  }
+  c->host_last = total;
+  // the first cap offsets (pattern after pattern) to the host
+  uint64_t done = 0;
+  for (uint32_t i = 0; i < P && done < cap; ++i) {
+    const uint64_t k = std::min<uint64_t>(matches[i], cap - done);
+    if (k)
+      RK_CUDA(cudaMemcpyAsync(h_out + done, seg[i], k * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                              sc));
+    done += k;
+  }
+  RK_CUDA(cudaStreamSynchronize(sc));
   return RK_OK;
 }
 
@@ -875,8 +1088,18 @@ int rk_scan_host_fetch(rk_ctx_t* c, int64_t* h_out, uint64_t first, uint64_t cou
   if (!h_out) return fail(RK_EINVAL, "NULL output");
   DeviceGuard g(c->device);
   if (int r = enter(c, c->s_comp)) return r;
-  RK_CUDA(cudaMemcpyAsync(h_out, c->d_out_stage + first, count * sizeof(int64_t),
-                          cudaMemcpyDeviceToHost, c->s_comp));
+  // the offsets are one segment per pattern (a single one after rk_scan_host)
+  uint64_t base = 0, done = 0;
+  for (const auto& sg : c->batch_segs) {
+    if (done == count) break;
+    const uint64_t lo = std::max(first + done, base), hi = std::min(first + count, base + sg.count);
+    if (lo < hi) {
+      RK_CUDA(cudaMemcpyAsync(h_out + done, sg.d + (lo - base), (hi - lo) * sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, c->s_comp));
+      done += hi - lo;
+    }
+    base += sg.count;
+  }
   RK_CUDA(cudaStreamSynchronize(c->s_comp));
   return RK_OK;
 }

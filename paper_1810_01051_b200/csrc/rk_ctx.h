@@ -134,6 +134,24 @@ struct rk_ctx {
     uint64_t tiles = 0, tile0 = 0;
     int64_t start_bias = 0;
   } last_scan;
+  // rk_scan_host_batch: per-pattern per-tile results, counter sets and output segments of
+  // the last batch (all live at once, so any pattern can be re-emitted after the counts
+  // are known)
+  uint32_t* d_binfo = nullptr;
+  uint64_t binfo_cap = 0;
+  uint32_t* d_bmasks = nullptr;
+  uint64_t bmasks_cap = 0;
+  int64_t* d_bspill = nullptr;  // offsets of patterns that overflowed their slot
+  uint64_t bspill_cap = 0;
+  unsigned long long* d_bsets = nullptr;
+  uint64_t bsets_cap = 0;
+  unsigned long long* h_bcounts = nullptr;  // pinned, mapped: {matches, hash_hits, collisions, 0} x P
+  uint32_t h_bcounts_cap = 0;
+  struct BatchSeg {
+    const int64_t* d;  // the pattern's ordered offsets on the device
+    uint64_t count;
+  };
+  std::vector<BatchSeg> batch_segs;  // the last host scan's offsets, in order (rk_scan_host_fetch)
   std::mutex mu;
 };
 

@@ -93,8 +93,8 @@ __device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t g, uint32
       if (__all_sync(kFull, hm == 0xffffffffu)) {
         // all 1024 windows match: a contiguous arithmetic run
         const uint64_t lim = e.cap > run ? e.cap - run : 0;
-        if (run + kChunk <= e.cap && (run & 1) == 0) {
-          int64_t* o = e.out + run;
+        int64_t* o = e.out + run;
+        if (run + kChunk <= e.cap && ((uintptr_t)o & 15u) == 0) {  // 16-byte stores
 #pragma unroll 4
           for (int i = 2 * lane; i < kChunk; i += 64) st_global_v2(o + i, chunk0 + i, chunk0 + i + 1);
         } else {

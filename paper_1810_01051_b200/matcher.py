@@ -109,6 +109,58 @@ def search_sequential(text, pattern, stats: ScanStats | None = None) -> MatchRes
     return MatchResult(n, m, _to_list(offsets))
 
 
+def search_each(text, patterns, stats: ScanStats | None = None) -> list[MatchResult]:
+    """``[search_sequential(text, p, stats) for p in patterns]`` -- the reference CLI's
+    per-pattern loop over a pattern file (cli.py:105-118) -- with a host text crossing
+    PCIe once for all of them (rk_scan_host_batch: the text lands chunk by chunk and every
+    pattern's windows are scanned as their bytes arrive).  Patterns keep their order and
+    duplicates (unlike search_multi's PatternSet); validation is search_sequential's, in
+    the same order, before any device work; ``stats`` accumulates over all patterns."""
+    t = _scan.as_u8(text)
+    pats = [_scan._host_bytes(_scan.as_u8(p)) for p in patterns]
+    for p in pats:
+        if p.size == 0:
+            raise ValueError("empty pattern")
+    n = _scan._size(t)
+    if _scan._device_of(t) is not None or not pats:
+        return [search_sequential(t, p, stats) for p in pats]
+    host = _scan._host_bytes(t)
+    L = _lib.lib()
+    out: list[MatchResult] = []
+    for a in range(0, len(pats), _lib.BATCH_MAX_PATTERNS):
+        batch = pats[a:a + _lib.BATCH_MAX_PATTERNS]
+        P = len(batch)
+        flat = np.concatenate(batch)
+        lengths = np.array([p.size for p in batch], dtype=np.uint32)
+        hashes = np.array([hash_full(p.tobytes()) for p in batch], dtype=np.uint64)
+        mt = np.zeros(P, dtype=np.uint64)
+        co = np.zeros(P, dtype=np.uint64)
+        hh = np.zeros(P, dtype=np.uint64)
+        cap = 1 << 16
+        offs = np.empty(cap, dtype=np.int64)
+        with _lib.acquire() as ctx:
+            _lib.check(L.rk_scan_host_batch(ctx.handle, _scan._ptr(host), n, flat.ctypes.data,
+                                            lengths.ctypes.data, hashes.ctypes.data, P,
+                                            offs.ctypes.data, cap, mt.ctypes.data,
+                                            co.ctypes.data, hh.ctypes.data))
+            total = int(mt.sum())
+            if total > cap:
+                offs = np.empty(total, dtype=np.int64)
+                _lib.check(L.rk_scan_host_fetch(ctx.handle, offs.ctypes.data, 0, total))
+        at = 0
+        for i, p in enumerate(batch):
+            k = int(mt[i])
+            m = int(p.size)
+            nw = n - m + 1
+            out.append(MatchResult(n, m, offs[at:at + k].tolist() if nw > 0 else []))
+            at += k
+            if stats is not None and nw > 0:
+                stats.windows += nw
+                stats.hash_hits += int(hh[i])
+                stats.collisions += int(co[i])
+    return out
+
+
 def search_bitmap(text, pattern, stats: ScanStats | None = None):
     """search_sequential(text, pattern).to_bitmap() computed on the device without the
     offset list (matcher.py:36-42 + :101-122): a bool array/tensor with one entry per

@@ -474,3 +474,31 @@ def test_bitmap_output(gpu):
     bm = rk.search_bitmap(b"abab", b"ab", stats=st)
     assert bm.tolist() == rk.MatchResult(4, 2, [0, 2]).to_bitmap().tolist()
     assert st == rk.ScanStats(3, 2, 0)
+
+
+def test_search_each_host_batch(gpu):
+    """search_each (rk_scan_host_batch: the host text crosses PCIe once) equals
+    search_sequential per pattern, with duplicates, lengths > n, a pattern whose hash no
+    window can reach, dense patterns overflowing their first slot, and stats."""
+    rng = np.random.default_rng(17)
+    n = (130 << 20) + 12345  # 3 staging chunks, ragged
+    text = rng.integers(0, 4, n, dtype=np.uint8)
+    text[5 << 20: (5 << 20) + 300000] = 0  # a dense run: 'AAAA'-style overflow
+    pats = [text[x:x + m].tobytes() for x, m in ((1000, 4), (77777, 8), (3 << 20, 16),
+                                                  (100 << 20, 32), (129 << 20, 1024))]
+    pats += [bytes(4), pats[1], b"\xff" * 20, bytes(range(200, 230)), b"x" * (n + 1)]
+    st = rk.ScanStats()
+    got = rk.search_each(text, pats, stats=st)
+    st2 = rk.ScanStats()
+    for p, r in zip(pats, got):
+        e = rk.search_sequential(text, p, stats=st2)
+        assert r == e, len(p)
+    assert (st.windows, st.hash_hits, st.collisions) == (st2.windows, st2.hash_hits, st2.collisions)
+    assert len(got[5].offsets) > (1 << 16)  # the overflowing pattern
+    # pageable bytes and a pinned tensor view take the same path
+    import torch
+
+    pinned = torch.from_numpy(text).pin_memory()
+    assert rk.search_each(pinned.numpy(), pats[:3]) == got[:3]
+    assert rk.search_each(text.tobytes()[: 1 << 20], [pats[0]]) == \
+        [rk.search_sequential(text.tobytes()[: 1 << 20], pats[0])]
