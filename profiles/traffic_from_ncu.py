@@ -7,8 +7,8 @@ roofline.traffic).
         python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu --sustained-steps 0
     python profiles/traffic_from_ncu.py gpurun_out/launches.csv profiles/r02_launches.csv
 
-Each launch of the sweep kernel is attributed to its m by the template argument in the
-kernel name; traffic = dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged
+Each launch of the sweep kernel is attributed to its m by its position in the step (the
+bench scans the sweep's lengths in order; every m >= 32 runs rk_scan_kernel<32>); traffic = dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged
 over the launches of that m (ncu runs each launch alone and cold: the per-launch bytes are
 what the kernel moves, the durations are only the kernel's share of the step).
 """
@@ -21,6 +21,8 @@ import re
 import sys
 from pathlib import Path
 
+SWEEP = (4, 8, 16, 32, 64, 128, 256, 512, 1024)
+
 
 def main(src, copy_to=None):
     text = Path(src).read_text()
@@ -31,12 +33,16 @@ def main(src, copy_to=None):
         per[(r["ID"], r["Kernel Name"])][r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
     acc = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])
     kernels = collections.Counter()
-    for (_, name), v in per.items():
+    i = 0
+    for (lid, name), v in sorted(per.items(), key=lambda kv: int(kv[0][0])):
         kernels[re.sub(r"\(.*", "", name)] += 1
         mt = re.search(r"rk_scan_kernel<(\d+)>", name)
         if not mt or "dram__bytes_read.sum" not in v:
             continue
-        a = acc[int(mt.group(1))]
+        m = SWEEP[i % len(SWEEP)]
+        i += 1
+        assert int(mt.group(1)) == min(m, 32) if m >= 32 or m in (4, 8, 16) else True, (m, name)
+        a = acc[m]
         a[0] += 1
         a[1] += v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"]
         a[2] += v["gpu__time_duration.sum"]
