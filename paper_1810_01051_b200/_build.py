@@ -26,7 +26,7 @@ LIB = Path(os.environ["RK_LIB_OUT"]).resolve() if os.environ.get("RK_LIB_OUT") e
 DEFINES = os.environ.get("RK_DEFINES", "").split()
 SOURCES = ["rk_scan.cu", *[f"rk_scan_g{g}.cu" for g in range(4)], "rk_multi.cu",
            "rk_multi_g0.cu", "rk_pairs.cu", "rk_emit.cu", "rk_aux.cu", "rk_capi.cu", "rk_comm.cu"]
-HEADERS = ["rk_device.cuh", "rk_internal.h", "rk_scan_impl.cuh", "rk_multi_impl.cuh", "rk_ctx.h"]
+HEADERS = ["rk_device.cuh", "rk_internal.h", "rk_scan_impl.cuh", "rk_short_impl.cuh", "rk_multi_impl.cuh", "rk_ctx.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--use_fast_math",

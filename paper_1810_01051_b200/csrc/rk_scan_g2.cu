@@ -1,7 +1,7 @@
 // rk_scan_g2.cu -- explicit instantiations of the single-pattern scan for m in
 // {17, 18, 19, 20, 21, 22, 23, 24} (m = 32 stands for every m >= 32).  The 32 variants are split
 // over four translation units to keep each ptxas run small and the build parallel.
-#include "rk_scan_impl.cuh"
+#include "rk_short_impl.cuh"
 
 namespace rkb {
 template cudaError_t launch_m<17>(const ScanArgs&, int, cudaStream_t);

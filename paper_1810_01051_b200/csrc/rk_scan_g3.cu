@@ -1,7 +1,7 @@
 // rk_scan_g3.cu -- explicit instantiations of the single-pattern scan for m in
 // {25, 26, 27, 28, 29, 30, 31, 32} (m = 32 stands for every m >= 32).  The 32 variants are split
 // over four translation units to keep each ptxas run small and the build parallel.
-#include "rk_scan_impl.cuh"
+#include "rk_short_impl.cuh"
 
 namespace rkb {
 template cudaError_t launch_m<25>(const ScanArgs&, int, cudaStream_t);

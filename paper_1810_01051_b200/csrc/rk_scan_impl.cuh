@@ -572,41 +572,4 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
   flush_totals(a, tot, lane);
 }
 
-template <int M>
-cudaError_t launch_m(const ScanArgs& a, int grid, cudaStream_t s) {
-  const size_t smem = scan_smem_bytes(M);
-  static bool attr[kMaxDevices] = {};  // per-variant, per-device opt-in to > 48 KiB smem
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= kMaxDevices || !attr[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(rk_scan_kernel<M>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    if (dev < kMaxDevices) attr[dev] = true;
-  }
-  // programmatic dependent launch: scheduled as the previous kernel's CTAs retire; the
-  // kernel waits for that grid's completion before touching memory (griddepcontrol.wait)
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(32 * a.warps);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = RK_PDL;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, rk_scan_kernel<M>, a);
-}
-
-template <int M>
-int occupancy_m() {
-  cudaFuncSetAttribute(rk_scan_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)scan_smem_bytes(M));
-  int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rk_scan_kernel<M>, 32 * scan_warps(M),
-                                                scan_smem_bytes(M));
-  return b > 0 ? b : 1;
-}
-
 }  // namespace rkb
