@@ -59,10 +59,28 @@ constexpr uint32_t kWideFrom = RK_WIDE_FROM;  // first m with the wide shape
 // measured per length (tools/ab.sh): m = 8 likes 20 warps in one CTA, m = 5..7 two CTAs
 // of 8 warps (the two dependent dp4a per window want warps; the cooperative settle's
 // chunk-end ballots want smaller CTAs)
+// short-pattern shapes (warps, stage chunks, CTAs per SM); separate macros because nvcc
+// splits -D values at commas
+#ifndef RK_S8_W
+#define RK_S8_W 20
+#define RK_S8_S 4
+#define RK_S8_B 1
+#endif
+#ifndef RK_S57_W
+#define RK_S57_W 20  // (measured: 8 x 2 CTAs 5121 / 4921 / 5280 GB/s at m = 5 / 6 / 7,
+#define RK_S57_S 4   //  12 x 2 5312 / 5081 / 5609, 20 x 1 5361 / 5169 / 5556)
+#define RK_S57_B 1
+#endif
+#ifndef RK_S34_W
+#define RK_S34_W RK_BASE_W
+#define RK_S34_S RK_BASE_S
+#define RK_S34_B RK_BASE_B
+#endif
 __host__ __device__ constexpr ScanShape scan_shape(uint32_t m) {
   return m >= kWideFrom ? ScanShape{RK_WIDE_W, RK_WIDE_S, RK_WIDE_B}
-         : m == 8       ? ScanShape{20, 4, 1}
-         : (m >= 5 && m <= 7) ? ScanShape{8, 4, 2}
+         : m == 8       ? ScanShape{RK_S8_W, RK_S8_S, RK_S8_B}
+         : (m >= 5 && m <= 7) ? ScanShape{RK_S57_W, RK_S57_S, RK_S57_B}
+         : (m >= 3 && m <= 4) ? ScanShape{RK_S34_W, RK_S34_S, RK_S34_B}
                               : ScanShape{RK_BASE_W, RK_BASE_S, RK_BASE_B};
 }
 __host__ __device__ constexpr int scan_warps(uint32_t m) { return scan_shape(m).warps; }

@@ -75,6 +75,12 @@ __device__ __forceinline__ void lds_chunk(uint32_t p, uint32_t& lb6, uint32_t& l
                : "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]), "=r"(v.w[7]) : "r"(p + 48));
 }
 
+// acc += p, as one predicated add
+__device__ __forceinline__ void add_if(uint32_t& acc, bool p) {
+  asm("{.reg .pred q;\n setp.ne.b32 q, %1, 0;\n @q add.u32 %0, %0, 1;}"
+      : "+r"(acc) : "r"((uint32_t)p));
+}
+
 template <int M>
 __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
     rk_short_kernel(const ScanArgs a) {
@@ -157,71 +163,57 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
             anyf |= f[j];
           }
         }
-        if (sd || anyf) {
-          // the stage's chunks to settle, as a bit mask (all of them in dense mode)
-          uint32_t cm = 0;
+        // settle: flagged chunks of a full tile with few flagged lanes cooperatively, in
+        // the unrolled order (no dynamic selection of f[j]); dense chunks, dense mode and
+        // partial tiles per lane, in one rolled loop (one copy of that code)
+        uint32_t im = sd ? (1u << SC) - 1u : 0u;
+        if (!sd && anyf) {
 #pragma unroll
-          for (int j = 0; j < SC; ++j) cm |= (sd || f[j]) ? 1u << j : 0u;
-#pragma unroll 1
-          while (cm) {
-            const int j = __ffs(cm) - 1;
-            cm &= cm - 1;
-            uint32_t flags = f[0];
-#pragma unroll
-            for (int jj = 1; jj < SC; ++jj) flags = j == jj ? f[jj] : flags;
-            if (sd) flags = kFull;
-            const int c = s * SC + j;
-            if (sd || __popc(flags) > kShortCoopLanes) {
-              // dense chunk: per-lane settle from registers
-              uint32_t lb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-              Vec32 v;
-              lds_chunk(stage_p + (uint32_t)j * kChunk, lb[6], lb[7], v);
-              inline_settle(v, lb, ta + c * kChunk + lane * kR, c);
+          for (int j = 0; j < SC; ++j) {
+            uint32_t flags = f[j];
+            if (!flags) continue;
+            if (!full || __popc(flags) > kShortCoopLanes) {
+              im |= 1u << j;
               continue;
             }
-            // cooperative settle of the flagged lanes, from the stage in shared memory
+            const int c = s * SC + j;
             const uint32_t base = settle_s + slot_off + (uint32_t)j * kChunk;
             uint32_t hm = 0;
-            const auto settle = [&](auto full_tag) {
-              constexpr bool kAllValid = decltype(full_tag)::value;
-              uint32_t vlo = 0, vspan = kChunk;
-              if constexpr (!kAllValid) {
-                const int64_t J0 = ta + c * kChunk;
-                vlo = (uint32_t)min(max((int64_t)g.ja_lo - J0, (int64_t)0), (int64_t)kChunk);
-                vspan = (uint32_t)min(max((int64_t)g.ja_hi - J0, (int64_t)0), (int64_t)kChunk) - vlo;
+            do {
+              const int L = __ffs(flags) - 1;
+              flags &= flags - 1;
+              const uint32_t q = base + 32u * L;
+              const uint32_t x1 = lds_u32(q + 4);
+              const uint32_t A = __funnelshift_r(lds_u32(q), x1, sr);
+              uint32_t d, B = 0;
+              if constexpr (M > 4) {
+                B = __funnelshift_r(x1, lds_u32(q + 8), sr);
+                d = __dp4a(A, W0, __dp4a(B, W1, negT));
+              } else {
+                d = __dp4a(A, W0, negT);
               }
-              do {
-                const int L = __ffs(flags) - 1;
-                flags &= flags - 1;
-                const uint32_t q = base + 32u * L;
-                const uint32_t x1 = lds_u32(q + 4);
-                const uint32_t A = __funnelshift_r(lds_u32(q), x1, sr);
-                uint32_t d, B = 0;
-                if constexpr (M > 4) {
-                  B = __funnelshift_r(x1, lds_u32(q + 8), sr);
-                  d = __dp4a(A, W0, __dp4a(B, W1, negT));
-                } else {
-                  d = __dp4a(A, W0, negT);
-                }
-                bool hit = d == 0u;
-                if constexpr (!kAllValid) hit &= (uint32_t)(kR * L + lane) - vlo < vspan;
-                const bool eq = hit & (((A ^ P0) & K0) == 0u) & (((B ^ P1) & K1) == 0u);
-                my_hits += hit;
-                my_matches += eq;
-                const unsigned em = __ballot_sync(kFull, eq);
-                hm = lane == L ? em : hm;
-              } while (flags);
-            };
-            if (full) {
-              settle(std::true_type{});
-            } else {
-              settle(std::false_type{});
-            }
+              const bool hit = d == 0u;
+              const bool eq = hit & (((A ^ P0) & K0) == 0u) & (((B ^ P1) & K1) == 0u);
+              add_if(my_hits, hit);
+              add_if(my_matches, eq);
+              const unsigned em = __ballot_sync(kFull, eq);
+              hm = lane == L ? em : hm;
+            } while (flags);
             if (__ballot_sync(kFull, hm != 0)) {
               tmask[c * 32 + lane] = hm;
               hitflags |= 1u << c;
             }
           }
+        }
+#pragma unroll 1
+        while (im) {
+          const int j = __ffs(im) - 1;
+          im &= im - 1;
+          const int c = s * SC + j;
+          uint32_t lb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          Vec32 v;
+          lds_chunk(stage_p + (uint32_t)j * kChunk, lb[6], lb[7], v);
+          inline_settle(v, lb, ta + c * kChunk + lane * kR, c);
         }
         // the slot's bytes are consumed: hand it back to the producer
         S.cslot = (S.cslot + 1) & (kStages - 1);
