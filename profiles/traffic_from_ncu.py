@@ -36,7 +36,7 @@ def main(src, copy_to=None):
     i = 0
     for (lid, name), v in sorted(per.items(), key=lambda kv: int(kv[0][0])):
         kernels[re.sub(r"\(.*", "", name)] += 1
-        mt = re.search(r"rk_scan_kernel<(\d+)>", name)
+        mt = re.search(r"rk_(?:scan|short)_kernel<(\d+)>", name)
         if not mt or "dram__bytes_read.sum" not in v:
             continue
         m = SWEEP[i % len(SWEEP)]
