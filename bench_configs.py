@@ -145,6 +145,51 @@ def c3_mixed(reps, n=4 << 30, P=1024):
             "note": "rk_multi_scan_mixed incl. table build + host ordering of the pairs"}
 
 
+def c3_dense(reps, n=64 << 20, lengths=(4, 5, 6)):
+    """Dense multi-pattern output: all 'a' with {'aaaa', 'aaaaa', 'aaaaaa'} (every window of
+    every length matches: ~3n (offset, index) pairs through rk_multi_scan_mixed, the ordered
+    device sort included).  Parity: each pattern's list is range(n - m + 1)."""
+    import torch
+
+    import paper_1810_01051_b200 as rk
+    from paper_1810_01051_b200 import _lib
+
+    t = torch.full((n,), 97, dtype=torch.uint8, device="cuda")
+    pats = [b"a" * m for m in lengths]
+    flat = np.frombuffer(b"".join(pats), dtype=np.uint8)
+    lens = np.array(lengths, dtype=np.uint32)
+    hashes = np.array([rk.hash_full(p) for p in pats], dtype=np.uint64)
+    total = sum(n - m + 1 for m in lengths)
+    off = torch.empty(total, dtype=torch.int64, device="cuda")
+    idx = torch.empty(total, dtype=torch.int32, device="cuda")
+    pairs = _lib.u64ref()
+    ctx = _lib.context()
+    L = _lib.lib()
+    s = torch.cuda.current_stream()
+
+    def run():
+        _lib.check(L.rk_multi_scan_mixed(ctx.handle, t.data_ptr(), n, flat.ctypes.data,
+                                         lens.ctypes.data, len(pats), hashes.ctypes.data,
+                                         off.data_ptr(), idx.data_ptr(), total,
+                                         ctypes.byref(pairs), s.cuda_stream))
+
+    before = ctx.launches
+    run()
+    sweeps = ctx.launches - before
+    ms = timed(run, reps, s)
+    assert int(pairs.value) == total
+    at = 0
+    for i, m in enumerate(lengths):
+        k = n - m + 1
+        assert torch.equal(idx[at:at + k], torch.full((k,), i, dtype=torch.int32, device="cuda"))
+        assert torch.equal(off[at:at + k], torch.arange(k, device="cuda"))
+        at += k
+    return {"config": "C3dense", "bytes": n, "lengths": list(lengths), "pairs": total,
+            "launches": sweeps, "ms": ms, "GBps_text": n / ms / 1e6,
+            "Mpairs_per_s": total / ms / 1e3,
+            "note": "all 'a', every window of every length matches; parity checked on device"}
+
+
 def c4(reps, n=16 << 30, m=32):
     import torch
 
@@ -210,6 +255,8 @@ def main():
            # not a BASELINE config: C3's shape over DNA (low-entropy q-grams)
            "C3dna": lambda r: c3(r, m=32, alphabet=b"ACGT", tag="C3dna"),
            "C3mixed": c3_mixed,
+           "C3dense": c3_dense,
+           "C3short6": lambda r: c3(r, m=6, tag="C3short6"),
            "C3short": lambda r: c3(r, m=5, tag="C3short"),
            "C3short4": lambda r: c3(r, m=4, tag="C3short4")}
     for name in args.only.split(","):

@@ -150,7 +150,8 @@ int rk_multi_scan(rk_ctx_t* ctx, const uint8_t* d_text, uint64_t n, const uint8_
  * h_patterns holds the P deduplicated patterns back to back, pattern i being
  * h_lengths[i] bytes; pair indices are positions in this list.  Lengths >= 7 share one
  * sweep over the text per 64 distinct lengths (the reference runs one pass per length,
- * matcher.py:139-153); each length < 7 gets its own sweep.  Patterns longer than the text
+ * matcher.py:139-153); the lengths 4..6 share one more sweep and 1..3 another (at most
+ * two for all lengths < 7).  Patterns longer than the text
  * have no windows.  Output and ordering as rk_multi_scan.
  */
 int rk_multi_scan_mixed(rk_ctx_t* ctx, const uint8_t* d_text, uint64_t n,

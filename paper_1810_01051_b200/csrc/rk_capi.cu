@@ -533,86 +533,98 @@ int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, 
       const uint32_t bit = (r.first * 0x9E3779B1u) >> 16;
       filter[bit >> 5] |= 1u << (bit & 31);
     }
-    if (m < 7) {
-      // cuckoo table of the packed patterns (index in the top 16 bits), 2 slots per key
-      std::vector<uint64_t> key(b.P);
-      for (uint32_t i = 0; i < b.P; ++i) {
-        uint64_t k = 0;
-        memcpy(&k, h_patterns + first_byte[members[i]], m);
-        key[i] = k;
-      }
-      std::vector<uint64_t> slots;
-      TinyHash th{};
-      bool ok = false;
-      for (uint32_t size = 64; !ok && size <= kTinySlotsMax; size <<= 1) {
-        if (size < 2 * b.P) continue;
-        uint32_t lg = 0;
-        while ((1u << lg) < size) ++lg;
-        for (uint32_t seed = 0; !ok && seed < 64; ++seed) {
-          th.c1 = 0x9E3779B1u + 0x6A09E667u * seed;
-          th.c2 = 0x85EBCA77u ^ (0xBB67AE85u * seed);
-          th.c3 = 0xC2B2AE3Du + 0x3C6EF372u * seed;
-          th.c1 |= 1u;
-          th.c3 |= 1u;
-          th.shift = 32 - lg;
-          th.size = size;
-          slots.assign(size, ~0ull);
-          ok = true;
-          for (uint32_t i = 0; i < b.P && ok; ++i) {
-            uint64_t cur = key[i] | ((uint64_t)members[i] << 48);
-            uint32_t s1, s2;
-            tiny_slots(tiny_key_hash((uint32_t)cur, (uint32_t)(cur >> 32) & 0xffffu, th), th, s1,
-                       s2);
-            uint32_t at = s1;
-            for (int kick = 0; kick < 500; ++kick) {
-              std::swap(cur, slots[at]);
-              if (cur == ~0ull) break;
-              tiny_slots(tiny_key_hash((uint32_t)cur, (uint32_t)(cur >> 32) & 0xffffu, th), th,
-                         s1, s2);
-              at = (at == s1) ? s2 : s1;
-              if (kick == 499) ok = false;
-            }
-          }
-        }
-      }
-      if (!ok) return fail(RK_ECUDA, "cannot build the short-pattern table");
-      b.tiny_hash = th;
-      b.tiny = reserve((uint64_t)th.size * 8 + kTinyFilterBytes);
-      memcpy(blob.data() + b.tiny, slots.data(), (uint64_t)th.size * 8);
-      uint32_t* filt = reinterpret_cast<uint32_t*>(blob.data() + b.tiny + (uint64_t)th.size * 8);
-      if ((int)m >= kTinyAnchorFrom) {
-        // anchored q-grams: an occurrence at y holds the q-gram ending at the first anchor
-        // e >= y + q - 1 (anchors every 2 bytes), i.e. p[j:j+q] with j in {0, 1}
-        const int q = tiny_gram_q((int)m);
-        for (uint32_t i = 0; i < b.P; ++i) {
-          for (int j = 0; j < 2; ++j) {
-            uint32_t gram = 0;
-            memcpy(&gram, h_patterns + first_byte[members[i]] + j, q);
-            const uint32_t h = gram * kGramMul;
-            uint32_t* blk = filt + 2 * (h >> 21);
-            blk[0] |= 1u << ((h >> 16) & 31);
-            blk[1] |= 1u << ((h >> 11) & 31);
-          }
-        }
-      } else {
-        for (uint32_t i = 0; i < b.P; ++i) {
-          const uint32_t f = tiny_key_hash((uint32_t)key[i], (uint32_t)(key[i] >> 32), th);
-          uint32_t* blk = filt + 2 * (f >> kTinyFilterShift);
-          const uint32_t q = f ^ (f >> 13);
-          blk[0] |= (1u << (q & 31)) | (1u << ((q >> 5) & 31));
-          blk[1] |= (1u << ((q >> 10) & 31)) | (1u << ((q >> 15) & 31));
-        }
-      }
-    }
     plan.groups.push_back(b);
   }
 
-  // sweeps: each length < 7 alone (per-window filter); lengths >= 7 in runs of
-  // kMultiMaxGroups sharing one q-gram filter
+  // sweeps: the lengths 4..6 of the set in one anchored short sweep, 1..3 in one
+  // per-window short sweep, lengths >= 7 in runs of kMultiMaxGroups sharing one q-gram
+  // filter
   size_t gi = 0;
-  for (; gi < plan.groups.size() && plan.groups[gi].m < 7; ++gi) {
+  std::vector<uint32_t> short_sets[2];  // [0] lengths 1..3, [1] lengths 4..6
+  for (; gi < plan.groups.size() && plan.groups[gi].m < 7; ++gi)
+    short_sets[plan.groups[gi].m >= 4].push_back((uint32_t)gi);
+  for (const auto& members : short_sets) {
+    if (members.empty()) continue;
     MultiPlan::Sweep sw{};
-    sw.groups = {(uint32_t)gi};
+    sw.groups = members;
+    const uint32_t m_min = plan.groups[members.front()].m;
+    sw.sq = m_min >= 4 ? (uint32_t)short_gram_q((int)m_min) : 0u;
+    // every pattern of the sweep: (tagged key, caller index)
+    struct Entry {
+      uint32_t lo, hb, len, idx;
+    };
+    std::vector<Entry> es;
+    for (uint32_t g : members) {
+      const MultiPlan::Group& b = plan.groups[g];
+      for (uint32_t i = 0; i < b.P; ++i) {
+        Entry e{0, 0, b.m, 0};
+        const uint8_t* pb = blob.data() + b.pats + (uint64_t)i * b.m;
+        memcpy(&e.lo, pb, std::min<uint32_t>(b.m, 4));
+        if (b.m > 4) memcpy(&e.hb, pb + 4, b.m - 4);
+        memcpy(&e.idx, blob.data() + b.gidx + 4ull * i, 4);
+        es.push_back(e);
+      }
+    }
+    std::vector<uint64_t> slots;
+    TinyHash th{};
+    bool ok = false;
+    for (uint32_t size = 64; !ok && size <= kTinySlotsMax; size <<= 1) {
+      if (size < 2 * es.size()) continue;
+      uint32_t lg = 0;
+      while ((1u << lg) < size) ++lg;
+      for (uint32_t seed = 0; !ok && seed < 64; ++seed) {
+        th.c1 = (0x9E3779B1u + 0x6A09E667u * seed) | 1u;
+        th.c2 = 0x85EBCA77u ^ (0xBB67AE85u * seed);
+        th.c3 = (0xC2B2AE3Du + 0x3C6EF372u * seed) | 1u;
+        th.shift = 32 - lg;
+        th.size = size;
+        slots.assign(size, ~0ull);
+        ok = true;
+        for (size_t i = 0; i < es.size() && ok; ++i) {
+          uint64_t cur = short_key(es[i].lo, es[i].hb, es[i].len) | ((uint64_t)es[i].idx << 51);
+          uint32_t s1, s2;
+          const auto slots_of = [&](uint64_t v) {
+            const uint32_t lo = (uint32_t)v, hb = (uint32_t)(v >> 32) & 0xffffu;
+            const uint32_t len = (uint32_t)(v >> 48) & 7u;
+            tiny_slots(tiny_key_hash(lo, short_tag(hb, len), th), th, s1, s2);
+          };
+          slots_of(cur);
+          uint32_t at = s1;
+          for (int kick = 0; kick < 500; ++kick) {
+            std::swap(cur, slots[at]);
+            if (cur == ~0ull) break;
+            slots_of(cur);
+            at = (at == s1) ? s2 : s1;
+            if (kick == 499) ok = false;
+          }
+        }
+      }
+    }
+    if (!ok) return fail(RK_ECUDA, "cannot build the short-pattern table");
+    sw.th = th;
+    sw.stab = reserve((uint64_t)th.size * 8 + kShortFilterWords * 4);
+    memcpy(blob.data() + sw.stab, slots.data(), (uint64_t)th.size * 8);
+    uint32_t* filt = reinterpret_cast<uint32_t*>(blob.data() + sw.stab + (uint64_t)th.size * 8);
+    const auto set_bits = [&](uint32_t x) {
+      const uint32_t h = short_filter_hash(x);
+      filt[short_filter_word(h)] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31)) |
+                                    (RK_SHORT_FILTER_BITS == 3 ? 1u << ((h >> 10) & 31) : 0u);
+    };
+    for (const Entry& e : es) {
+      if (sw.sq) {
+        // the anchored q-grams p[j:j+q], j = 0, 1 (q + 1 <= m)
+        uint8_t pb[8] = {};
+        memcpy(pb, &e.lo, 4);
+        memcpy(pb + 4, &e.hb, 2);
+        for (int j = 0; j < 2; ++j) {
+          uint32_t gram = 0;
+          memcpy(&gram, pb + j, sw.sq);
+          set_bits(gram);
+        }
+      } else {
+        set_bits(tiny_key_hash(e.lo, short_tag(0u, e.len), th));
+      }
+    }
     plan.sweeps.push_back(sw);
   }
   for (; gi < plan.groups.size(); gi += kMultiMaxGroups) {
@@ -1194,8 +1206,6 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
     G.gidx = reinterpret_cast<const uint32_t*>(dev + b.gidx);
     G.table = reinterpret_cast<const uint2*>(dev + b.table);
     G.filter = reinterpret_cast<const uint32_t*>(dev + b.filter);
-    G.tiny = dev + b.tiny;
-    G.tiny_hash = b.tiny_hash;
     G.ys_hi = b.m <= n ? amis + (n - b.m + 1) : amis;  // longer than the text: no windows
     G.m = b.m;
     G.tsize = b.tsize;
@@ -1223,14 +1233,20 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
       p.qfilter = reinterpret_cast<const uint32_t*>(dev + sw.qfilter);
       p.qmap = reinterpret_cast<const uint4*>(dev + sw.qmap);
       p.qmap_size = sw.qmap_size;
-    } else if ((int)m_min >= kTinyAnchorFrom) {
-      // anchored tiny kernel: tiles over the anchors (q-gram ends, every 2 bytes) of the
-      // window starts [amis, amis + nw); window validity is checked on the starts
-      const uint64_t q = (uint64_t)tiny_gram_q((int)m_min);
-      gg.ja_lo = gg.amis + q - 1;
-      gg.ja_hi = std::min<uint64_t>(gg.amis + nw - 1 + q - 1 + 2, gg.amis + n);
-      gg.tile_first = gg.ja_lo / kTile;
-      gg.num_tiles = (gg.ja_hi - 1) / kTile - gg.tile_first + 1;
+    } else {
+      p.stab = dev + sw.stab;
+      p.th = sw.th;
+      p.sq = sw.sq;
+      if (sw.sq) {
+        // anchored short sweep: tiles over the anchors (q-gram ends, every 2 bytes) of the
+        // window starts [amis, amis + nw); window validity is checked on the starts
+        const uint64_t q = sw.sq;
+        gg.ja_lo = gg.amis + q - 1;
+        gg.ja_hi = std::min<uint64_t>(gg.amis + nw - 1 + q - 1 + 2, gg.amis + n);
+        gg.tile_first = gg.ja_lo / kTile;
+        gg.num_tiles = (gg.ja_hi - 1) / kTile - gg.tile_first + 1;
+      }
+      // (per-window short sweep: tiles over the window ends of the shortest length)
     }
     p.G = (uint32_t)sw.groups.size();
     for (size_t k = 0; k < sw.groups.size(); ++k)
@@ -1242,7 +1258,7 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
     p.cap = cap;
     p.counters = c->d_mcount;
     const uint64_t grid = std::max<uint64_t>(
-        1, std::min<uint64_t>((uint64_t)c->num_sms * multi_blocks_per_sm(p.qmode, m_min),
+        1, std::min<uint64_t>((uint64_t)c->num_sms * multi_blocks_per_sm(p),
                               (gg.num_tiles + kMultiWarps - 1) / kMultiWarps));
     RK_CUDA(launch_multi(p, (int)grid, s));
     ++c->launches;

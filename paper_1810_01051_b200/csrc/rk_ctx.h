@@ -51,8 +51,6 @@ struct MultiPlan {
   struct Group {
     uint32_t m, P, tsize;
     uint64_t pats, phash, order, gidx, table, filter;
-    uint64_t tiny = 0;  // m < 7: cuckoo table of the packed patterns
-    TinyHash tiny_hash{};
   };
   struct Sweep {
     std::vector<uint32_t> groups;  // ascending lengths
@@ -60,6 +58,10 @@ struct MultiPlan {
     uint64_t qfilter = 0;  // blob offset of the sweep's q-gram filter (qmode > 0)
     uint64_t qmap = 0;     // blob offset of its q-gram -> group-mask table
     uint32_t qmap_size = 0;
+    // short sweeps (qmode == 0, lengths < 7): cuckoo table + filter, anchored q-gram length
+    uint64_t stab = 0;
+    TinyHash th{};
+    uint32_t sq = 0;
   };
   std::vector<uint8_t> key;  // P, lengths, hashes, pattern bytes
   std::vector<Group> groups;

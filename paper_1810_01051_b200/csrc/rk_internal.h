@@ -129,36 +129,57 @@ __host__ __device__ __forceinline__ uint32_t qgram_hash(const uint32_t* w) {
   return h ^ (h >> 15);
 }
 
-// m < 7: cuckoo table of the patterns (slot = key bytes | index << 48, empty = ~0): the
-// two slots of a key of low word lo and high word hi (bytes 4..5), for the same
-// function on the host (build) and the device (lookup).
+// Lengths < 7 (rk_multi_short_kernel): a window of length L <= 6 is its own exact key.
+// One sweep takes every such length of a set (lengths 4..6 in one "anchored" sweep,
+// lengths 1..3 in one per-window sweep); its patterns sit in ONE cuckoo table keyed by
+// (bytes, length): slot = bytes (48 bits) | L << 48 (3 bits) | caller index << 51
+// (12 bits), empty = ~0.  The two slots of a key come from tiny_key_hash of the low word
+// and the tagged high word (bytes 4..5 | L << 16), for the same function on the host
+// (build) and the device (lookup).
 struct TinyHash {
   uint32_t c1, c2, c3;  // seeds (the host retries others if an insertion cycles)
   uint32_t shift;       // 32 - log2(size)
   uint32_t size;        // slots, a power of two
 };
-// anchored q-gram filter (m >= kTinyAnchorFrom), a blocked Bloom filter of 2048 64-bit
-// blocks: h = gram * kGramMul, block = h >> 21, bit h >> 16 (mod 32) of its low word and
-// bit h >> 11 (mod 32) of its high word.  (Shifts by IMAD.HI on the FMA pipe measured
-// slower than SHF, here and in the q-gram kernel.)
-// m >= this: the tiny kernel tests one anchored q-gram per 2 bytes (q = 3 for m = 4, else
-// 4; q + s - 1 <= m) instead of every window's key
-constexpr int kTinyAnchorFrom = 4;
-constexpr uint32_t kGramMul = 0x9E3779B1u;
-__host__ __device__ constexpr int tiny_gram_q(int m) { return m == 4 ? 3 : 4; }
-
-constexpr uint32_t kTinySlotsMax = 8192;             // 64 KiB of shared memory
-constexpr uint32_t kTinyFilterBytes = (1u << 17) / 8;  // 2^17-bit key filter, 16 KiB
-constexpr uint32_t kTinyFilterShift = 32 - 11;         // 64-bit block: top 11 bits of f
-__host__ __device__ __forceinline__ uint32_t tiny_key_hash(uint32_t lo, uint32_t hi,
+constexpr uint32_t kTinySlotsMax = 8192;  // 64 KiB of shared memory (2 slots per pattern)
+constexpr uint64_t kShortKeyMask = (1ull << 51) - 1;  // bytes + length
+__host__ __device__ __forceinline__ uint32_t short_tag(uint32_t hi_bytes, uint32_t len) {
+  return hi_bytes | (len << 16);
+}
+__host__ __device__ __forceinline__ uint64_t short_key(uint32_t lo, uint32_t hi_bytes,
+                                                       uint32_t len) {
+  return (uint64_t)lo | ((uint64_t)hi_bytes << 32) | ((uint64_t)len << 48);
+}
+__host__ __device__ __forceinline__ uint32_t tiny_key_hash(uint32_t lo, uint32_t tag,
                                                            const TinyHash& t) {
-  return lo * t.c1 + hi * t.c2;
+  return lo * t.c1 + tag * t.c2;
 }
 __host__ __device__ __forceinline__ void tiny_slots(uint32_t f, const TinyHash& t, uint32_t& s1,
                                                     uint32_t& s2) {
   s1 = f >> t.shift;
   s2 = ((f ^ (f >> 15)) * t.c3) >> t.shift;
 }
+// The sweep's Bloom filter: 4096 32-bit words (16 KiB).  An entry x (an anchored q-gram's
+// bytes as a little-endian word, or a per-window sweep's tiny_key_hash) is mixed as
+// h = umulhi(x * kGramMul, kFiltMix) and sets bits h, h >> 5 and h >> 10 (mod 32) of word
+// h >> 20: one 32-bit shared-memory load per test, three bits (false positives ~1e-4 at
+// 2048 entries).  The mixing multiplies run on the FMA pipe and leave the bit positions in
+// the low bits, where the test's rotates take them without masking.
+constexpr uint32_t kShortFilterWords = 4096;
+constexpr uint32_t kGramMul = 0x9E3779B1u;
+#ifndef RK_SHORT_FILTER_BITS
+#define RK_SHORT_FILTER_BITS 3  // (measured: 3 bits 2089 GB/s at 1024 x m = 5, 2 bits 1840)
+#endif
+__host__ __device__ __forceinline__ uint32_t short_filter_hash(uint32_t x) {
+  // both halves of the 64-bit product: every bit depends on every input bit
+  const uint64_t p = (uint64_t)x * kGramMul;
+  return (uint32_t)p + (uint32_t)(p >> 32);
+}
+__host__ __device__ __forceinline__ uint32_t short_filter_word(uint32_t h) { return h >> 20; }
+// anchored sweeps: anchors every 2 bytes, q-gram length q = 3 when the sweep has length 4
+// (q + 2 - 1 <= m), else 4; an occurrence at y holds the q-gram ending at the first anchor
+// e >= y + q - 1, i.e. p[j:j+q] with j in {0, 1}
+__host__ __device__ constexpr int short_gram_q(int m_min) { return m_min == 4 ? 3 : 4; }
 
 // One length group of a multi-pattern launch (all arrays device-resident).
 struct MultiGroup {
@@ -168,8 +189,6 @@ struct MultiGroup {
   const uint32_t* gidx;    // group-local index -> the caller's pattern index
   const uint2* table;      // tsize entries: {key, (first << 13) | count}, y = empty marker
   const uint32_t* filter;  // kMultiFilterWords words over the low-32 keys
-  const uint8_t* tiny;     // m < 7: the cuckoo table (see rk_multi_tiny_kernel)
-  TinyHash tiny_hash;
   uint64_t ys_hi;          // one past the last window start with room for m bytes (a-space)
   uint32_t m, tsize, P;
 };
@@ -195,12 +214,17 @@ struct MultiArgs {
   unsigned long long* counters;  // [0] = pairs found
   const uint4* qmap;             // q-gram hash -> length-group mask (qmode > 0)
   uint32_t qmap_size;            // entries, a power of two
-  uint32_t G;                    // length groups in grp (1 when qmode == 0)
+  uint32_t G;                    // length groups in grp
+  // short sweeps (qmode == 0): the sweep's cuckoo table (tsize slots) followed by its
+  // filter (kShortFilterWords words), and the anchored q-gram length (0: per window)
+  const uint8_t* stab;
+  TinyHash th;
+  uint32_t sq;
   MultiGroup grp[kMultiMaxGroups];
 };
 size_t multi_smem_bytes();
-size_t multi_tiny_smem_bytes();
-int multi_blocks_per_sm(uint32_t qmode, uint32_t m);
+size_t multi_short_smem_bytes(uint32_t slots);
+int multi_blocks_per_sm(const MultiArgs& a);
 cudaError_t launch_multi(const MultiArgs& a, int grid, cudaStream_t s);
 
 // device ordering of (pattern index, offset) pairs (rk_pairs.cu)

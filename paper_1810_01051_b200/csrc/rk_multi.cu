@@ -1,5 +1,5 @@
-// rk_multi.cu -- dispatch of the multi-pattern scan kernels (m < 7 variants instantiated
-// in rk_multi_g0.cu; kernels in rk_multi_impl.cuh).
+// rk_multi.cu -- dispatch of the multi-pattern scan kernels (the short-length variants
+// instantiated in rk_multi_g0.cu; kernels in rk_multi_impl.cuh).
 #include "rk_multi_impl.cuh"
 
 namespace rkb {
@@ -32,37 +32,40 @@ __global__ void __launch_bounds__(kMultiBlock) rk_multi_qgram_kernel(const __gri
   }
 }
 
-template <int M>
-cudaError_t launch_multi_tiny(const MultiArgs& a, int grid, cudaStream_t s);
-template <int M>
-int multi_tiny_occupancy();
-
-using MultiLaunchFn = cudaError_t (*)(const MultiArgs&, int, cudaStream_t);
-using MultiOccFn = int (*)();
-static constexpr MultiLaunchFn kTinyLaunch[6] = {
-    &launch_multi_tiny<1>, &launch_multi_tiny<2>, &launch_multi_tiny<3>,
-    &launch_multi_tiny<4>, &launch_multi_tiny<5>, &launch_multi_tiny<6>};
-static constexpr MultiOccFn kTinyOcc[6] = {
-    &multi_tiny_occupancy<1>, &multi_tiny_occupancy<2>, &multi_tiny_occupancy<3>,
-    &multi_tiny_occupancy<4>, &multi_tiny_occupancy<5>, &multi_tiny_occupancy<6>};
+template <int Q>
+cudaError_t launch_multi_short(const MultiArgs& a, int grid, cudaStream_t s);
+template <int Q>
+int multi_short_occupancy(size_t smem);
 
 size_t multi_smem_bytes() {
   return sizeof(MultiRing) * kMultiWarps + kQFilterWords * sizeof(uint32_t);
 }
 
-size_t multi_tiny_smem_bytes() {  // rings + the largest cuckoo table
-  return sizeof(MultiRing) * kMultiWarps + kTinySlotsMax * 8u + kTinyFilterBytes;
+size_t multi_short_smem_bytes(uint32_t slots) {  // rings + the sweep's cuckoo table + filter
+  return sizeof(MultiRing) * kMultiWarps + slots * 8u + kShortFilterWords * 4u;
 }
 
-int multi_blocks_per_sm(uint32_t qmode, uint32_t m) {
-  if (qmode == 0) return kTinyOcc[m - 1]();
+int multi_blocks_per_sm(const MultiArgs& a) {
+  if (a.qmode == 0) {
+    static int occ[kTinySlotsMax * 2] = {};  // per table size (a power of two)
+    const uint32_t k = a.th.size;
+    if (!occ[k]) {
+      const size_t smem = multi_short_smem_bytes(k);
+      occ[k] = a.sq == 3 ? multi_short_occupancy<3>(smem)
+               : a.sq == 4 ? multi_short_occupancy<4>(smem) : multi_short_occupancy<0>(smem);
+    }
+    return occ[k];
+  }
   static int occ = 0;  // same on every B200
   if (!occ) occ = multi_occupancy(rk_multi_qgram_kernel, multi_smem_bytes());
   return occ;
 }
 
 cudaError_t launch_multi(const MultiArgs& a, int grid, cudaStream_t s) {
-  if (a.qmode == 0) return kTinyLaunch[a.g.m - 1](a, grid, s);
+  if (a.qmode == 0) {
+    return a.sq == 3 ? launch_multi_short<3>(a, grid, s)
+           : a.sq == 4 ? launch_multi_short<4>(a, grid, s) : launch_multi_short<0>(a, grid, s);
+  }
   return multi_launch_kernel<struct QgramAttr>(rk_multi_qgram_kernel, a, grid,
                                                multi_smem_bytes(), s);
 }

@@ -1,33 +1,44 @@
-// rk_multi_g0.cu -- explicit instantiations of the m < 7 multi-pattern kernels.
+// rk_multi_g0.cu -- explicit instantiations of the short-length (m < 7) multi-pattern
+// kernel: anchored q-grams of 3 or 4 bytes, or per-window keys (Q = 0).
 #include "rk_multi_impl.cuh"
 
 namespace rkb {
 
-template <int M>
-struct rk_multi_tiny_tag {};
+template <int Q>
+struct rk_multi_short_tag {};
 
-template <int M>
-cudaError_t launch_multi_tiny(const MultiArgs& a, int grid, cudaStream_t s) {
-  return multi_launch_kernel<rk_multi_tiny_tag<M>>(rk_multi_tiny_kernel<M>, a, grid,
-                                                   multi_tiny_smem_bytes(), s);
+template <int Q>
+cudaError_t launch_multi_short(const MultiArgs& a, int grid, cudaStream_t s) {
+  // the dynamic shared memory follows the sweep's table size; the opt-in covers the largest
+  static bool attr[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= kMaxDevices || !attr[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(rk_multi_short_kernel<Q>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)multi_short_smem_bytes(kTinySlotsMax));
+    if (e != cudaSuccess) return e;
+    if (dev < kMaxDevices) attr[dev] = true;
+  }
+  rk_multi_short_kernel<Q><<<grid, kMultiBlock, multi_short_smem_bytes(a.th.size), s>>>(a);
+  return cudaGetLastError();
 }
 
-template <int M>
-int multi_tiny_occupancy() {
-  return multi_occupancy(rk_multi_tiny_kernel<M>, multi_tiny_smem_bytes());
+template <int Q>
+int multi_short_occupancy(size_t smem) {
+  // (the opt-in stays at the largest table's size; only the query uses this one's)
+  cudaFuncSetAttribute(rk_multi_short_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)multi_short_smem_bytes(kTinySlotsMax));
+  int b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rk_multi_short_kernel<Q>, kMultiBlock, smem);
+  return b > 0 ? b : 1;
 }
 
-template cudaError_t launch_multi_tiny<1>(const MultiArgs&, int, cudaStream_t);
-template cudaError_t launch_multi_tiny<2>(const MultiArgs&, int, cudaStream_t);
-template cudaError_t launch_multi_tiny<3>(const MultiArgs&, int, cudaStream_t);
-template cudaError_t launch_multi_tiny<4>(const MultiArgs&, int, cudaStream_t);
-template cudaError_t launch_multi_tiny<5>(const MultiArgs&, int, cudaStream_t);
-template cudaError_t launch_multi_tiny<6>(const MultiArgs&, int, cudaStream_t);
-template int multi_tiny_occupancy<1>();
-template int multi_tiny_occupancy<2>();
-template int multi_tiny_occupancy<3>();
-template int multi_tiny_occupancy<4>();
-template int multi_tiny_occupancy<5>();
-template int multi_tiny_occupancy<6>();
+template cudaError_t launch_multi_short<0>(const MultiArgs&, int, cudaStream_t);
+template cudaError_t launch_multi_short<3>(const MultiArgs&, int, cudaStream_t);
+template cudaError_t launch_multi_short<4>(const MultiArgs&, int, cudaStream_t);
+template int multi_short_occupancy<0>(size_t);
+template int multi_short_occupancy<3>(size_t);
+template int multi_short_occupancy<4>(size_t);
 
 }  // namespace rkb

@@ -22,8 +22,8 @@
 //     group (exact hash + table + bytes), and since each window has one anchor nothing
 //     is reported twice.  (s, q) is chosen on the host from the lengths and the pattern
 //     alphabet: q up to 16 bytes so that low-entropy texts (DNA: 4^q q-grams) still filter.
-//   * m < 7 (one length per launch): the window is its own exact key, looked up in a cuckoo
-//     table of the patterns in shared memory (rk_multi_tiny_kernel).
+//   * m < 7 (lengths 4..6 in one sweep, 1..3 in another): the window is its own exact key,
+//     looked up in a cuckoo table of the patterns in shared memory (rk_multi_short_kernel).
 // Hits are appended with warp ballot/popc and one atomic per warp; the host orders them
 // by (pattern index, offset), which is exactly the reference's per-pattern ascending lists.
 #pragma once
@@ -230,84 +230,49 @@ __device__ __forceinline__ void qgram_tile(const MultiArgs& a, MultiRing* R, Str
       });
 }
 
-// m < 7: a window is at most 6 bytes, so it is its own exact key.  The set's patterns sit
-// in a cuckoo table in shared memory -- slot = key bytes | pattern index << 48, every
-// key in one of its two slots -- so a window is looked up with two 8-byte loads and no
-// loop or branch: the reference's "hash equal, then bytes equal" (matcher.py:147-153)
-// collapses into one exact comparison, since a window of this length IS its hash input.
+// ---------------------------------------------------------------------------------
+// Lengths < 7: a window of length L <= 6 is its own exact key, so the reference's
+// "hash equal, then bytes equal" (matcher.py:147-153) collapses into one exact lookup of
+// (bytes, L) in the sweep's cuckoo table in shared memory (two 8-byte loads, no loop).
 // (The rolling-hash filter of the longer lengths would pass most windows here: a 5-byte
-// hash takes ~3000 values over printable ASCII.)
+// hash takes ~3000 values over printable ASCII.)  Which windows are looked up:
+//   * anchored sweep (every length of the set in 4..6): one q-gram per 2 bytes (anchors
+//     at odd lane offsets k, the q-gram being the q bytes ending at J + k) is tested
+//     against the sweep's Bloom filter of the patterns' anchored q-grams; a passing anchor
+//     makes its two window starts candidates for every length of the sweep.  Each window
+//     has exactly one anchor, so nothing is reported twice.
+//   * per-window sweep (lengths 1..3): every window end, for every length, tests its key
+//     against the filter of the patterns' keys.
+// The fast pass only builds each lane's pass mask; candidates are then settled in warp
+// rounds -- every lane with a pending candidate takes its next one -- and appended with
+// one ballot and ONE atomic per warp per round (multi_append), so dense output (all 'a'
+// against {aaaa, aaaaa, aaaaaa}) costs a warp-wide append per round, not an atomic per
+// match.
 __device__ __forceinline__ unsigned long long ld_shared_u64(uint32_t a) {
   unsigned long long v;
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
   return v;
 }
 
-// Blocked Bloom filter of the keys: 2048 blocks of 64 bits, 4 bits per key (2 per half),
-// one LDS.64 per window; ~5e-5 false positives per window at 1024 patterns, so a group
-// of 8 windows rarely leaves the fast path.
-__device__ __forceinline__ uint32_t tiny_filter_test(uint32_t bitmap, uint32_t f) {
-  unsigned long long x = ld_shared_u64(bitmap + 8 * (f >> kTinyFilterShift));
-  const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
-  const uint32_t p = f ^ (f >> 13);  // bit positions from mixed bits, each mod 32
-  return __funnelshift_r(xl, xl, p) & __funnelshift_r(xl, xl, p >> 5) &
-         __funnelshift_r(xh, xh, p >> 10) & __funnelshift_r(xh, xh, p >> 15) & 1u;
-}
-
-// The 32 windows go in four groups of 8: one filter probe each and one predicate per
-// group; a group with a filter hit looks its passing windows up in the cuckoo table.
-template <int M>
-__device__ __forceinline__ void tiny_chunk(const MultiArgs& a, const Vec32& v,
-                                           const uint32_t (&lb)[8], int64_t J, uint32_t vmask,
-                                           uint32_t slots, uint32_t bitmap, const TinyHash& th) {
-  constexpr uint32_t K0 = M >= 4 ? 0xffffffffu : ((1u << (8 * M)) - 1u);
-  constexpr uint32_t K1 = M > 4 ? ((1u << (8 * (M - 4))) - 1u) : 0u;
-#pragma unroll
-  for (int grp = 0; grp < 4; ++grp) {
-    uint32_t lo[8], hi[8], f[8], pass = 0;
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const int s0 = 33 + grp * 8 + kk - M;  // first byte of the window, in lb ++ v
-      lo[kk] = w64(lb, v, s0) & K0;
-      hi[kk] = M > 4 ? (w64(lb, v, s0 + 4) & K1) : 0u;
-      f[kk] = tiny_key_hash(lo[kk], hi[kk], th);
-      pass |= tiny_filter_test(bitmap, f[kk]) << kk;
-    }
-    pass &= vmask >> (grp * 8);
-    if (pass & 0xffu) {
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        if ((pass >> kk) & 1u) {
-          uint32_t s1, s2;
-          tiny_slots(f[kk], th, s1, s2);
-          const unsigned long long key = ((unsigned long long)hi[kk] << 32) | lo[kk];
-          const unsigned long long e1 = ld_shared_u64(slots + 8 * s1) ^ key;
-          const unsigned long long e2 = ld_shared_u64(slots + 8 * s2) ^ key;
-          // a hit leaves only the index (< 2^12) in the top 16 bits; empty slots are ~0
-          const bool h1 = (e1 & 0xffffffffffffull) == 0 && (e1 >> 48) < 0xffffull;
-          const bool h2 = (e2 & 0xffffffffffffull) == 0 && (e2 >> 48) < 0xffffull;
-          if (h1 || h2) {
-            const unsigned long long pos = atomicAdd(&a.counters[0], 1ull);
-            if (pos < a.cap) {
-              a.out_off[pos] = J + grp * 8 + kk - M + 1 - (int64_t)a.g.amis;
-              a.out_idx[pos] = (uint32_t)((h1 ? e1 : e2) >> 48);
-            }
-          }
-        }
-      }
-    }
-  }
+// 1 iff the entry x's three bits are set in the sweep's filter (rk_internal.h)
+__device__ __forceinline__ uint32_t short_filter_test(uint32_t filt, uint32_t x) {
+  const uint32_t h = short_filter_hash(x);
+  const uint32_t w = lds_u32(filt + 4u * short_filter_word(h));
+  // rotates take the bit positions mod 32
+#if RK_SHORT_FILTER_BITS == 3
+  return __funnelshift_r(w, w, h) & __funnelshift_r(w, w, h >> 5) &
+         __funnelshift_r(w, w, h >> 10) & 1u;
+#else
+  return __funnelshift_r(w, w, h) & __funnelshift_r(w, w, h >> 5) & 1u;
+#endif
 }
 
 // 8 bytes of the text at a-space position p (the bytes of a candidate window): from the
 // TMA stage in shared memory when staged (cur = shared address of a-space position c0),
-// else from global memory with bounds checks (edge tiles, the end of a chunk).
-__device__ __forceinline__ uint2 tiny_window_bytes(const TextGeom& g, uint32_t cur, int64_t c0,
-                                                   int64_t p) {
-  // the stage holds the chunk's 32-byte lookback and its 1 KiB (a window may end up to 2
-  // bytes past the chunk: those bytes are the next chunk's, which the stage only holds
-  // when the chunk is not its last)
-  if (cur && p - c0 + 12 <= 32 + kChunk) {
+// else from global memory with bounds checks (edge tiles, the end of a stage).
+__device__ __forceinline__ uint2 short_window_bytes(const TextGeom& g, uint32_t cur, int64_t c0,
+                                                    int64_t p, uint32_t stage_bytes) {
+  if (cur && p >= c0 && p - c0 + 12 <= (int64_t)stage_bytes) {
     const uint32_t addr = cur + (uint32_t)(p - c0);
     const uint32_t al = addr & ~3u, r = 8u * (addr & 3u);
     const uint32_t x0 = lds_u32(al), x1 = lds_u32(al + 4), x2 = lds_u32(al + 8);
@@ -317,72 +282,159 @@ __device__ __forceinline__ uint2 tiny_window_bytes(const TextGeom& g, uint32_t c
   return make_uint2(edge_word(g.abase, lo, hi, p), edge_word(g.abase, lo, hi, p + 4));
 }
 
-// m in [kTinyAnchorFrom, 6]: one anchored q-gram per 2 bytes (anchors at odd lane offsets
-// k, the q-gram being the q bytes ending at J + k) is tested against a blocked Bloom
-// filter (2 bits in one 64-bit block, one LDS.64) of the patterns' anchored q-grams
-// (p[0:q], p[1:q+1]; ~0.1% false positives at 1024 patterns); a passing anchor makes its two
-// window starts (J + k - q + 1 - j, j = 0, 1) candidates, looked up exactly in the cuckoo
-// table.  Each window has exactly one anchor, so nothing is reported twice.
-template <int M>
-__device__ __forceinline__ void tiny_anchor_chunk(const MultiArgs& a, const Vec32& v,
-                                                  const uint32_t (&lb)[8], int64_t J,
-                                                  uint32_t cur, int lane, uint32_t slots,
-                                                  uint32_t bitmap, const TinyHash& th) {
-  constexpr int Q = tiny_gram_q(M);
-  constexpr uint32_t QK = Q >= 4 ? 0xffffffffu : ((1u << (8 * Q)) - 1u);
-  constexpr uint32_t K0 = M >= 4 ? 0xffffffffu : ((1u << (8 * M)) - 1u);
-  constexpr uint32_t K1 = M > 4 ? ((1u << (8 * (M - 4))) - 1u) : 0u;
-  uint32_t pass = 0;
-#pragma unroll
-  for (int t = 0; t < 16; ++t) {
-    const int k = 2 * t + 1;  // the anchor is window end J + k
-    const uint32_t h = (w64(lb, v, 33 + k - Q) & QK) * kGramMul;
-    const unsigned long long x = ld_shared_u64(bitmap + 8u * (h >> 21));
-    const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
-    pass |= (__funnelshift_r(xl, xl, h >> 16) & __funnelshift_r(xh, xh, h >> 11) & 1u) << t;
-  }
-  if (!pass) return;
-  const int64_t c0 = J - kR * lane - 32;  // a-space position of the chunk's lookback start
-  do {
-    const int t = __ffs(pass) - 1;
-    pass &= pass - 1;
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int64_t ya = J + 2 * t + 2 - Q - j;  // candidate window start, a-space
-      if (ya < (int64_t)a.ys_lo || ya >= (int64_t)a.grp[0].ys_hi) continue;
-      const uint2 w = tiny_window_bytes(a.g, cur, c0, ya);
-      const uint32_t lo = w.x & K0, hi = w.y & K1;
-      const uint32_t f = tiny_key_hash(lo, hi, th);
-      uint32_t s1, s2;
-      tiny_slots(f, th, s1, s2);
-      const unsigned long long key = ((unsigned long long)hi << 32) | lo;
-      const unsigned long long e1 = ld_shared_u64(slots + 8 * s1) ^ key;
-      const unsigned long long e2 = ld_shared_u64(slots + 8 * s2) ^ key;
-      const bool h1 = (e1 & 0xffffffffffffull) == 0 && (e1 >> 48) < 0xffffull;
-      const bool h2 = (e2 & 0xffffffffffffull) == 0 && (e2 >> 48) < 0xffffull;
-      if (h1 || h2) {
-        const unsigned long long pos = atomicAdd(&a.counters[0], 1ull);
-        if (pos < a.cap) {
-          a.out_off[pos] = ya - (int64_t)a.g.amis;
-          a.out_idx[pos] = (uint32_t)((h1 ? e1 : e2) >> 48);
-        }
-      }
-    }
-  } while (pass);
+// Caller's index of the pattern (lo, hb, L) -- a window's bytes, masked to its length --
+// in the sweep's cuckoo table, or -1.
+__device__ __forceinline__ int short_probe(const MultiArgs& a, uint32_t slots, uint32_t lo,
+                                           uint32_t hb, uint32_t L) {
+  const uint32_t tag = short_tag(hb, L);  // = the key's high word
+  const uint32_t f = tiny_key_hash(lo, tag, a.th);
+  uint32_t s1, s2;
+  tiny_slots(f, a.th, s1, s2);
+  const unsigned long long key = ((unsigned long long)tag << 32) | lo;
+  const unsigned long long e1 = ld_shared_u64(slots + 8 * s1);
+  const unsigned long long e2 = ld_shared_u64(slots + 8 * s2);
+  // a hit leaves only the index bits; empty slots (~0) have the top bit set
+  if (((e1 ^ key) & kShortKeyMask) == 0 && !(e1 >> 63)) return (int)((e1 >> 51) & 0xfffu);
+  if (((e2 ^ key) & kShortKeyMask) == 0 && !(e2 >> 63)) return (int)((e2 >> 51) & 0xfffu);
+  return -1;
 }
 
-template <int M>
-__global__ void __launch_bounds__(kMultiBlock) rk_multi_tiny_kernel(const __grid_constant__ MultiArgs a) {
+// Caller's index of the pattern of length L equal to the window at a-space ya, or -1.
+__device__ __forceinline__ int short_lookup(const MultiArgs& a, uint32_t slots, uint32_t cur,
+                                            int64_t c0, uint32_t stage_bytes, int64_t ya,
+                                            uint32_t L, uint64_t ys_hi) {
+  if (ya < (int64_t)a.ys_lo || ya >= (int64_t)ys_hi) return -1;
+  const uint2 w = short_window_bytes(a.g, cur, c0, ya, stage_bytes);
+  const uint32_t lo = L >= 4 ? w.x : (w.x & ((1u << (8 * L)) - 1u));
+  const uint32_t hb = L > 4 ? (w.y & ((1u << (8 * (L - 4))) - 1u)) : 0u;
+  return short_probe(a, slots, lo, hb, L);
+}
+
+// One chunk: the lane's 32 positions end at J (a-space); v = its 32 bytes, lb the 32
+// before; cur = shared address of the chunk's 32-byte lookback (0: edge tile, global).
+// The sweep's lengths (<= 3 of them: 4..6 or 1..3) and their byte masks, kept in registers.
+struct ShortLens {
+  uint32_t G, L[3], klo[3], khi[3];
+  __device__ explicit ShortLens(const MultiArgs& a) : G(a.G) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      L[i] = i < (int)G ? a.grp[i].m : 0u;
+      klo[i] = L[i] >= 4 ? 0xffffffffu : ((1u << (8 * L[i])) - 1u);
+      khi[i] = L[i] > 4 ? ((1u << (8 * (L[i] - 4))) - 1u) : 0u;
+    }
+  }
+};
+
+template <int Q>
+__device__ __forceinline__ void short_chunk_multi(const MultiArgs& a, const ShortLens& SL,
+                                                  const Vec32& v, const uint32_t (&lb)[8],
+                                                  int64_t J, uint32_t cur, int lane,
+                                                  uint32_t slots, uint32_t filt,
+                                                  uint32_t stage_bytes) {
+  const int64_t c0 = J - kR * lane - 32;  // a-space position of the chunk's lookback start
+  if constexpr (Q > 0) {
+    // anchored: bit t = the q-gram ending at J + 2t + 1 passed
+    constexpr uint32_t QK = Q >= 4 ? 0xffffffffu : ((1u << (8 * Q)) - 1u);
+    uint32_t pass = 0;
+#pragma unroll
+    for (int t = 15; t >= 0; --t) {  // pass = 2 pass + bit: one IMAD, bit t = anchor t
+      const int k = 2 * t + 1;
+      pass = pass * 2u + short_filter_test(filt, w64(lb, v, 33 + k - Q) & QK);
+    }
+    unsigned act = __ballot_sync(kFull, pass != 0);
+    if (!act) return;
+    // every candidate window of the chunk lies in the text and in the stage (most chunks):
+    // lookups straight from shared memory without per-window checks
+    const int64_t ys_hi_min = (int64_t)a.grp[a.G - 1].ys_hi;  // the longest length's
+    const bool easy = __all_sync(kFull, cur != 0) && c0 >= (int64_t)a.ys_lo &&
+                      c0 + 32 + kChunk <= ys_hi_min && 32u + kChunk + 16u <= stage_bytes;
+    while (act) {
+      int t = -1;
+      if (pass) {
+        t = __ffs(pass) - 1;
+        pass &= pass - 1;
+      }
+      const int64_t y0 = J + 2 * t + 2 - Q;  // the anchor's window starts: y0 and y0 - 1
+      if (easy) {
+        // bytes [y0 - 1, y0 + 7) in shared memory, as the words of each start
+        uint32_t lo1 = 0, hi1 = 0, lo0 = 0, hi0 = 0;
+        if (t >= 0) {
+          const uint32_t addr = cur + (uint32_t)(y0 - 1 - c0);
+          const uint32_t al = addr & ~3u, r = 8u * (addr & 3u);
+          const uint32_t x0 = lds_u32(al), x1 = lds_u32(al + 4), x2 = lds_u32(al + 8);
+          lo1 = __funnelshift_r(x0, x1, r);
+          hi1 = __funnelshift_r(x1, x2, r);
+          lo0 = __funnelshift_r(lo1, hi1, 8);
+          hi0 = __funnelshift_r(hi1, x2 >> r, 8);
+        }
+#pragma unroll
+        for (int gi = 0; gi < 3; ++gi) {
+          if (gi >= (int)SL.G) break;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            int idx = -1;
+            if (t >= 0) {
+              const uint32_t lo = j ? lo1 : lo0, hw = j ? hi1 : hi0;
+              idx = short_probe(a, slots, lo & SL.klo[gi], hw & SL.khi[gi], SL.L[gi]);
+            }
+            multi_append(a, idx, y0 - j - (int64_t)a.g.amis, lane);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int64_t ya = y0 - j;  // candidate window start, a-space
+          for (uint32_t gi = 0; gi < a.G; ++gi) {
+            const int idx = t >= 0 ? short_lookup(a, slots, cur, c0, stage_bytes, ya,
+                                                  a.grp[gi].m, a.grp[gi].ys_hi)
+                                   : -1;
+            multi_append(a, idx, ya - (int64_t)a.g.amis, lane);
+          }
+        }
+      }
+      act = __ballot_sync(kFull, pass != 0);
+    }
+  } else {
+    // per window end J + k and length L (<= 3): the key's filter test
+    for (uint32_t gi = 0; gi < a.G; ++gi) {
+      const uint32_t L = a.grp[gi].m;
+      const uint32_t K = (1u << (8 * L)) - 1u;
+      uint32_t pass = 0;
+#pragma unroll
+      for (int k = 31; k >= 0; --k) {
+        // the L bytes ending at J + k are the top L bytes of the word ending there
+        const uint32_t kb = (w64(lb, v, 29 + k) >> (8 * (4 - L))) & K;
+        pass = pass * 2u + short_filter_test(filt, tiny_key_hash(kb, short_tag(0u, L), a.th));
+      }
+      unsigned act = __ballot_sync(kFull, pass != 0);
+      while (act) {
+        int k = -1;
+        if (pass) {
+          k = __ffs(pass) - 1;
+          pass &= pass - 1;
+        }
+        const int64_t ya = J + k - (int64_t)L + 1;
+        const int idx =
+            k >= 0 ? short_lookup(a, slots, cur, c0, stage_bytes, ya, L, a.grp[gi].ys_hi) : -1;
+        multi_append(a, idx, ya - (int64_t)a.g.amis, lane);
+        act = __ballot_sync(kFull, pass != 0);
+      }
+    }
+  }
+}
+
+// Q = anchored q-gram length (3 or 4), 0 = per-window keys.
+template <int Q>
+__global__ void __launch_bounds__(kMultiBlock) rk_multi_short_kernel(const __grid_constant__ MultiArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   MultiRing* rings = reinterpret_cast<MultiRing*>(smem);
   uint8_t* tab = smem + sizeof(MultiRing) * kMultiWarps;
-  const TinyHash th = a.grp[0].tiny_hash;
-  const uint32_t n16 = (th.size * 8u + kTinyFilterBytes) / 16u;  // slots, then the filter
-  const uint4* src = reinterpret_cast<const uint4*>(a.grp[0].tiny);
+  const uint32_t n16 = (a.th.size * 8u + kShortFilterWords * 4u) / 16u;  // slots, then filter
+  const uint4* src = reinterpret_cast<const uint4*>(a.stab);
   for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) reinterpret_cast<uint4*>(tab)[i] = src[i];
   __syncthreads();
   const uint32_t slots = smem_u32(tab);
-  const uint32_t bitmap = slots + th.size * 8u;
+  const uint32_t filt = slots + a.th.size * 8u;
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -392,17 +444,15 @@ __global__ void __launch_bounds__(kMultiBlock) rk_multi_tiny_kernel(const __grid
   const uint64_t w = (uint64_t)blockIdx.x * kMultiWarps + warp;
   Stream S;
   stream_init(a.g, R, S, (uint32_t)w, (uint32_t)W, lane);
+  const ShortLens SL(a);
   for (uint32_t t = (uint32_t)w; t < (uint32_t)a.g.num_tiles; t += (uint32_t)W) {
-    const int64_t ta = a.g.tile_a(t);
-    const bool full = ta >= (int64_t)a.g.ja_lo && ta + kTile <= (int64_t)a.g.ja_hi;
-    stream_tile<M, false>(a.g, R, S, t, lane,
-                          [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J, int) {
-                            if constexpr (M >= kTinyAnchorFrom) {
-                              tiny_anchor_chunk<M>(a, v, lb, J, S.cur, lane, slots, bitmap, th);
-                            } else {
-                              tiny_chunk<M>(a, v, lb, J, full ? 0xffffffffu : valid_mask(a.g, J),
-                                            slots, bitmap, th);
-                            }
+    stream_tile<8, false>(a.g, R, S, t, lane,
+                          [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J, int c) {
+                            // the stage holds the chunk's lookback, itself and the rest of
+                            // the stage's chunks
+                            const uint32_t sb =
+                                32u + (uint32_t)(kMultiStageChunks - c % kMultiStageChunks) * kChunk;
+                            short_chunk_multi<Q>(a, SL, v, lb, J, S.cur, lane, slots, filt, sb);
                           });
   }
 }

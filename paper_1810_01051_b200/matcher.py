@@ -197,7 +197,7 @@ def _device_text(t):
 
 def multi_scan(t_dev, dev: int, pats: list[bytes]):
     """Patterns of any lengths through rk_multi_scan_mixed (one device sweep for all lengths
-    >= 7) -> [offsets ndarray per pattern]."""
+    >= 7, one for 4..6, one for 1..3) -> [offsets ndarray per pattern]."""
     import torch
 
     L = _lib.lib()
@@ -229,7 +229,7 @@ def multi_scan(t_dev, dev: int, pats: list[bytes]):
 
 def search_multi(text, patterns) -> list[tuple[int, MatchResult]]:
     """Every pattern of a PatternSet (matcher.py:125-157): all lengths >= 7 in one device
-    sweep, each shorter length in its own.
+    sweep (per 64 lengths), 4..6 in one more, 1..3 in another.
 
     Returns one (pattern index, MatchResult) per distinct pattern, in index order; each
     result equals search_naive for that pattern."""

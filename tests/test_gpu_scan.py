@@ -502,3 +502,52 @@ def test_search_each_host_batch(gpu):
     assert rk.search_each(pinned.numpy(), pats[:3]) == got[:3]
     assert rk.search_each(text.tobytes()[: 1 << 20], [pats[0]]) == \
         [rk.search_sequential(text.tobytes()[: 1 << 20], pats[0])]
+
+
+def test_multi_short_lengths_folded(gpu):
+    """Every length < 7 of a set in at most two sweeps (1..3 per-window keys, 4..6 anchored
+    q-grams, one cuckoo table keyed by (bytes, length) each) next to the >= 7 sweep;
+    results equal the per-length oracle at both text ends and at odd device offsets."""
+    torch = _torch()
+    from paper_1810_01051_b200 import _lib
+
+    rng = np.random.default_rng(91)
+    for alpha, lo in ((4, 65), (95, 32), (256, 0)):
+        n = 200000
+        base = (rng.integers(0, alpha, n + 8, dtype=np.uint8) + lo).astype(np.uint8)
+        for shift in (0, 5):
+            host = base[shift: shift + n].copy()
+            pats = []
+            for m in (1, 2, 3, 4, 5, 6, 9, 20):
+                for x in (0, 1, 1023, 1024, 4095, n // 2, n - m):
+                    pats.append(host[x: x + m].tobytes())
+                for _ in range(30):
+                    pats.append((rng.integers(0, alpha, m) + lo).astype(np.uint8).tobytes())
+            dev = torch.from_numpy(base).cuda()[shift: shift + n]
+            ctx = _lib.context()
+            before = ctx.launches
+            out = rk.search_multi(dev, pats)
+            total = sum(len(r.offsets) for _, r in out)
+            # 1..3, 4..6, >= 7 (twice when the pairs overflow search_multi's first buffer)
+            assert ctx.launches - before == 3 * (2 if total > (1 << 16) else 1)
+            ps, by_len, _ = oracle.pattern_set(pats)
+            expect = {}
+            for m, idxs in by_len.items():
+                for j, offs in oracle.c_search_multi_group(host, [ps[i] for i in idxs]):
+                    expect[idxs[j]] = offs.tolist()
+            for i, r in out:
+                assert r.offsets == expect[i], (alpha, shift, i, len(ps[i]))
+
+
+def test_multi_dense_short_lengths(gpu):
+    """Dense output through the short sweeps: all 'a' against a, aa, ..., a^8 -- every
+    window of every length matches (appended one atomic per warp per round)."""
+    torch = _torch()
+    for n in (200003, 4096 + 7):
+        t = torch.full((n,), 97, dtype=torch.uint8, device="cuda")
+        pats = [b"a" * m for m in range(1, 9)] + [b"ab", b"aab", b"aaaab"]
+        out = rk.search_multi(t, pats)
+        for i, r in out:
+            m = len(pats[i])
+            exp = list(range(n - m + 1)) if b"b" not in pats[i] else []
+            assert r.offsets == exp, (n, pats[i])
