@@ -1283,7 +1283,7 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
   if (k > pre) {  // too many for a host round trip: radix-sort the pairs on the device
     const size_t need = sort_pairs_scratch(k);
     if (int r = grow(&c->d_sort, &c->sort_cap, (uint64_t)need, false, s)) return r;
-    RK_CUDA(sort_pairs(d_off, d_idx, k, c->d_sort, c->sort_cap, s));
+    RK_CUDA(sort_pairs(d_off, d_idx, k, n, P, c->d_sort, c->sort_cap, s));
   } else if (k > 1) {
     std::vector<int64_t> off(k);
     std::vector<uint32_t> idx(k);

@@ -229,8 +229,8 @@ cudaError_t launch_multi(const MultiArgs& a, int grid, cudaStream_t s);
 
 // device ordering of (pattern index, offset) pairs (rk_pairs.cu)
 size_t sort_pairs_scratch(uint64_t k);
-cudaError_t sort_pairs(int64_t* d_off, uint32_t* d_idx, uint64_t k, void* scratch,
-                       size_t scratch_bytes, cudaStream_t s);
+cudaError_t sort_pairs(int64_t* d_off, uint32_t* d_idx, uint64_t k, uint64_t n, uint32_t P,
+                       void* scratch, size_t scratch_bytes, cudaStream_t s);
 
 // auxiliaries (rk_aux.cu)
 cudaError_t launch_window_hashes(const uint8_t* text, uint64_t n, uint32_t m, uint64_t start,

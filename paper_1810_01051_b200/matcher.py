@@ -207,7 +207,9 @@ def multi_scan(t_dev, dev: int, pats: list[bytes]):
     lengths = np.array([len(p) for p in pats], dtype=np.uint32)
     hashes = np.array([hash_full(p) for p in pats], dtype=np.uint64)
     stream = _scan._stream(dev)
-    cap = 1 << 16
+    # pairs beyond cap are counted but not written (the sweep then runs again with exact
+    # room): room for the text's own size covers every set short of adversarial density
+    cap = max(1 << 16, min(n, 1 << 24))
     pairs = _lib.u64ref()
     for _attempt in range(2):
         off = torch.empty(cap, dtype=torch.int64, device=t_dev.device)
