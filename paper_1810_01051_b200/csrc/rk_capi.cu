@@ -665,9 +665,14 @@ int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, 
             case 2: h = qgram_hash<2>(w); break;
             default: h = qgram_hash<1>(w); break;
           }
-          uint32_t* blk = reinterpret_cast<uint32_t*>(blob.data() + sw.qfilter) + 2 * (h >> 19);
+          uint32_t* qf = reinterpret_cast<uint32_t*>(blob.data() + sw.qfilter);
+#if RK_QFILTER_WORD32
+          qf[h >> 18] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31)) | (1u << ((h >> 10) & 31));
+#else
+          uint32_t* blk = qf + 2 * (h >> 19);
           blk[0] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31));
           blk[1] |= (1u << ((h >> 10) & 31)) | (1u << ((h >> 15) & 31));
+#endif
           groups_of[h] |= 1ull << (k - gi);
         }
       }

@@ -48,11 +48,18 @@ __device__ __forceinline__ bool filter_test(const uint32_t* __restrict__ f, uint
 template <int QW>
 __device__ __forceinline__ bool qfilter_test(const uint32_t* __restrict__ f, const uint32_t* w) {
   const uint32_t h = qgram_hash<QW>(w);
+#if RK_QFILTER_WORD32
+  // one 32-bit word per q-gram, three bits: one LDS.32 (fewer bank conflicts than LDS.64)
+  const uint32_t x = f[h >> 18];
+  return (__funnelshift_r(x, x, h) & __funnelshift_r(x, x, h >> 5) &
+          __funnelshift_r(x, x, h >> 10) & 1u) != 0u;
+#else
   const uint2 x = reinterpret_cast<const uint2*>(f)[h >> 19];
   // rotates take the position mod 32: four SHF and two LOP3, no masking
   const uint32_t r = __funnelshift_r(x.x, x.x, h) & __funnelshift_r(x.x, x.x, h >> 5) &
                      __funnelshift_r(x.y, x.y, h >> 10) & __funnelshift_r(x.y, x.y, h >> 15);
   return (r & 1u) != 0u;
+#endif
 }
 
 // Anchored q-gram tests of one lane (window-end anchors e = J + s*t + s - 1, the q-gram
