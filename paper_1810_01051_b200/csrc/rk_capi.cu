@@ -651,6 +651,9 @@ int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, 
     else if (m_min >= 11) sw.qmode = 4, sw.qwords = 2;
     else sw.qmode = 4, sw.qwords = 1;
     sw.qfilter = reserve(kQFilterWords * sizeof(uint32_t));
+    // several lengths: 32-bit filter words (fewer bank conflicts, measured +10% on 64 mixed
+    // lengths); one length: 64-bit blocks (fewer false positives, +3% on C3)
+    sw.qf32 = (g_end - gi) > 1 ? 1u : 0u;
     std::unordered_map<uint32_t, uint64_t> groups_of;  // q-gram hash -> group mask
     for (size_t k = gi; k < g_end; ++k)
       for (uint32_t i = 0; i < plan.groups[k].P; ++i) {
@@ -666,13 +669,13 @@ int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, 
             default: h = qgram_hash<1>(w); break;
           }
           uint32_t* qf = reinterpret_cast<uint32_t*>(blob.data() + sw.qfilter);
-#if RK_QFILTER_WORD32
-          qf[h >> 18] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31)) | (1u << ((h >> 10) & 31));
-#else
-          uint32_t* blk = qf + 2 * (h >> 19);
-          blk[0] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31));
-          blk[1] |= (1u << ((h >> 10) & 31)) | (1u << ((h >> 15) & 31));
-#endif
+          if (sw.qf32) {
+            qf[h >> 18] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31)) | (1u << ((h >> 10) & 31));
+          } else {
+            uint32_t* blk = qf + 2 * (h >> 19);
+            blk[0] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31));
+            blk[1] |= (1u << ((h >> 10) & 31)) | (1u << ((h >> 15) & 31));
+          }
           groups_of[h] |= 1ull << (k - gi);
         }
       }
@@ -1227,6 +1230,7 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
     MultiArgs p{};
     p.qmode = sw.qmode;
     p.qwords = sw.qwords;
+    p.qf32 = sw.qf32;
     if (sw.qmode) {
       // tiles over the anchors e (q-gram ends): [first start + q - 1, last start of the
       // shortest length + q - 1 + s), clamped to the text

@@ -55,6 +55,7 @@ struct MultiPlan {
   struct Sweep {
     std::vector<uint32_t> groups;  // ascending lengths
     uint32_t qmode = 0, qwords = 0;
+    uint32_t qf32 = 0;     // q-gram filter of 32-bit words (several lengths) or 64-bit blocks
     uint64_t qfilter = 0;  // blob offset of the sweep's q-gram filter (qmode > 0)
     uint64_t qmap = 0;     // blob offset of its q-gram -> group-mask table
     uint32_t qmap_size = 0;

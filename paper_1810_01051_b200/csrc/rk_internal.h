@@ -121,10 +121,6 @@ constexpr uint32_t kMultiEmpty = 0xffffffffu;
 // against 0.095% for a 2-probe filter of the same size.)  The same hash runs on the host
 // (filter build) and the device (text q-grams): block = h >> 19, bit positions
 // h, h >> 5 (low half) and h >> 10, h >> 15 (high half), each mod 32.
-#ifndef RK_QFILTER_WORD32
-#define RK_QFILTER_WORD32 0  // q-gram filter: 4 bits in a 64-bit block (0) or 3 in one 32-bit word (1: LDS.32;
-                             // measured C3 5245 -> 5080 GB/s, C3 mixed lengths 3626 -> 4000)
-#endif
 template <int QW>
 __host__ __device__ __forceinline__ uint32_t qgram_hash(const uint32_t* w) {
   const uint32_t C[4] = {0x9E3779B1u, 0x85EBCA77u, 0xC2B2AE3Du, 0x165667B1u};
@@ -211,6 +207,7 @@ struct MultiArgs {
   const uint32_t* qfilter;    // kQFilterWords words (q-gram mode)
   uint32_t qmode;             // sampling step s (8 or 4), 0 = per-window filter (m < 7)
   uint32_t qwords;            // q-gram length in words (q = 4 * qwords)
+  uint32_t qf32;              // filter layout: 32-bit words (1) or 64-bit blocks (0)
   uint64_t ys_lo;             // first valid window start, a-space
   int64_t* out_off;
   uint32_t* out_idx;

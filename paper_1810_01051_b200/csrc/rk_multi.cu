@@ -22,12 +22,17 @@ __global__ void __launch_bounds__(kMultiBlock) rk_multi_qgram_kernel(const __gri
   stream_init(a.g, R, S, (uint32_t)w, (uint32_t)W, lane);
   const int s = (int)a.qmode;
   for (uint32_t t = (uint32_t)w; t < (uint32_t)a.g.num_tiles; t += (uint32_t)W) {
-    switch (s * 8 + (int)a.qwords) {
-      case 8 * 8 + 4: qgram_tile<8, 4>(a, R, S, t, lane, sfilter); break;
-      case 8 * 8 + 2: qgram_tile<8, 2>(a, R, S, t, lane, sfilter); break;
-      case 4 * 8 + 3: qgram_tile<4, 3>(a, R, S, t, lane, sfilter); break;
-      case 4 * 8 + 2: qgram_tile<4, 2>(a, R, S, t, lane, sfilter); break;
-      default: qgram_tile<4, 1>(a, R, S, t, lane, sfilter); break;
+    switch (s * 16 + (int)a.qwords * 2 + (int)a.qf32) {
+      case 8 * 16 + 4 * 2: qgram_tile<8, 4, false>(a, R, S, t, lane, sfilter); break;
+      case 8 * 16 + 2 * 2: qgram_tile<8, 2, false>(a, R, S, t, lane, sfilter); break;
+      case 4 * 16 + 3 * 2: qgram_tile<4, 3, false>(a, R, S, t, lane, sfilter); break;
+      case 4 * 16 + 2 * 2: qgram_tile<4, 2, false>(a, R, S, t, lane, sfilter); break;
+      case 4 * 16 + 1 * 2: qgram_tile<4, 1, false>(a, R, S, t, lane, sfilter); break;
+      case 8 * 16 + 4 * 2 + 1: qgram_tile<8, 4, true>(a, R, S, t, lane, sfilter); break;
+      case 8 * 16 + 2 * 2 + 1: qgram_tile<8, 2, true>(a, R, S, t, lane, sfilter); break;
+      case 4 * 16 + 3 * 2 + 1: qgram_tile<4, 3, true>(a, R, S, t, lane, sfilter); break;
+      case 4 * 16 + 2 * 2 + 1: qgram_tile<4, 2, true>(a, R, S, t, lane, sfilter); break;
+      default: qgram_tile<4, 1, true>(a, R, S, t, lane, sfilter); break;
     }
   }
 }

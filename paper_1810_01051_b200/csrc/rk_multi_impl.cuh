@@ -45,26 +45,29 @@ __device__ __forceinline__ bool filter_test(const uint32_t* __restrict__ f, uint
   return (f[b >> 5] >> (b & 31)) & 1u;
 }
 
-template <int QW>
+// F32: the filter's layout -- one 32-bit word per q-gram with three bits (one LDS.32),
+// or one 64-bit block with four (one LDS.64; fewer false positives).  The host picks per
+// sweep (MultiPlan::Sweep::qf32): measured C3 (one length) 5245 GB/s with 64-bit blocks
+// against 5080 with words, 64 mixed lengths 3626 against 4000.
+template <int QW, bool F32>
 __device__ __forceinline__ bool qfilter_test(const uint32_t* __restrict__ f, const uint32_t* w) {
   const uint32_t h = qgram_hash<QW>(w);
-#if RK_QFILTER_WORD32
-  // one 32-bit word per q-gram, three bits: one LDS.32 (fewer bank conflicts than LDS.64)
-  const uint32_t x = f[h >> 18];
-  return (__funnelshift_r(x, x, h) & __funnelshift_r(x, x, h >> 5) &
-          __funnelshift_r(x, x, h >> 10) & 1u) != 0u;
-#else
-  const uint2 x = reinterpret_cast<const uint2*>(f)[h >> 19];
-  // rotates take the position mod 32: four SHF and two LOP3, no masking
-  const uint32_t r = __funnelshift_r(x.x, x.x, h) & __funnelshift_r(x.x, x.x, h >> 5) &
-                     __funnelshift_r(x.y, x.y, h >> 10) & __funnelshift_r(x.y, x.y, h >> 15);
-  return (r & 1u) != 0u;
-#endif
+  if constexpr (F32) {
+    const uint32_t x = f[h >> 18];
+    return (__funnelshift_r(x, x, h) & __funnelshift_r(x, x, h >> 5) &
+            __funnelshift_r(x, x, h >> 10) & 1u) != 0u;
+  } else {
+    const uint2 x = reinterpret_cast<const uint2*>(f)[h >> 19];
+    // rotates take the position mod 32: four SHF and two LOP3, no masking
+    const uint32_t r = __funnelshift_r(x.x, x.x, h) & __funnelshift_r(x.x, x.x, h >> 5) &
+                       __funnelshift_r(x.y, x.y, h >> 10) & __funnelshift_r(x.y, x.y, h >> 15);
+    return (r & 1u) != 0u;
+  }
 }
 
 // Anchored q-gram tests of one lane (window-end anchors e = J + s*t + s - 1, the q-gram
 // being the QW words ending at e inside lb ++ v); bit t set when anchor t passes.
-template <int S, int QW>
+template <int S, int QW, bool F32>
 __device__ __forceinline__ uint32_t qgram_tests(const uint32_t* f, const Vec32& v,
                                                 const uint32_t (&lb)[8]) {
   uint32_t w[16];
@@ -78,7 +81,7 @@ __device__ __forceinline__ uint32_t qgram_tests(const uint32_t* f, const Vec32& 
   for (int t = 0; t < 32 / S; ++t) {
     constexpr int kw = S / 4;              // words per step
     const int end_w = 8 + (t + 1) * kw;    // one past the q-gram's last word
-    qm |= (uint32_t)qfilter_test<QW>(f, &w[end_w - QW]) << t;
+    qm |= (uint32_t)qfilter_test<QW, F32>(f, &w[end_w - QW]) << t;
   }
   return qm;
 }
@@ -210,7 +213,7 @@ __device__ __forceinline__ void qgram_candidate(const MultiArgs& a, int64_t e, i
 
 // One tile of anchored q-grams (one per SS bytes, ending at e = J + SS*t + SS - 1); a
 // q-gram that passes the filter makes its SS windows candidates, checked by SS lanes at once.
-template <int SS, int QW>
+template <int SS, int QW, bool F32>
 __device__ __forceinline__ void qgram_tile(const MultiArgs& a, MultiRing* R, Stream& S,
                                            uint32_t t, int lane, const uint32_t* sfilter) {
   constexpr int q = 4 * QW;
@@ -220,7 +223,7 @@ __device__ __forceinline__ void qgram_tile(const MultiArgs& a, MultiRing* R, Str
   stream_tile<kStreamM, RK_MULTI_UNROLL>(
       a.g, R, S, t, lane,
       [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J, int) {
-        const uint32_t qm = qgram_tests<SS, QW>(sfilter, v, lb);
+        const uint32_t qm = qgram_tests<SS, QW, F32>(sfilter, v, lb);
         unsigned lanes = __ballot_sync(kFull, qm != 0);
         while (lanes) {
           const int src = __ffs(lanes) - 1;
