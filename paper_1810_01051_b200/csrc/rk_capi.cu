@@ -5,6 +5,7 @@
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -41,7 +42,8 @@ class CopyPool {
  public:
   CopyPool() {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    n_ = std::min(8u, hw);
+    n_ = std::min(16u, hw);  // (C2 text, 16-core box: 8 threads 31 GB/s, 12-16 42-45)
+    if (const char* e = getenv("RKB200_COPY_THREADS")) n_ = std::max(1, atoi(e));
     for (unsigned i = 1; i < n_; ++i) th_.emplace_back([this, i] { loop(i); });
   }
   ~CopyPool() {

@@ -36,8 +36,12 @@ struct DeviceGuard {
 };
 
 constexpr uint64_t kStageChunk = 64ull << 20;  // host staging granularity (multiple of kTile)
-constexpr int kRing = 3;                        // pinned staging slots for pageable texts
-constexpr uint64_t kRingSlot = 32ull << 20;     // bytes per pinned slot
+#ifndef RK_RING_SLOTS
+#define RK_RING_SLOTS 4
+#define RK_RING_SLOT_MB 16
+#endif
+constexpr int kRing = RK_RING_SLOTS;                       // pinned staging slots (pageable texts)
+constexpr uint64_t kRingSlot = (uint64_t)RK_RING_SLOT_MB << 20;  // bytes per pinned slot
 
 class CopyPool;  // pageable -> pinned copy threads (rk_capi.cu)
 
