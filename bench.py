@@ -299,7 +299,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1810_01051_b200 as rk
-    from paper_1810_01051_b200 import _lib, sharded
+    from paper_1810_01051_b200 import _lib, _scan, sharded
 
     if args.lib:
         _lib.LIB_PATH = Path(args.lib).resolve()
@@ -324,7 +324,11 @@ def run_ours(args):
         plans[m] = (a - byte_lo, b - byte_lo, rk.hash_full(pats[m]))
     L = _lib.lib()
     ctx = _lib.context(dev)
-    comm = sharded.Communicator(device=dev) if world > 1 else None
+    # N > 1: the exchange through the C ABI (NCCL); --dist-backend gloo (the plumbing test of
+    # this multi-rank path on one GPU: ranks never wait on each other's kernels) exchanges
+    # through torch.distributed on the host instead
+    comm = sharded.Communicator(device=dev) if world > 1 and args.dist_backend == "nccl" else None
+    gloo = world > 1 and comm is None
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
     cap = 1 << 22
@@ -340,7 +344,14 @@ def run_ours(args):
             a, b, hx = plans[m]
             if ev_pairs is not None:
                 ev_pairs[i][0].record(stream)
-            if comm is None:
+            if gloo:
+                def scan_fn(t, p, lo, hi, hx=hx):
+                    o, k, co, hh = _scan.scan_counts(t, p, hx, lo, hi)
+                    return o.cpu(), k, co, hh
+                allo, tot = sharded.search_sharded(text, pats[m], a + byte_lo, b + byte_lo, byte_lo,
+                                                   scan_fn=scan_fn)
+                glob[m] = (allo, tot[0], tot[2], tot[1])
+            elif comm is None:
                 _lib.check(L.rk_scan_async(ctx.handle, text.data_ptr(), n_local,
                                            pat_bufs[m].ctypes.data, m, hx, a, b,
                                            outs[m].data_ptr(), cap, byte_lo,
@@ -359,7 +370,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     # correctness gate: counts add up; at N > 1 every rank holds the same global ascending
     # list, and its total is the sum over ranks
-    if comm is None:
+    if world == 1:
         host_counts = counts.cpu().numpy()
     else:
         host_counts = np.array([[glob[m][1], glob[m][3], glob[m][2]] for m in sweep], dtype=np.int64)
@@ -405,7 +416,7 @@ def run_ours(args):
 
     # roofline of the scan kernel: algorithmic bytes = n + 8*matches per launch (local)
     peak, peak_kind = load_peaks()
-    local_counts = counts.cpu().numpy() if comm is None else None
+    local_counts = counts.cpu().numpy() if world == 1 else None
     alg = [(plans[m][1] - plans[m][0] + m - 1) +
            8 * int((local_counts if local_counts is not None else host_counts)[i, 0])
            for i, m in enumerate(sweep)]
