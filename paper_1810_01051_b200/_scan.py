@@ -98,11 +98,28 @@ def _ptr(a: np.ndarray) -> int:
     return a.ctypes.data if a.size else 0
 
 
-def scan_counts(text, pattern, hx: int, start: int, stop: int, *, out_bias: int = 0):
+def to_device(host: np.ndarray, dev: int):
+    """A CUDA copy of a host uint8 array (read-only buffers such as ``bytes`` included):
+    staged through a pinned buffer, so the upload is one DMA and no read-only numpy array
+    is ever wrapped by a torch tensor."""
+    torch = _torch()
+    h = np.ascontiguousarray(host).reshape(-1)
+    out = torch.empty(h.size, dtype=torch.uint8, device=f"cuda:{dev}")
+    if h.size:
+        pinned = torch.empty(h.size, dtype=torch.uint8, pin_memory=True)
+        pinned.numpy()[:] = h
+        out.copy_(pinned, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()  # the pinned buffer is freed after
+    return out
+
+
+def scan_counts(text, pattern, hx: int, start: int, stop: int, *, out_bias: int = 0,
+                device: int | None = None):
     """Core call: (offsets, matches, collisions, hash_hits) for windows [start, stop).
 
     ``offsets`` is an int64 ndarray for host text and an int64 CUDA tensor for CUDA
-    text, holding all matches in ascending order."""
+    text, holding all matches in ascending order.  A host text is staged to ``device``
+    (default: the current one)."""
     L = _lib.lib()
     p = _host_bytes(pattern)
     m = int(p.size)
@@ -114,7 +131,7 @@ def scan_counts(text, pattern, hx: int, start: int, stop: int, *, out_bias: int 
         t = _host_bytes(text)
         cap = max(0, min(stop - start, _INITIAL_CAPACITY))
         out = np.empty(max(cap, 1), dtype=np.int64)
-        with _lib.acquire() as ctx:
+        with _lib.acquire(device) as ctx:
             _lib.check(L.rk_scan_host(ctx.handle, _ptr(t), n, _ptr(p), m, hx, start, stop,
                                       out.ctypes.data, cap, ctypes.byref(mt), ctypes.byref(co),
                                       ctypes.byref(hh)))
@@ -177,7 +194,7 @@ def scan_bitmap(text, pattern, hx: int, start: int, stop: int, *, packed: bool =
     on_host = dev is None
     if on_host:
         dev = _lib.default_device()
-        t = torch.from_numpy(np.array(_host_bytes(text), copy=True)).to(f"cuda:{dev}")
+        t = to_device(_host_bytes(text), dev)
     else:
         t = text
     words = torch.zeros(max((count + 31) // 32, 1), dtype=torch.int32, device=t.device)
@@ -218,7 +235,7 @@ def window_hashes(text, m: int, start: int, stop: int):
     on_host = dev is None
     if on_host:
         dev = _lib.default_device()
-        t = torch.from_numpy(np.ascontiguousarray(text)).to(f"cuda:{dev}")
+        t = to_device(_host_bytes(text), dev)
     else:
         t = text
     out = torch.empty(stop - start, dtype=torch.uint64, device=t.device)

@@ -189,10 +189,7 @@ def _device_text(t):
     if _scan._device_of(t) is not None:
         return t, _scan._device_of(t)
     dev = _lib.default_device()
-    host = torch.from_numpy(np.ascontiguousarray(t))
-    if host.numel():
-        host = host.pin_memory()
-    return host.to(f"cuda:{dev}", non_blocking=True), dev
+    return _scan.to_device(_scan._host_bytes(t), dev), dev
 
 
 def multi_scan(t_dev, dev: int, pats: list[bytes]):

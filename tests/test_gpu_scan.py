@@ -551,3 +551,21 @@ def test_multi_dense_short_lengths(gpu):
             m = len(pats[i])
             exp = list(range(n - m + 1)) if b"b" not in pats[i] else []
             assert r.offsets == exp, (n, pats[i])
+
+
+def test_search_parallel_device_shards_host_text(gpu):
+    """search_parallel(devices=[...]) with a host text: each shard goes through its device's
+    own staging pipeline (here two shards on cuda:0, scanned concurrently on two contexts)
+    and the rank-order concatenation equals the reference's result; pageable and pinned."""
+    torch = _torch()
+    rng = np.random.default_rng(12)
+    text = rng.integers(0, 4, (3 << 20) + 11, dtype=np.uint8)
+    for pat in (text[1000:1008].tobytes(), text[(3 << 20) // 2 - 4:(3 << 20) // 2 + 28].tobytes()):
+        cfg = rk.plan_launch(text.size, len(pat), 256)
+        st = rk.ScanStats()
+        r = rk.search_parallel(text.tobytes(), pat, cfg, 4, stats=st, devices=[0, 0])
+        st2 = rk.ScanStats()
+        assert r == rk.search_sequential(text.tobytes(), pat, stats=st2)
+        assert (st.hash_hits, st.collisions) == (st2.hash_hits, st2.collisions)
+        pinned = torch.from_numpy(text).pin_memory()
+        assert rk.search_parallel(pinned.numpy(), pat, cfg, 2, devices=[0, 0]) == r
