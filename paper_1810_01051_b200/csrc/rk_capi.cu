@@ -672,9 +672,9 @@ int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, 
           }
           uint32_t* qf = reinterpret_cast<uint32_t*>(blob.data() + sw.qfilter);
           if (sw.qf32) {
-            qf[h >> 18] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31)) | (1u << ((h >> 10) & 31));
+            qf[h >> kQWordShift] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31)) | (1u << ((h >> 10) & 31));
           } else {
-            uint32_t* blk = qf + 2 * (h >> 19);
+            uint32_t* blk = qf + 2 * (h >> kQBlockShift);
             blk[0] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31));
             blk[1] |= (1u << ((h >> 10) & 31)) | (1u << ((h >> 15) & 31));
           }

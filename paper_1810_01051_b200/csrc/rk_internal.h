@@ -112,7 +112,12 @@ cudaError_t launch_emit(EmitArgs e, int num_sms, cudaStream_t s);
 
 // multi pattern (rk_multi.cu, kernels in rk_multi_impl.cuh)
 constexpr int kMultiFilterWords = (1 << 16) / 32;
-constexpr int kQFilterWords = (1 << 19) / 32;  // q-gram Bloom filter, 64 KiB
+#ifndef RK_QFILTER_LOG2_BITS
+#define RK_QFILTER_LOG2_BITS 19  // q-gram Bloom filter of 2^19 bits = 64 KiB
+#endif
+constexpr int kQFilterWords = (1 << RK_QFILTER_LOG2_BITS) / 32;
+constexpr int kQBlockShift = 32 - (RK_QFILTER_LOG2_BITS - 6);  // h >> this = 64-bit block
+constexpr int kQWordShift = 32 - (RK_QFILTER_LOG2_BITS - 5);   // h >> this = 32-bit word
 constexpr uint32_t kMultiEmpty = 0xffffffffu;
 
 // Blocked Bloom filter of q-grams of QW = 1..4 little-endian words: 8192 blocks of 64

@@ -53,11 +53,11 @@ template <int QW, bool F32>
 __device__ __forceinline__ bool qfilter_test(const uint32_t* __restrict__ f, const uint32_t* w) {
   const uint32_t h = qgram_hash<QW>(w);
   if constexpr (F32) {
-    const uint32_t x = f[h >> 18];
+    const uint32_t x = f[h >> kQWordShift];
     return (__funnelshift_r(x, x, h) & __funnelshift_r(x, x, h >> 5) &
             __funnelshift_r(x, x, h >> 10) & 1u) != 0u;
   } else {
-    const uint2 x = reinterpret_cast<const uint2*>(f)[h >> 19];
+    const uint2 x = reinterpret_cast<const uint2*>(f)[h >> kQBlockShift];
     // rotates take the position mod 32: four SHF and two LOP3, no masking
     const uint32_t r = __funnelshift_r(x.x, x.x, h) & __funnelshift_r(x.x, x.x, h >> 5) &
                        __funnelshift_r(x.y, x.y, h >> 10) & __funnelshift_r(x.y, x.y, h >> 15);
