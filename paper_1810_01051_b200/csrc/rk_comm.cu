@@ -226,6 +226,15 @@ int rk_scan_sharded(rk_comm_t* k, const uint8_t* text, uint64_t len, uint64_t by
   const uint64_t start = win_hi > win_lo ? win_lo - byte_lo : 0;
   const uint64_t stop = win_hi > win_lo ? win_hi - byte_lo : 0;
   const bool on_device = stop > start && is_device_pointer(text, c->device);
+  if (stop > start && !on_device) {
+    cudaPointerAttributes attr;
+    const bool other = cudaPointerGetAttributes(&attr, text) == cudaSuccess &&
+                       attr.type == cudaMemoryTypeDevice;
+    cudaGetLastError();
+    if (other)
+      return fail(RK_EINVAL, "text is device memory of device %d, the communicator's is %d",
+                  attr.device, c->device);
+  }
 
   // 1. the local scan: ordered offsets (biased to global positions) + counters in d_cnt
   int64_t** local = &k->d_local;
