@@ -215,6 +215,22 @@ int rk_scan_sharded(rk_comm_t* comm, const uint8_t* text, uint64_t len, uint64_t
                     uint64_t win_hi, int64_t* d_out, uint64_t cap, uint64_t* matches,
                     uint64_t* collisions, uint64_t* hash_hits, void* stream);
 
+/*
+ * rk_multi_scan_sharded -- search_multi (matcher.py:125-157) over a text sharded across the
+ * communicator's ranks (collective).  Each rank passes the bytes it holds, d_text = global
+ * bytes [byte_lo, byte_lo + len) in device memory, and the window starts it owns,
+ * [start_lo, start_hi) (the held bytes must cover them plus the longest pattern's
+ * (m - 1)-byte halo, unless the shard ends the text).  Every rank receives ALL ranks'
+ * (offset, pattern index) pairs ordered by (index, offset) -- the reference's per-pattern
+ * ascending lists -- the first min(total, cap) of them in d_off / d_idx; *pairs = total.
+ * Patterns as rk_multi_scan_mixed; n_total = the whole text's length.
+ */
+int rk_multi_scan_sharded(rk_comm_t* comm, const uint8_t* d_text, uint64_t len, uint64_t byte_lo,
+                          uint64_t n_total, const uint8_t* h_patterns, const uint32_t* h_lengths,
+                          uint32_t P, const uint64_t* h_hashes, uint64_t start_lo,
+                          uint64_t start_hi, int64_t* d_off, uint32_t* d_idx, uint64_t cap,
+                          uint64_t* pairs, void* stream);
+
 /* Copies offsets [first, first + count) of the last rk_scan_sharded on this communicator
  * whose total exceeded its cap (every rank keeps the whole gathered list, so a caller
  * whose cap was too small never rescans).  Stream-ordered on `stream`. */

@@ -468,7 +468,7 @@ int host_scan_enqueue(rk_ctx* c, const uint8_t* h_text, uint64_t n, const uint8_
 // Builds (or reuses) the device tables of a pattern set: every length group's patterns,
 // hashes, key table and filter, plus one q-gram filter per sweep, in one device blob.
 // The plan is cached per context: repeating a search with the same set uploads nothing.
-int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, uint32_t P,
+int rkb::multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, uint32_t P,
                const uint64_t* h_hashes, cudaStream_t s) {
   std::vector<uint8_t> key(sizeof(uint32_t) + P * (sizeof(uint32_t) + sizeof(uint64_t)));
   uint64_t total = 0;
@@ -710,6 +710,161 @@ int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, 
   c->mplan = std::move(plan);
   return RK_OK;
 }
+
+namespace rkb {
+
+// Launches the sweeps of a PatternSet over the device text (patterns already planned into
+// c->mplan): every (window start, caller index) pair whose start lies in [start_lo,
+// start_hi) is appended, unordered, to d_off (start + bias) / d_idx, the count to
+// c->d_mcount.  Enqueued only.
+int multi_enqueue(rk_ctx* c, const uint8_t* d_text, uint64_t n, uint64_t start_lo,
+                  uint64_t start_hi, int64_t bias, int64_t* d_off, uint32_t* d_idx,
+                  uint64_t cap, cudaStream_t s) {
+  const MultiPlan& plan = c->mplan;
+  RK_CUDA(cudaMemsetAsync(c->d_mcount, 0, sizeof(unsigned long long), s));
+  const uint8_t* dev = c->d_mblob;
+  auto group_of = [&](const MultiPlan::Group& b, uint64_t amis) {
+    MultiGroup G{};
+    G.pats = dev + b.pats;
+    G.phash = reinterpret_cast<const uint64_t*>(dev + b.phash);
+    G.order = reinterpret_cast<const uint32_t*>(dev + b.order);
+    G.gidx = reinterpret_cast<const uint32_t*>(dev + b.gidx);
+    G.table = reinterpret_cast<const uint2*>(dev + b.table);
+    G.filter = reinterpret_cast<const uint32_t*>(dev + b.filter);
+    // window starts the sweep may report: [start_lo, min(n - m + 1, start_hi))
+    const uint64_t hi = b.m <= n ? std::min<uint64_t>(n - b.m + 1, start_hi) : 0;
+    G.ys_hi = amis + std::max<uint64_t>(hi, start_lo);
+    G.m = b.m;
+    G.tsize = b.tsize;
+    G.P = b.P;
+    return G;
+  };
+  for (const MultiPlan::Sweep& sw : plan.sweeps) {
+    // (lengths longer than the text stay in the sweep -- group bits are positions in
+    // it -- with an empty window range)
+    const uint32_t m_min = plan.groups[sw.groups.front()].m;
+    if (m_min > n) continue;
+    const uint64_t nw = n - m_min + 1;
+    Geometry gg = geometry(d_text, m_min, 0, nw);
+    MultiArgs p{};
+    p.qmode = sw.qmode;
+    p.qwords = sw.qwords;
+    p.qf32 = sw.qf32;
+    if (sw.qmode) {
+      // tiles over the anchors e (q-gram ends): [first start + q - 1, last start of the
+      // shortest length + q - 1 + s), clamped to the text
+      const uint64_t q = 4ull * sw.qwords;
+      gg.ja_lo = gg.amis + q - 1;
+      gg.ja_hi = std::min<uint64_t>(gg.amis + nw - 1 + q - 1 + sw.qmode, gg.amis + n);
+      gg.tile_first = gg.ja_lo / kTile;
+      gg.num_tiles = (gg.ja_hi - 1) / kTile - gg.tile_first + 1;
+      p.qfilter = reinterpret_cast<const uint32_t*>(dev + sw.qfilter);
+      p.qmap = reinterpret_cast<const uint4*>(dev + sw.qmap);
+      p.qmap_size = sw.qmap_size;
+    } else {
+      p.stab = dev + sw.stab;
+      p.th = sw.th;
+      p.sq = sw.sq;
+      if (sw.sq) {
+        // anchored short sweep: tiles over the anchors (q-gram ends, every 2 bytes) of the
+        // window starts [amis, amis + nw); window validity is checked on the starts
+        const uint64_t q = sw.sq;
+        gg.ja_lo = gg.amis + q - 1;
+        gg.ja_hi = std::min<uint64_t>(gg.amis + nw - 1 + q - 1 + 2, gg.amis + n);
+        gg.tile_first = gg.ja_lo / kTile;
+        gg.num_tiles = (gg.ja_hi - 1) / kTile - gg.tile_first + 1;
+      }
+      // (per-window short sweep: tiles over the window ends of the shortest length)
+    }
+    p.G = (uint32_t)sw.groups.size();
+    for (size_t k = 0; k < sw.groups.size(); ++k)
+      p.grp[k] = group_of(plan.groups[sw.groups[k]], gg.amis);
+    p.g = text_geom(gg, n, m_min, 0);
+    p.ys_lo = gg.amis + start_lo;
+    p.out_bias = bias;
+    p.out_off = d_off;
+    p.out_idx = d_idx;
+    p.cap = cap;
+    p.counters = c->d_mcount;
+    const uint64_t grid = std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)c->num_sms * multi_blocks_per_sm(p),
+                              (gg.num_tiles + kMultiWarps - 1) / kMultiWarps));
+    RK_CUDA(launch_multi(p, (int)grid, s));
+    ++c->launches;
+  }
+
+  return RK_OK;
+}
+
+// Orders the k pairs of d_off / d_idx by (caller index, offset) -- the reference's
+// per-pattern ascending lists: on the host when they fit one round trip (the count and a
+// prefix come back together), else by the device radix sort.  Offsets < n, indices < P.
+// *total receives the pair count (which may exceed cap: only cap were written).
+// Orders k pairs of d_off / d_idx by (caller index, offset) -- the reference's per-pattern
+// ascending lists -- given the first min(k, kMultiPrefix) of them already in
+// c->h_mresult (offsets at +1, indices at +1+kMultiPrefix): on the host when they all
+// are, else by the device radix sort.  Offsets < n, indices < P.
+int order_pairs(rk_ctx* c, int64_t* d_off, uint32_t* d_idx, uint64_t k, uint64_t n, uint32_t P,
+                cudaStream_t s) {
+  if (k > kMultiPrefix) {  // too many for a host round trip: radix-sort the pairs on the device
+    const size_t need = sort_pairs_scratch(k);
+    if (int r = grow(&c->d_sort, &c->sort_cap, (uint64_t)need, false, s)) return r;
+    RK_CUDA(sort_pairs(d_off, d_idx, k, n, P, c->d_sort, c->sort_cap, s));
+  } else if (k > 1) {
+    std::vector<int64_t> off(k);
+    std::vector<uint32_t> idx(k);
+    memcpy(off.data(), c->h_mresult + 1, k * sizeof(int64_t));
+    memcpy(idx.data(), c->h_mresult + 1 + kMultiPrefix, k * sizeof(uint32_t));
+    std::vector<uint64_t> perm(k);
+    for (uint64_t i = 0; i < k; ++i) perm[i] = i;
+    std::sort(perm.begin(), perm.end(), [&](uint64_t x, uint64_t y) {
+      return idx[x] != idx[y] ? idx[x] < idx[y] : off[x] < off[y];
+    });
+    bool sorted = true;
+    for (uint64_t i = 0; i < k && sorted; ++i) sorted = perm[i] == i;
+    if (!sorted) {
+      std::vector<int64_t> off2(k);
+      std::vector<uint32_t> idx2(k);
+      for (uint64_t i = 0; i < k; ++i) {
+        off2[i] = off[perm[i]];
+        idx2[i] = idx[perm[i]];
+      }
+      // pageable sources: each call returns once its bytes are staged
+      RK_CUDA(cudaMemcpyAsync(d_off, off2.data(), k * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      RK_CUDA(cudaMemcpyAsync(d_idx, idx2.data(), k * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    }
+  }
+  return RK_OK;
+}
+
+// Copies the first min(k, kMultiPrefix) pairs into c->h_mresult (synchronising s).
+int fetch_pair_prefix(rk_ctx* c, const int64_t* d_off, const uint32_t* d_idx, uint64_t k,
+                      cudaStream_t s) {
+  const uint64_t pre = std::min<uint64_t>(k, kMultiPrefix);
+  if (pre) {
+    RK_CUDA(cudaMemcpyAsync(c->h_mresult + 1, d_off, pre * sizeof(int64_t),
+                            cudaMemcpyDeviceToHost, s));
+    RK_CUDA(cudaMemcpyAsync(c->h_mresult + 1 + kMultiPrefix, d_idx, pre * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, s));
+  }
+  RK_CUDA(cudaStreamSynchronize(s));
+  return RK_OK;
+}
+
+// The pair count (from d_count) and a prefix of the pairs come back in one round trip;
+// then the first min(count, cap) pairs are ordered (order_pairs).  *total_out receives the
+// count, which may exceed cap: only cap pairs were written.
+int multi_order(rk_ctx* c, int64_t* d_off, uint32_t* d_idx, uint64_t cap, uint64_t n, uint32_t P,
+                const unsigned long long* d_count, uint64_t* total_out, cudaStream_t s) {
+  RK_CUDA(cudaMemcpyAsync(c->h_mresult, d_count, sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, s));
+  if (int r = fetch_pair_prefix(c, d_off, d_idx, cap, s)) return r;
+  const uint64_t total = c->h_mresult[0];
+  *total_out = total;
+  return order_pairs(c, d_off, d_idx, std::min(total, cap), n, P, s);
+}
+
+}  // namespace rkb
 
 extern "C" {
 
@@ -1204,122 +1359,8 @@ int rk_multi_scan_mixed(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const ui
   if (min_len > n) return RK_OK;  // no pattern has a window
   if (!d_text) return fail(RK_EINVAL, "text pointer is NULL");
   if (int r = multi_plan(c, h_patterns, h_lengths, P, h_hashes, s)) return r;
-  const MultiPlan& plan = c->mplan;
-  RK_CUDA(cudaMemsetAsync(c->d_mcount, 0, sizeof(unsigned long long), s));
-
-  const uint8_t* dev = c->d_mblob;
-  auto group_of = [&](const MultiPlan::Group& b, uint64_t amis) {
-    MultiGroup G{};
-    G.pats = dev + b.pats;
-    G.phash = reinterpret_cast<const uint64_t*>(dev + b.phash);
-    G.order = reinterpret_cast<const uint32_t*>(dev + b.order);
-    G.gidx = reinterpret_cast<const uint32_t*>(dev + b.gidx);
-    G.table = reinterpret_cast<const uint2*>(dev + b.table);
-    G.filter = reinterpret_cast<const uint32_t*>(dev + b.filter);
-    G.ys_hi = b.m <= n ? amis + (n - b.m + 1) : amis;  // longer than the text: no windows
-    G.m = b.m;
-    G.tsize = b.tsize;
-    G.P = b.P;
-    return G;
-  };
-  for (const MultiPlan::Sweep& sw : plan.sweeps) {
-    // (lengths longer than the text stay in the sweep -- group bits are positions in
-    // it -- with an empty window range)
-    const uint32_t m_min = plan.groups[sw.groups.front()].m;
-    if (m_min > n) continue;
-    const uint64_t nw = n - m_min + 1;
-    Geometry gg = geometry(d_text, m_min, 0, nw);
-    MultiArgs p{};
-    p.qmode = sw.qmode;
-    p.qwords = sw.qwords;
-    p.qf32 = sw.qf32;
-    if (sw.qmode) {
-      // tiles over the anchors e (q-gram ends): [first start + q - 1, last start of the
-      // shortest length + q - 1 + s), clamped to the text
-      const uint64_t q = 4ull * sw.qwords;
-      gg.ja_lo = gg.amis + q - 1;
-      gg.ja_hi = std::min<uint64_t>(gg.amis + nw - 1 + q - 1 + sw.qmode, gg.amis + n);
-      gg.tile_first = gg.ja_lo / kTile;
-      gg.num_tiles = (gg.ja_hi - 1) / kTile - gg.tile_first + 1;
-      p.qfilter = reinterpret_cast<const uint32_t*>(dev + sw.qfilter);
-      p.qmap = reinterpret_cast<const uint4*>(dev + sw.qmap);
-      p.qmap_size = sw.qmap_size;
-    } else {
-      p.stab = dev + sw.stab;
-      p.th = sw.th;
-      p.sq = sw.sq;
-      if (sw.sq) {
-        // anchored short sweep: tiles over the anchors (q-gram ends, every 2 bytes) of the
-        // window starts [amis, amis + nw); window validity is checked on the starts
-        const uint64_t q = sw.sq;
-        gg.ja_lo = gg.amis + q - 1;
-        gg.ja_hi = std::min<uint64_t>(gg.amis + nw - 1 + q - 1 + 2, gg.amis + n);
-        gg.tile_first = gg.ja_lo / kTile;
-        gg.num_tiles = (gg.ja_hi - 1) / kTile - gg.tile_first + 1;
-      }
-      // (per-window short sweep: tiles over the window ends of the shortest length)
-    }
-    p.G = (uint32_t)sw.groups.size();
-    for (size_t k = 0; k < sw.groups.size(); ++k)
-      p.grp[k] = group_of(plan.groups[sw.groups[k]], gg.amis);
-    p.g = text_geom(gg, n, m_min, 0);
-    p.ys_lo = gg.amis;
-    p.out_off = d_off;
-    p.out_idx = d_idx;
-    p.cap = cap;
-    p.counters = c->d_mcount;
-    const uint64_t grid = std::max<uint64_t>(
-        1, std::min<uint64_t>((uint64_t)c->num_sms * multi_blocks_per_sm(p),
-                              (gg.num_tiles + kMultiWarps - 1) / kMultiWarps));
-    RK_CUDA(launch_multi(p, (int)grid, s));
-    ++c->launches;
-  }
-
-  // the count and a prefix of the pairs come back in one round trip; the host orders
-  // them by (pattern index, offset) -- the reference's per-pattern ascending lists -- and
-  // writes them back (stream-ordered, so the caller sees them in its next operation)
-  const uint64_t pre = std::min<uint64_t>(cap, kMultiPrefix);
-  RK_CUDA(cudaMemcpyAsync(c->h_mresult, c->d_mcount, sizeof(unsigned long long),
-                          cudaMemcpyDeviceToHost, s));
-  if (pre) {
-    RK_CUDA(cudaMemcpyAsync(c->h_mresult + 1, d_off, pre * sizeof(int64_t),
-                            cudaMemcpyDeviceToHost, s));
-    RK_CUDA(cudaMemcpyAsync(c->h_mresult + 1 + kMultiPrefix, d_idx, pre * sizeof(uint32_t),
-                            cudaMemcpyDeviceToHost, s));
-  }
-  RK_CUDA(cudaStreamSynchronize(s));
-  const uint64_t total = c->h_mresult[0];
-  *pairs = total;
-  const uint64_t k = std::min(total, cap);
-  if (k > pre) {  // too many for a host round trip: radix-sort the pairs on the device
-    const size_t need = sort_pairs_scratch(k);
-    if (int r = grow(&c->d_sort, &c->sort_cap, (uint64_t)need, false, s)) return r;
-    RK_CUDA(sort_pairs(d_off, d_idx, k, n, P, c->d_sort, c->sort_cap, s));
-  } else if (k > 1) {
-    std::vector<int64_t> off(k);
-    std::vector<uint32_t> idx(k);
-    memcpy(off.data(), c->h_mresult + 1, k * sizeof(int64_t));
-    memcpy(idx.data(), c->h_mresult + 1 + kMultiPrefix, k * sizeof(uint32_t));
-    std::vector<uint64_t> perm(k);
-    for (uint64_t i = 0; i < k; ++i) perm[i] = i;
-    std::sort(perm.begin(), perm.end(), [&](uint64_t x, uint64_t y) {
-      return idx[x] != idx[y] ? idx[x] < idx[y] : off[x] < off[y];
-    });
-    bool sorted = true;
-    for (uint64_t i = 0; i < k && sorted; ++i) sorted = perm[i] == i;
-    if (!sorted) {
-      std::vector<int64_t> off2(k);
-      std::vector<uint32_t> idx2(k);
-      for (uint64_t i = 0; i < k; ++i) {
-        off2[i] = off[perm[i]];
-        idx2[i] = idx[perm[i]];
-      }
-      // pageable sources: each call returns once its bytes are staged
-      RK_CUDA(cudaMemcpyAsync(d_off, off2.data(), k * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-      RK_CUDA(cudaMemcpyAsync(d_idx, idx2.data(), k * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-    }
-  }
-  return RK_OK;
+  if (int r = multi_enqueue(c, d_text, n, 0, n, 0, d_off, d_idx, cap, s)) return r;
+  return multi_order(c, d_off, d_idx, cap, n, P, c->d_mcount, pairs, s);
 }
 
 }  // extern "C"

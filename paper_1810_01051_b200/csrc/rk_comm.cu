@@ -107,6 +107,13 @@ struct rk_comm {
   uint64_t local_cap = 0;
   int64_t* d_gather = nullptr;             // whole gathered list when the caller's cap < total
   uint64_t gather_cap = 0;
+  // multi-pattern shards: this rank's pairs, and every rank's gathered
+  int64_t* d_moff = nullptr;
+  uint32_t* d_midx = nullptr;
+  uint64_t m_cap = 0;
+  int64_t* d_goff = nullptr;
+  uint32_t* d_gidx = nullptr;
+  uint64_t g_cap = 0;
   uint64_t gathered = 0;                   // offsets of the last sharded scan in d_gather
 };
 
@@ -174,6 +181,10 @@ int rk_comm_destroy(rk_comm_t* k) {
   cudaFreeHost(k->h_allcnt);
   cudaFree(k->d_local);
   cudaFree(k->d_gather);
+  cudaFree(k->d_moff);
+  cudaFree(k->d_midx);
+  cudaFree(k->d_goff);
+  cudaFree(k->d_gidx);
   delete k;
   return RK_OK;
 }
@@ -307,6 +318,132 @@ int rk_scan_sharded(rk_comm_t* k, const uint8_t* text, uint64_t len, uint64_t by
   if (matches) *matches = total;
   if (hash_hits) *hash_hits = hits;
   if (collisions) *collisions = coll;
+  return RK_OK;
+}
+
+int rk_multi_scan_sharded(rk_comm_t* k, const uint8_t* d_text, uint64_t len, uint64_t byte_lo,
+                          uint64_t n_total, const uint8_t* h_patterns, const uint32_t* h_lengths,
+                          uint32_t P, const uint64_t* h_hashes, uint64_t start_lo,
+                          uint64_t start_hi, int64_t* d_off, uint32_t* d_idx, uint64_t cap,
+                          uint64_t* pairs, void* stream) {
+  if (!k || !pairs) return fail(RK_EINVAL, "communicator or pairs is NULL");
+  *pairs = 0;
+  if (P < 1 || P > RK_MULTI_MAX_PATTERNS)
+    return fail(RK_EINVAL, "pattern count %u outside [1, %d]", P, RK_MULTI_MAX_PATTERNS);
+  if (!h_patterns || !h_lengths || !h_hashes) return fail(RK_EINVAL, "NULL pattern arrays");
+  uint64_t max_len = 0;
+  for (uint32_t i = 0; i < P; ++i) {
+    if (h_lengths[i] < 1) return fail(RK_EINVAL, "pattern %u is empty", i);
+    max_len = std::max<uint64_t>(max_len, h_lengths[i]);
+  }
+  if (byte_lo + len > n_total) return fail(RK_EINVAL, "shard beyond the text");
+  if (start_hi > start_lo) {
+    // every window starting in the range must fit in the held bytes (the halo) unless the
+    // shard ends the text
+    if (start_lo < byte_lo || (start_hi - byte_lo + max_len - 1 > len && byte_lo + len < n_total))
+      return fail(RK_EINVAL, "starts [%llu, %llu) with patterns up to %llu bytes need bytes the "
+                  "shard [%llu, %llu) does not hold", (unsigned long long)start_lo,
+                  (unsigned long long)start_hi, (unsigned long long)max_len,
+                  (unsigned long long)byte_lo, (unsigned long long)(byte_lo + len));
+    if (!d_text) return fail(RK_EINVAL, "text pointer is NULL");
+  }
+  if (cap && (!d_off || !d_idx)) return fail(RK_EINVAL, "NULL output with cap > 0");
+  rk_ctx* c = k->ctx;
+  NcclApi& api = nccl();
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int r = enter(c, s)) return r;
+
+  // 1. this rank's pairs (global offsets), every start of [start_lo, start_hi) reported once
+  uint64_t local = 0;
+  if (k->m_cap < (1ull << 16)) {
+    cudaFree(k->d_moff);
+    cudaFree(k->d_midx);
+    k->d_moff = nullptr;
+    k->d_midx = nullptr;
+    RK_CUDA(cudaMalloc(&k->d_moff, (1ull << 16) * sizeof(int64_t)));
+    RK_CUDA(cudaMalloc(&k->d_midx, (1ull << 16) * sizeof(uint32_t)));
+    k->m_cap = 1ull << 16;
+  }
+  const bool any = start_hi > start_lo && len > 0;
+  if (any) {
+    if (int r = multi_plan(c, h_patterns, h_lengths, P, h_hashes, s)) return r;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if (int r = multi_enqueue(c, d_text, len, start_lo - byte_lo, start_hi - byte_lo,
+                                (int64_t)byte_lo, k->d_moff, k->d_midx, k->m_cap, s))
+        return r;
+      RK_CUDA(cudaMemcpyAsync(c->h_mresult, c->d_mcount, sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, s));
+      RK_CUDA(cudaStreamSynchronize(s));
+      local = c->h_mresult[0];
+      if (local <= k->m_cap) break;
+      // more pairs than the buffer held: again with exact room (the sweep appends
+      // unordered, so nothing beyond the buffer was kept)
+      RK_CUDA(cudaFree(k->d_moff));
+      RK_CUDA(cudaFree(k->d_midx));
+      k->d_moff = nullptr;
+      k->d_midx = nullptr;
+      RK_CUDA(cudaMalloc(&k->d_moff, local * sizeof(int64_t)));
+      RK_CUDA(cudaMalloc(&k->d_midx, local * sizeof(uint32_t)));
+      k->m_cap = local;
+    }
+  }
+
+  // 2. every rank's pair count, then the pairs themselves (allgather-v, offsets and indices)
+  k->h_allcnt[4 * k->rank] = local;  // (scratch) this rank's count to the device slot
+  RK_CUDA(cudaMemcpyAsync(k->d_cnt, &k->h_allcnt[4 * k->rank], sizeof(unsigned long long),
+                          cudaMemcpyHostToDevice, s));
+  RK_NCCL(api.AllGather(k->d_cnt, k->d_allcnt, 4, ncclUint64, k->comm, s));
+  RK_CUDA(cudaMemcpyAsync(k->h_allcnt, k->d_allcnt, 4ull * k->nranks * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, s));
+  RK_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint64_t> cnt(k->nranks), prefix(k->nranks + 1, 0);
+  for (int r = 0; r < k->nranks; ++r) {
+    cnt[r] = k->h_allcnt[4 * r];
+    prefix[r + 1] = prefix[r] + cnt[r];
+  }
+  const uint64_t total = prefix[k->nranks];
+  *pairs = total;
+  if (!total) return RK_OK;
+  int64_t* goff = d_off;
+  uint32_t* gidx = d_idx;
+  if (cap < total) {
+    if (k->g_cap < total) {
+      RK_CUDA(cudaStreamSynchronize(s));
+      cudaFree(k->d_goff);
+      cudaFree(k->d_gidx);
+      k->d_goff = nullptr;
+      k->d_gidx = nullptr;
+      RK_CUDA(cudaMalloc(&k->d_goff, total * sizeof(int64_t)));
+      RK_CUDA(cudaMalloc(&k->d_gidx, total * sizeof(uint32_t)));
+      k->g_cap = total;
+    }
+    goff = k->d_goff;
+    gidx = k->d_gidx;
+  }
+  RK_NCCL(api.GroupStart());
+  for (int r = 0; r < k->nranks; ++r) {
+    if (!cnt[r]) continue;
+    const bool me = r == k->rank;
+    ncclResult_t e = api.Broadcast(me ? (const void*)k->d_moff : (const void*)(goff + prefix[r]),
+                                   goff + prefix[r], cnt[r], ncclInt64, r, k->comm, s);
+    if (e == ncclSuccess)
+      e = api.Broadcast(me ? (const void*)k->d_midx : (const void*)(gidx + prefix[r]),
+                        gidx + prefix[r], cnt[r], ncclUint32, r, k->comm, s);
+    if (e != ncclSuccess) {
+      api.GroupEnd();
+      return fail(RK_ENCCL, "ncclBroadcast(root %d) failed: %s", r, api.GetErrorString(e));
+    }
+  }
+  RK_NCCL(api.GroupEnd());
+  // 3. (pattern index, offset) order over all ranks -- the reference's per-pattern lists
+  if (int r = fetch_pair_prefix(c, goff, gidx, total, s)) return r;
+  if (int r = order_pairs(c, goff, gidx, total, n_total, P, s)) return r;
+  if (goff != d_off && cap) {
+    RK_CUDA(cudaMemcpyAsync(d_off, goff, cap * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    RK_CUDA(cudaMemcpyAsync(d_idx, gidx, cap * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+  }
   return RK_OK;
 }
 

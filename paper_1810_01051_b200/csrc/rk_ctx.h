@@ -191,5 +191,16 @@ int host_scan_enqueue(rk_ctx* c, const uint8_t* h_text, uint64_t n, const uint8_
                       uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t bias,
                       uint64_t* d_counts);
 bool is_device_pointer(const void* p, int device);
+int multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_lengths, uint32_t P,
+               const uint64_t* h_hashes, cudaStream_t s);
+int multi_enqueue(rk_ctx* c, const uint8_t* d_text, uint64_t n, uint64_t start_lo,
+                  uint64_t start_hi, int64_t bias, int64_t* d_off, uint32_t* d_idx,
+                  uint64_t cap, cudaStream_t s);
+int multi_order(rk_ctx* c, int64_t* d_off, uint32_t* d_idx, uint64_t cap, uint64_t n, uint32_t P,
+                const unsigned long long* d_count, uint64_t* total_out, cudaStream_t s);
+int fetch_pair_prefix(rk_ctx* c, const int64_t* d_off, const uint32_t* d_idx, uint64_t k,
+                      cudaStream_t s);
+int order_pairs(rk_ctx* c, int64_t* d_off, uint32_t* d_idx, uint64_t k, uint64_t n, uint32_t P,
+                cudaStream_t s);
 
 }  // namespace rkb

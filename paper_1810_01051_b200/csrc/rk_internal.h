@@ -213,7 +213,8 @@ struct MultiArgs {
   uint32_t qmode;             // sampling step s (8 or 4), 0 = per-window filter (m < 7)
   uint32_t qwords;            // q-gram length in words (q = 4 * qwords)
   uint32_t qf32;              // filter layout: 32-bit words (1) or 64-bit blocks (0)
-  uint64_t ys_lo;             // first valid window start, a-space
+  uint64_t ys_lo;             // first window start the sweep reports, a-space
+  int64_t out_bias;           // added to every reported offset (shards)
   int64_t* out_off;
   uint32_t* out_idx;
   uint64_t cap;

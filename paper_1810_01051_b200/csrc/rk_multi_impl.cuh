@@ -151,7 +151,7 @@ __device__ __forceinline__ void multi_append(const MultiArgs& a, int idx, int64_
     if (idx >= 0) {
       const uint64_t pos = base + __popc(hit & ((1u << lane) - 1u));
       if (pos < a.cap) {
-        a.out_off[pos] = y;
+        a.out_off[pos] = y + a.out_bias;
         a.out_idx[pos] = (uint32_t)idx;
       }
     }

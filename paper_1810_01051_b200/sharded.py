@@ -272,6 +272,71 @@ class Communicator:
                 out = full
         return out[:k], k, int(co.value), int(hh.value)
 
+    def multi_scan(self, text, patterns, start_lo: int, start_hi: int, byte_lo: int,
+                   n_total: int, *, cap: int = 1 << 16, stream=None):
+        """rk_multi_scan_sharded: this rank's window starts [start_lo, start_hi) of the
+        global text, whose bytes [byte_lo, byte_lo + len(text)) it holds on this device,
+        against the PatternSet ``patterns``.  Returns every rank's pairs as (index int32
+        tensor, offset int64 tensor) ordered by (index, offset), on every rank."""
+        import numpy as np
+        import torch
+
+        from . import _scan
+        from .matcher import PatternSet
+        from .rkhash import hash_full
+
+        L = _lib.lib()
+        ps = patterns if isinstance(patterns, PatternSet) else PatternSet(patterns)
+        flat = np.frombuffer(b"".join(ps.patterns), dtype=np.uint8)
+        lengths = np.array([len(p) for p in ps.patterns], dtype=np.uint32)
+        hashes = np.array([hash_full(p) for p in ps.patterns], dtype=np.uint64)
+        t = _scan.as_u8(text)
+        if not (isinstance(t, torch.Tensor) and t.is_cuda):
+            t = _scan.to_device(_scan._host_bytes(t), self.device)
+        n = int(t.numel())
+        s = _scan._stream(self.device) if stream is None else stream
+        pairs = _lib.u64ref()
+        for _attempt in range(2):
+            off = torch.empty(max(cap, 1), dtype=torch.int64, device=f"cuda:{self.device}")
+            idx = torch.empty(max(cap, 1), dtype=torch.int32, device=f"cuda:{self.device}")
+            with self.ctx.lock:
+                _lib.check(L.rk_multi_scan_sharded(
+                    self.handle, t.data_ptr() if n else 0, n, byte_lo, n_total, flat.ctypes.data,
+                    lengths.ctypes.data, len(ps), hashes.ctypes.data, start_lo, start_hi,
+                    off.data_ptr(), idx.data_ptr(), cap, ctypes.byref(pairs), s))
+            k = int(pairs.value)
+            if k <= cap:
+                break
+            cap = k
+        return idx[:k], off[:k]
+
+    def search_multi(self, shard, patterns, n_total: int):
+        """search_multi's result over a text sharded across the ranks (multi_shard: each
+        rank owns a contiguous range of window starts and holds the longest pattern's
+        halo): ``shard`` is this rank's bytes, or the whole text (then sliced).  Returns
+        [(pattern index, MatchResult)] of the whole text on every rank."""
+        from . import _scan
+        from .matcher import MatchResult, PatternSet
+
+        ps = patterns if isinstance(patterns, PatternSet) else PatternSet(patterns)
+        lengths = [len(p) for p in ps.patterns]
+        fits = [m <= n_total for m in lengths]
+        found = {i: [] for i in range(len(ps))}
+        if any(fits):
+            a, b, blo, bhi = multi_shard(self.rank, self.world, n_total,
+                                         [m for m, f in zip(lengths, fits) if f])
+            t = _scan.as_u8(shard)
+            if _scan._size(t) == n_total and (blo, bhi) != (0, n_total):
+                t = t[blo:bhi]
+            idx, off = self.multi_scan(t, ps, a, b, blo, n_total)
+            idx, off = idx.cpu().numpy(), off.cpu().numpy()
+            import numpy as np
+
+            bounds = np.searchsorted(idx, np.arange(len(ps) + 1), side="left")
+            for i in range(len(ps)):
+                found[i] = off[bounds[i]:bounds[i + 1]].tolist()
+        return [(i, MatchResult(n_total, lengths[i], found[i])) for i in range(len(ps))]
+
     def search(self, shard, pattern, n_total: int, stats=None):
         """search_parallel's result over a text sharded across the ranks (strong partition,
         rk_shard_range): ``shard`` is this rank's bytes [byte_lo, byte_hi) -- or the whole

@@ -118,3 +118,28 @@ def test_communicator_over_torch_distributed(gpu):
         c.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_sharded_multi_pattern(comm):
+    """rk_multi_scan_sharded (one rank): the pairs of a whole PatternSet -- short, q-gram
+    and mixed lengths -- equal search_multi's, and a sub-range of starts held from
+    byte 1000 on reports exactly its starts (global offsets)."""
+    import torch
+
+    rng = np.random.default_rng(44)
+    n = 3 << 20
+    host = rng.integers(0, 4, n, dtype=np.uint8) + 65
+    pats = [host[x:x + m].tobytes() for x, m in ((10, 4), (5000, 6), (77777, 9), (2 << 20, 20),
+                                                   (n - 33, 33))]
+    pats += [b"ACGT", b"TTTTTTTTTTTTTT"]
+    text = torch.from_numpy(host).cuda()
+    got = comm.search_multi(text, pats, n)
+    assert got == rk.search_multi(text, pats)
+    # starts [5000, 2 MiB) held from byte 1000 (+ the 32-byte halo)
+    a, b, blo = 5000, 2 << 20, 1000
+    idx, off = comm.multi_scan(text[blo: b + 32], pats, a, b, blo, n)
+    ps = rk.PatternSet(pats)
+    full = dict(rk.search_multi(host.tobytes(), ps))
+    for i in range(len(ps)):
+        exp = [x for x in full[i].offsets if a <= x < b]
+        assert off[idx == i].cpu().tolist() == exp, i
