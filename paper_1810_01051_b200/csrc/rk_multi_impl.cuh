@@ -35,6 +35,9 @@ namespace rkb {
 #ifndef RK_MULTI_UNROLL
 #define RK_MULTI_UNROLL false
 #endif
+#ifndef RK_MULTI_STAGED_TESTS
+#define RK_MULTI_STAGED_TESTS 1  // q-gram tests unrolled per TMA stage, candidates afterwards
+#endif
 constexpr int kMultiBlock = 32 * kMultiWarps;
 using MultiRing = WarpRingT<kMultiStageChunks>;
 
@@ -211,32 +214,80 @@ __device__ __forceinline__ void qgram_candidate(const MultiArgs& a, int64_t e, i
   if (gmask) multi_check_window(a, e - q + 1 - lane, lane < SS, lane, gmask);
 }
 
+// The candidates of one chunk (qm = the lane's passing anchors, J = its first position):
+// each anchor's SS windows are checked by SS lanes at once (warp-uniform call).
+template <int SS, int QW>
+__device__ __forceinline__ void qgram_settle(const MultiArgs& a, uint32_t qm, int64_t J, int lane) {
+  unsigned lanes = __ballot_sync(kFull, qm != 0);
+  while (lanes) {
+    const int src = __ffs(lanes) - 1;
+    lanes &= lanes - 1;
+    uint32_t ms = __shfl_sync(kFull, qm, src);
+    const int64_t Js = __shfl_sync(kFull, J, src);
+    while (ms) {
+      const int tt = __ffs(ms) - 1;
+      ms &= ms - 1;
+      // the window whose anchor this is: its q-gram starts j = lane bytes in
+      qgram_candidate<SS, QW>(a, Js + (int64_t)SS * tt + SS - 1, lane);
+    }
+  }
+}
+
 // One tile of anchored q-grams (one per SS bytes, ending at e = J + SS*t + SS - 1); a
-// q-gram that passes the filter makes its SS windows candidates, checked by SS lanes at once.
+// q-gram that passes the filter makes its SS windows candidates, checked by SS lanes at
+// once.  Staged tiles run each TMA stage's chunks through the filter tests unrolled, with
+// nothing else in that code, and settle the (rare) candidates after the stage's tests.
 template <int SS, int QW, bool F32>
 __device__ __forceinline__ void qgram_tile(const MultiArgs& a, MultiRing* R, Stream& S,
                                            uint32_t t, int lane, const uint32_t* sfilter) {
-  constexpr int q = 4 * QW;
   // the anchored q-grams only reach into the 32 bytes before the lane's when a q-gram is
   // longer than the sampling step (QW words > SS / 4): otherwise skip loading them
   constexpr int kStreamM = QW > SS / 4 ? 31 : 0;
-  stream_tile<kStreamM, RK_MULTI_UNROLL>(
-      a.g, R, S, t, lane,
-      [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J, int) {
-        const uint32_t qm = qgram_tests<SS, QW, F32>(sfilter, v, lb);
-        unsigned lanes = __ballot_sync(kFull, qm != 0);
-        while (lanes) {
-          const int src = __ffs(lanes) - 1;
-          lanes &= lanes - 1;
-          uint32_t ms = __shfl_sync(kFull, qm, src);
-          const int64_t Js = __shfl_sync(kFull, J, src);
-          while (ms) {
-            const int tt = __ffs(ms) - 1;
-            ms &= ms - 1;
-            // the window whose anchor this is: its q-gram starts j = lane bytes in
-            qgram_candidate<SS, QW>(a, Js + (int64_t)SS * tt + SS - 1, lane);
-          }
+  constexpr int SC = kMultiStageChunks;
+  const TextGeom& g = a.g;
+  const int64_t ta = g.tile_a(t);
+#if RK_MULTI_STAGED_TESTS
+  if (t >= S.int_lo && t < S.int_hi) {
+#pragma unroll 1
+    for (int s = 0; s < kTileChunks / SC; ++s) {
+      mbar_wait(&R->bar[S.cslot], S.cphase);
+      const uint8_t* st = R->buf[S.cslot];
+      uint32_t qm[SC], anyq = 0;
+#pragma unroll
+      for (int j = 0; j < SC; ++j) {
+        const Vec32 v = lds32(st + 32 + j * kChunk + lane * kR);
+        uint32_t lb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if constexpr (kStreamM > 0) {
+          const Vec32 l = lds32(st + j * kChunk + lane * kR);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) lb[i] = l.w[i];
         }
+        qm[j] = qgram_tests<SS, QW, F32>(sfilter, v, lb);
+        anyq |= qm[j];
+      }
+      if (__any_sync(kFull, anyq != 0)) {
+#pragma unroll 1
+        for (int j = 0; j < SC; ++j) {
+          uint32_t q = qm[0];
+#pragma unroll
+          for (int jj = 1; jj < SC; ++jj) q = j == jj ? qm[jj] : q;
+          qgram_settle<SS, QW>(a, q, ta + (int64_t)(s * SC + j) * kChunk + lane * kR, lane);
+        }
+      }
+      // the slot's bytes are consumed: hand it back to the producer
+      S.cslot = (S.cslot + 1) & (kStages - 1);
+      S.cphase ^= (S.cslot == 0);
+      --S.pending;
+      __syncwarp();
+      stream_issue(R, S, lane);
+    }
+    return;
+  }
+#endif
+  stream_tile<kStreamM, RK_MULTI_UNROLL>(
+      g, R, S, t, lane,
+      [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J, int) {
+        qgram_settle<SS, QW>(a, qgram_tests<SS, QW, F32>(sfilter, v, lb), J, lane);
       });
 }
 
