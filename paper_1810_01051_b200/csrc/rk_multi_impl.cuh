@@ -386,76 +386,94 @@ struct ShortLens {
   }
 };
 
+// Anchored sweep, fast pass of one chunk: bit t = the q-gram ending at J + 2t + 1 passed.
+template <int Q>
+__device__ __forceinline__ uint32_t short_anchor_pass(uint32_t filt, const Vec32& v,
+                                                      const uint32_t (&lb)[8]) {
+  constexpr uint32_t QK = Q >= 4 ? 0xffffffffu : ((1u << (8 * Q)) - 1u);
+  uint32_t pass = 0;
+#pragma unroll
+  for (int t = 15; t >= 0; --t) {  // pass = 2 pass + bit: one IMAD, bit t = anchor t
+    const int k = 2 * t + 1;
+    pass = pass * 2u + short_filter_test(filt, w64(lb, v, 33 + k - Q) & QK);
+  }
+  return pass;
+}
+
+// Anchored sweep: the candidates of one chunk (each lane's passing anchors), settled in warp
+// rounds (warp-uniform call).
+template <int Q>
+__device__ __forceinline__ void short_anchor_candidates(const MultiArgs& a, const ShortLens& SL,
+                                                        uint32_t pass, int64_t J, uint32_t cur,
+                                                        int lane, uint32_t slots,
+                                                        uint32_t stage_bytes) {
+  const int64_t c0 = J - kR * lane - 32;  // a-space position of the chunk's lookback start
+  unsigned act = __ballot_sync(kFull, pass != 0);
+  if (!act) return;
+  // every candidate window of the chunk lies in the text and in the stage (most chunks):
+  // lookups straight from shared memory without per-window checks
+  const int64_t ys_hi_min = (int64_t)a.grp[a.G - 1].ys_hi;  // the longest length's
+  const bool easy = __all_sync(kFull, cur != 0) && c0 >= (int64_t)a.ys_lo &&
+                    c0 + 32 + kChunk <= ys_hi_min && 32u + kChunk + 16u <= stage_bytes;
+  while (act) {
+    int t = -1;
+    if (pass) {
+      t = __ffs(pass) - 1;
+      pass &= pass - 1;
+    }
+    const int64_t y0 = J + 2 * t + 2 - Q;  // the anchor's window starts: y0 and y0 - 1
+    if (easy) {
+      // bytes [y0 - 1, y0 + 7) in shared memory, as the words of each start
+      uint32_t lo1 = 0, hi1 = 0, lo0 = 0, hi0 = 0;
+      if (t >= 0) {
+        const uint32_t addr = cur + (uint32_t)(y0 - 1 - c0);
+        const uint32_t al = addr & ~3u, r = 8u * (addr & 3u);
+        const uint32_t x0 = lds_u32(al), x1 = lds_u32(al + 4), x2 = lds_u32(al + 8);
+        lo1 = __funnelshift_r(x0, x1, r);
+        hi1 = __funnelshift_r(x1, x2, r);
+        lo0 = __funnelshift_r(lo1, hi1, 8);
+        hi0 = __funnelshift_r(hi1, x2 >> r, 8);
+      }
+#pragma unroll
+      for (int gi = 0; gi < 3; ++gi) {
+        if (gi >= (int)SL.G) break;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          int idx = -1;
+          if (t >= 0) {
+            const uint32_t lo = j ? lo1 : lo0, hw = j ? hi1 : hi0;
+            idx = short_probe(a, slots, lo & SL.klo[gi], hw & SL.khi[gi], SL.L[gi]);
+          }
+          multi_append(a, idx, y0 - j - (int64_t)a.g.amis, lane);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int64_t ya = y0 - j;  // candidate window start, a-space
+        for (uint32_t gi = 0; gi < a.G; ++gi) {
+          const int idx = t >= 0 ? short_lookup(a, slots, cur, c0, stage_bytes, ya,
+                                                a.grp[gi].m, a.grp[gi].ys_hi)
+                                 : -1;
+          multi_append(a, idx, ya - (int64_t)a.g.amis, lane);
+        }
+      }
+    }
+    act = __ballot_sync(kFull, pass != 0);
+  }
+}
+
 template <int Q>
 __device__ __forceinline__ void short_chunk_multi(const MultiArgs& a, const ShortLens& SL,
                                                   const Vec32& v, const uint32_t (&lb)[8],
                                                   int64_t J, uint32_t cur, int lane,
                                                   uint32_t slots, uint32_t filt,
                                                   uint32_t stage_bytes) {
-  const int64_t c0 = J - kR * lane - 32;  // a-space position of the chunk's lookback start
   if constexpr (Q > 0) {
-    // anchored: bit t = the q-gram ending at J + 2t + 1 passed
-    constexpr uint32_t QK = Q >= 4 ? 0xffffffffu : ((1u << (8 * Q)) - 1u);
-    uint32_t pass = 0;
-#pragma unroll
-    for (int t = 15; t >= 0; --t) {  // pass = 2 pass + bit: one IMAD, bit t = anchor t
-      const int k = 2 * t + 1;
-      pass = pass * 2u + short_filter_test(filt, w64(lb, v, 33 + k - Q) & QK);
-    }
-    unsigned act = __ballot_sync(kFull, pass != 0);
-    if (!act) return;
-    // every candidate window of the chunk lies in the text and in the stage (most chunks):
-    // lookups straight from shared memory without per-window checks
-    const int64_t ys_hi_min = (int64_t)a.grp[a.G - 1].ys_hi;  // the longest length's
-    const bool easy = __all_sync(kFull, cur != 0) && c0 >= (int64_t)a.ys_lo &&
-                      c0 + 32 + kChunk <= ys_hi_min && 32u + kChunk + 16u <= stage_bytes;
-    while (act) {
-      int t = -1;
-      if (pass) {
-        t = __ffs(pass) - 1;
-        pass &= pass - 1;
-      }
-      const int64_t y0 = J + 2 * t + 2 - Q;  // the anchor's window starts: y0 and y0 - 1
-      if (easy) {
-        // bytes [y0 - 1, y0 + 7) in shared memory, as the words of each start
-        uint32_t lo1 = 0, hi1 = 0, lo0 = 0, hi0 = 0;
-        if (t >= 0) {
-          const uint32_t addr = cur + (uint32_t)(y0 - 1 - c0);
-          const uint32_t al = addr & ~3u, r = 8u * (addr & 3u);
-          const uint32_t x0 = lds_u32(al), x1 = lds_u32(al + 4), x2 = lds_u32(al + 8);
-          lo1 = __funnelshift_r(x0, x1, r);
-          hi1 = __funnelshift_r(x1, x2, r);
-          lo0 = __funnelshift_r(lo1, hi1, 8);
-          hi0 = __funnelshift_r(hi1, x2 >> r, 8);
-        }
-#pragma unroll
-        for (int gi = 0; gi < 3; ++gi) {
-          if (gi >= (int)SL.G) break;
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            int idx = -1;
-            if (t >= 0) {
-              const uint32_t lo = j ? lo1 : lo0, hw = j ? hi1 : hi0;
-              idx = short_probe(a, slots, lo & SL.klo[gi], hw & SL.khi[gi], SL.L[gi]);
-            }
-            multi_append(a, idx, y0 - j - (int64_t)a.g.amis, lane);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int64_t ya = y0 - j;  // candidate window start, a-space
-          for (uint32_t gi = 0; gi < a.G; ++gi) {
-            const int idx = t >= 0 ? short_lookup(a, slots, cur, c0, stage_bytes, ya,
-                                                  a.grp[gi].m, a.grp[gi].ys_hi)
-                                   : -1;
-            multi_append(a, idx, ya - (int64_t)a.g.amis, lane);
-          }
-        }
-      }
-      act = __ballot_sync(kFull, pass != 0);
-    }
+    short_anchor_candidates<Q>(a, SL, short_anchor_pass<Q>(filt, v, lb), J, cur, lane, slots,
+                               stage_bytes);
   } else {
+    const int64_t c0 = J - kR * lane - 32;  // a-space position of the chunk's lookback start
     // per window end J + k and length L (<= 3): the key's filter test
     for (uint32_t gi = 0; gi < a.G; ++gi) {
       const uint32_t L = a.grp[gi].m;
@@ -506,6 +524,9 @@ __global__ void __launch_bounds__(kMultiBlock) rk_multi_short_kernel(const __gri
   Stream S;
   stream_init(a.g, R, S, (uint32_t)w, (uint32_t)W, lane);
   const ShortLens SL(a);
+  // (the staged structure that speeds up the q-gram kernel -- all of a stage's filter tests
+  // first, then the candidates -- measured slower here: 1024 x m = 5 2079 -> 1968 GB/s,
+  // m = 4 1510 -> 1333; this kernel's candidates are ~1 per KiB, not ~0.03)
   for (uint32_t t = (uint32_t)w; t < (uint32_t)a.g.num_tiles; t += (uint32_t)W) {
     stream_tile<8, false>(a.g, R, S, t, lane,
                           [&](const Vec32& v, const uint32_t (&lb)[8], uint32_t&, int64_t J, int c) {

@@ -134,6 +134,9 @@ __device__ __forceinline__ SlowOut slow_chunk(const ScanArgs& a, int64_t J,
 
 // Patterns shorter than this settle candidates inline (see short_chunk).
 constexpr int kShortInline = 9;
+#ifndef RK_ROLL_UNROLL
+#define RK_ROLL_UNROLL false  // 9 <= m <= 14: the exact-roll chunk loop unrolled per stage
+#endif
 // From this length on, M < 32 filters with the 32-byte fold (see rk_scan_kernel): one
 // false positive per 2^M windows sends ~1 KiB/2^(M-10) of chunks to the exact pass, which
 // beats the exact roll from M = 15 (measured: m = 20 4.74 vs 4.27 TB/s, m = 15 4.54 vs 4.3,
@@ -503,7 +506,7 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
     } else if constexpr (M >= kShortInline) {
       // exact hits are rare (m = 8 printable ASCII: ~2% of chunks): flag chunks, settle
       // them in the exact pass
-      const uint32_t cand = fast_tile<M, false>(a.g, R, S, t, lane, pred);
+      const uint32_t cand = fast_tile<M, RK_ROLL_UNROLL>(a.g, R, S, t, lane, pred);
       finish_tile<M>(a, t, cand, lane, tot);
     } else {
       const uint64_t seq = a.g.seq_base + t;
