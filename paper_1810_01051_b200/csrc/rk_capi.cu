@@ -607,10 +607,11 @@ int rkb::multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_leng
     sw.stab = reserve((uint64_t)th.size * 8 + kShortFilterWords * 4);
     memcpy(blob.data() + sw.stab, slots.data(), (uint64_t)th.size * 8);
     uint32_t* filt = reinterpret_cast<uint32_t*>(blob.data() + sw.stab + (uint64_t)th.size * 8);
+    const uint32_t fbits = short_filter_bits(sw.sq);
     const auto set_bits = [&](uint32_t x) {
       const uint32_t h = short_filter_hash(x);
       filt[short_filter_word(h)] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31)) |
-                                    (RK_SHORT_FILTER_BITS == 3 ? 1u << ((h >> 10) & 31) : 0u);
+                                    (fbits == 3 ? 1u << ((h >> 10) & 31) : 0u);
     };
     for (const Entry& e : es) {
       if (sw.sq) {

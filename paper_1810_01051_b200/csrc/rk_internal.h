@@ -164,23 +164,28 @@ __host__ __device__ __forceinline__ void tiny_slots(uint32_t f, const TinyHash& 
   s1 = f >> t.shift;
   s2 = ((f ^ (f >> 15)) * t.c3) >> t.shift;
 }
-// The sweep's Bloom filter: 4096 32-bit words (16 KiB).  An entry x (an anchored q-gram's
+// The sweep's Bloom filter: 8192 32-bit words (32 KiB).  An entry x (an anchored q-gram's
 // bytes as a little-endian word, or a per-window sweep's tiny_key_hash) is mixed as
 // h = umulhi(x * kGramMul, kFiltMix) and sets bits h, h >> 5 and h >> 10 (mod 32) of word
-// h >> 20: one 32-bit shared-memory load per test, three bits (false positives ~1e-4 at
-// 2048 entries).  The mixing multiplies run on the FMA pipe and leave the bit positions in
+// h >> 19: one 32-bit shared-memory load per test, two or three bits (short_filter_bits).  The mixing multiplies run on the FMA pipe and leave the bit positions in
 // the low bits, where the test's rotates take them without masking.
-constexpr uint32_t kShortFilterWords = 4096;
-constexpr uint32_t kGramMul = 0x9E3779B1u;
-#ifndef RK_SHORT_FILTER_BITS
-#define RK_SHORT_FILTER_BITS 3  // (measured: 3 bits 2089 GB/s at 1024 x m = 5, 2 bits 1840)
+#ifndef RK_SHORT_FILTER_LOG2_WORDS
+#define RK_SHORT_FILTER_LOG2_WORDS 13  // 8192 words = 32 KiB (16 KiB: 1024 x m = 5 -13%)
 #endif
+constexpr uint32_t kShortFilterWords = 1u << RK_SHORT_FILTER_LOG2_WORDS;
+constexpr uint32_t kGramMul = 0x9E3779B1u;
+// bits per entry: 2 for 3-gram sweeps (q = 3, i.e. a set with length 4: its text 3-grams
+// match the patterns' for real ~1/400 anchors, so more bits only cost instructions; 1024 x
+// m = 4: 2.72 -> 2.62 ms), 3 otherwise (1024 x m = 5: 1.92 -> 1.79 ms)
+__host__ __device__ constexpr uint32_t short_filter_bits(uint32_t q) { return q == 3 ? 2u : 3u; }
 __host__ __device__ __forceinline__ uint32_t short_filter_hash(uint32_t x) {
   // both halves of the 64-bit product: every bit depends on every input bit
   const uint64_t p = (uint64_t)x * kGramMul;
   return (uint32_t)p + (uint32_t)(p >> 32);
 }
-__host__ __device__ __forceinline__ uint32_t short_filter_word(uint32_t h) { return h >> 20; }
+__host__ __device__ __forceinline__ uint32_t short_filter_word(uint32_t h) {
+  return h >> (32 - RK_SHORT_FILTER_LOG2_WORDS);
+}
 // anchored sweeps: anchors every 2 bytes, q-gram length q = 3 when the sweep has length 4
 // (q + 2 - 1 <= m), else 4; an occurrence at y holds the q-gram ending at the first anchor
 // e >= y + q - 1, i.e. p[j:j+q] with j in {0, 1}

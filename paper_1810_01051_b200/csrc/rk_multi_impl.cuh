@@ -316,16 +316,17 @@ __device__ __forceinline__ unsigned long long ld_shared_u64(uint32_t a) {
 }
 
 // 1 iff the entry x's three bits are set in the sweep's filter (rk_internal.h)
+template <int Q>
 __device__ __forceinline__ uint32_t short_filter_test(uint32_t filt, uint32_t x) {
   const uint32_t h = short_filter_hash(x);
   const uint32_t w = lds_u32(filt + 4u * short_filter_word(h));
   // rotates take the bit positions mod 32
-#if RK_SHORT_FILTER_BITS == 3
-  return __funnelshift_r(w, w, h) & __funnelshift_r(w, w, h >> 5) &
-         __funnelshift_r(w, w, h >> 10) & 1u;
-#else
-  return __funnelshift_r(w, w, h) & __funnelshift_r(w, w, h >> 5) & 1u;
-#endif
+  if constexpr (short_filter_bits(Q) == 3) {
+    return __funnelshift_r(w, w, h) & __funnelshift_r(w, w, h >> 5) &
+           __funnelshift_r(w, w, h >> 10) & 1u;
+  } else {
+    return __funnelshift_r(w, w, h) & __funnelshift_r(w, w, h >> 5) & 1u;
+  }
 }
 
 // 8 bytes of the text at a-space position p (the bytes of a candidate window): from the
@@ -395,7 +396,7 @@ __device__ __forceinline__ uint32_t short_anchor_pass(uint32_t filt, const Vec32
 #pragma unroll
   for (int t = 15; t >= 0; --t) {  // pass = 2 pass + bit: one IMAD, bit t = anchor t
     const int k = 2 * t + 1;
-    pass = pass * 2u + short_filter_test(filt, w64(lb, v, 33 + k - Q) & QK);
+    pass = pass * 2u + short_filter_test<Q>(filt, w64(lb, v, 33 + k - Q) & QK);
   }
   return pass;
 }
@@ -483,7 +484,7 @@ __device__ __forceinline__ void short_chunk_multi(const MultiArgs& a, const Shor
       for (int k = 31; k >= 0; --k) {
         // the L bytes ending at J + k are the top L bytes of the word ending there
         const uint32_t kb = (w64(lb, v, 29 + k) >> (8 * (4 - L))) & K;
-        pass = pass * 2u + short_filter_test(filt, tiny_key_hash(kb, short_tag(0u, L), a.th));
+        pass = pass * 2u + short_filter_test<0>(filt, tiny_key_hash(kb, short_tag(0u, L), a.th));
       }
       unsigned act = __ballot_sync(kFull, pass != 0);
       while (act) {
