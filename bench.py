@@ -344,7 +344,13 @@ def run_ours(args):
             a, b, hx = plans[m]
             if ev_pairs is not None:
                 ev_pairs[i][0].record(stream)
-            if gloo:
+            if comm is not None:
+                if ev_pairs is None:
+                    continue  # the whole sweep's exchange in one call, below
+                # (the per-length pass times each length's own collective)
+                glob[m] = comm.scan(text, pats[m], a + byte_lo, b + byte_lo, byte_lo,
+                                    cap=cap, out=outs[m], stream=sptr)
+            elif gloo:
                 def scan_fn(t, p, lo, hi, hx=hx):
                     o, k, co, hh = _scan.scan_counts(t, p, hx, lo, hi)
                     return o.cpu(), k, co, hh
@@ -356,13 +362,17 @@ def run_ours(args):
                                            pat_bufs[m].ctypes.data, m, hx, a, b,
                                            outs[m].data_ptr(), cap, byte_lo,
                                            counts[i].data_ptr(), sptr))
-            else:
-                # the C ABI's sharded scan: local scan, counters all-gathered, every rank's
-                # ordered positions broadcast into every rank's output (exact allgather-v)
-                glob[m] = comm.scan(text, pats[m], a + byte_lo, b + byte_lo, byte_lo,
-                                    cap=cap, out=outs[m], stream=sptr)
             if ev_pairs is not None:
                 ev_pairs[i][1].record(stream)
+        if comm is not None and ev_pairs is None:
+            # the C ABI's batched sharded scan: the nine local scans back to back, then one
+            # all-gather of every rank's counters, one host read and one NCCL group of
+            # broadcasts putting every rank's ordered positions into every rank's outputs
+            res = comm.scan_batch(text, [pats[m] for m in sweep],
+                                  [(plans[m][0] + byte_lo, plans[m][1] + byte_lo) for m in sweep],
+                                  byte_lo, [outs[m] for m in sweep], stream=sptr)
+            for m, r in zip(sweep, res):
+                glob[m] = r
         return counts
 
     for _ in range(max(args.warmup, 3)):

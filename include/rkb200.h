@@ -216,6 +216,23 @@ int rk_scan_sharded(rk_comm_t* comm, const uint8_t* text, uint64_t len, uint64_t
                     uint64_t* collisions, uint64_t* hash_hits, void* stream);
 
 /*
+ * rk_scan_sharded_batch -- rk_scan_sharded for P patterns over the same device shard in
+ * one collective: pattern i (h_lengths[i] bytes of h_patterns, hash h_hashes[i]) over its
+ * global windows [win_lo[i], win_hi[i]); its global ordered offsets go to d_outs[i] (a
+ * host array of P device pointers; the list is written only if it fits caps[i] -- else
+ * call again with room) and matches / collisions / hash_hits[i] receive the totals over
+ * all ranks.  The P local scans run back to back, then ONE all-gather of every rank's
+ * counters, one host read and one NCCL group of broadcasts (rk_scan_sharded costs one
+ * host round trip per pattern).  P <= RK_BATCH_MAX_PATTERNS; device texts only.
+ */
+int rk_scan_sharded_batch(rk_comm_t* comm, const uint8_t* d_text, uint64_t len, uint64_t byte_lo,
+                          const uint8_t* h_patterns, const uint32_t* h_lengths,
+                          const uint64_t* h_hashes, uint32_t P, const uint64_t* win_lo,
+                          const uint64_t* win_hi, int64_t* const* d_outs, const uint64_t* caps,
+                          uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits,
+                          void* stream);
+
+/*
  * rk_multi_scan_sharded -- search_multi (matcher.py:125-157) over a text sharded across the
  * communicator's ranks (collective).  Each rank passes the bytes it holds, d_text = global
  * bytes [byte_lo, byte_lo + len) in device memory, and the window starts it owns,

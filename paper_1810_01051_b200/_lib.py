@@ -27,7 +27,7 @@ EXPORTS = (
     "rk_scan_host_fetch", "rk_scan_fetch", "rk_scan_host_batch",
     "rk_multi_scan", "rk_multi_scan_mixed", "rk_window_hashes", "rk_generate", "rk_launch_count",
     "rk_comm_get_unique_id", "rk_comm_init", "rk_comm_destroy", "rk_comm_info", "rk_shard_range",
-    "rk_scan_sharded", "rk_comm_fetch", "rk_multi_scan_sharded",
+    "rk_scan_sharded", "rk_comm_fetch", "rk_multi_scan_sharded", "rk_scan_sharded_batch",
 )
 
 _lib = None
@@ -90,6 +90,9 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.rk_comm_info.argtypes = [vp, pi, pi, pi]
     lib.rk_shard_range.restype = ci
     lib.rk_shard_range.argtypes = [u64, u32, ci, ci, pu64, pu64, pu64, pu64]
+    lib.rk_scan_sharded_batch.restype = ci
+    lib.rk_scan_sharded_batch.argtypes = [vp, u8p, u64, u64, u8p, vp, vp, u32, vp, vp, vp, vp, vp,
+                                          vp, vp, vp]
     lib.rk_multi_scan_sharded.restype = ci
     lib.rk_multi_scan_sharded.argtypes = [vp, u8p, u64, u64, u64, u8p, vp, u32, vp, u64, u64, vp,
                                           vp, u64, pu64, vp]

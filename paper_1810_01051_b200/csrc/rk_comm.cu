@@ -115,6 +115,12 @@ struct rk_comm {
   uint32_t* d_gidx = nullptr;
   uint64_t g_cap = 0;
   uint64_t gathered = 0;                   // offsets of the last sharded scan in d_gather
+  // batched sharded scans: per pattern, this rank's offsets and counters
+  std::vector<int64_t*> b_local;
+  std::vector<uint64_t> b_cap;
+  unsigned long long* d_bcnt = nullptr;     // 4 x RK_BATCH_MAX_PATTERNS, this rank's
+  unsigned long long* d_ballcnt = nullptr;  // every rank's, rank-major
+  unsigned long long* h_ballcnt = nullptr;  // pinned mirror
 };
 
 extern "C" {
@@ -181,6 +187,10 @@ int rk_comm_destroy(rk_comm_t* k) {
   cudaFreeHost(k->h_allcnt);
   cudaFree(k->d_local);
   cudaFree(k->d_gather);
+  for (int64_t* p : k->b_local) cudaFree(p);
+  cudaFree(k->d_bcnt);
+  cudaFree(k->d_ballcnt);
+  cudaFreeHost(k->h_ballcnt);
   cudaFree(k->d_moff);
   cudaFree(k->d_midx);
   cudaFree(k->d_goff);
@@ -318,6 +328,152 @@ int rk_scan_sharded(rk_comm_t* k, const uint8_t* text, uint64_t len, uint64_t by
   if (matches) *matches = total;
   if (hash_hits) *hash_hits = hits;
   if (collisions) *collisions = coll;
+  return RK_OK;
+}
+
+int rk_scan_sharded_batch(rk_comm_t* k, const uint8_t* d_text, uint64_t len, uint64_t byte_lo,
+                          const uint8_t* h_patterns, const uint32_t* h_lengths,
+                          const uint64_t* h_hashes, uint32_t P, const uint64_t* win_lo,
+                          const uint64_t* win_hi, int64_t* const* d_outs, const uint64_t* caps,
+                          uint64_t* matches, uint64_t* collisions, uint64_t* hash_hits,
+                          void* stream) {
+  if (!k) return fail(RK_EINVAL, "communicator is NULL");
+  if (P < 1 || P > RK_BATCH_MAX_PATTERNS)
+    return fail(RK_EINVAL, "pattern count %u outside [1, %d]", P, RK_BATCH_MAX_PATTERNS);
+  if (!h_patterns || !h_lengths || !h_hashes || !win_lo || !win_hi || !d_outs || !caps ||
+      !matches || !collisions || !hash_hits)
+    return fail(RK_EINVAL, "NULL argument array");
+  uint64_t off = 0;
+  std::vector<uint64_t> pat_off(P);
+  for (uint32_t i = 0; i < P; ++i) {
+    const uint32_t m = h_lengths[i];
+    if (m < 1) return fail(RK_EINVAL, "pattern %u is empty", i);
+    pat_off[i] = off;
+    off += m;
+    if (win_hi[i] > win_lo[i]) {
+      if (win_lo[i] < byte_lo || win_hi[i] - byte_lo + m - 1 > len)
+        return fail(RK_EINVAL, "pattern %u: windows [%llu, %llu) need bytes the shard does not "
+                    "hold", i, (unsigned long long)win_lo[i], (unsigned long long)win_hi[i]);
+      if (!d_text) return fail(RK_EINVAL, "text pointer is NULL");
+    }
+    if (caps[i] && !d_outs[i]) return fail(RK_EINVAL, "pattern %u: NULL output", i);
+  }
+  rk_ctx* c = k->ctx;
+  NcclApi& api = nccl();
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d_text && len && !is_device_pointer(d_text, c->device))
+    return fail(RK_EINVAL, "rk_scan_sharded_batch takes device texts of the context's device");
+  if (int r = enter(c, s)) return r;
+  if (!k->d_bcnt) {
+    RK_CUDA(cudaMalloc(&k->d_bcnt, 4ull * RK_BATCH_MAX_PATTERNS * sizeof(unsigned long long)));
+    RK_CUDA(cudaMalloc(&k->d_ballcnt,
+                       4ull * RK_BATCH_MAX_PATTERNS * k->nranks * sizeof(unsigned long long)));
+    RK_CUDA(cudaMallocHost(&k->h_ballcnt,
+                           4ull * RK_BATCH_MAX_PATTERNS * k->nranks * sizeof(unsigned long long)));
+  }
+  if (k->b_local.size() < P) {
+    k->b_local.resize(P, nullptr);
+    k->b_cap.resize(P, 0);
+  }
+  // 1. every pattern's local scan, back to back (no host round trip between them); each
+  //    keeps its ordered offsets in its own buffer (sized by the previous call's counts)
+  const auto local_scan = [&](uint32_t i) -> int {
+    const uint32_t m = h_lengths[i];
+    const uint64_t start = win_hi[i] > win_lo[i] ? win_lo[i] - byte_lo : 0;
+    const uint64_t stop = win_hi[i] > win_lo[i] ? win_hi[i] - byte_lo : 0;
+    if (int r = grow(&k->b_local[i], &k->b_cap[i], 1ull << 12, false, s)) return r;
+    return enqueue_scan(c, d_text, len, h_patterns + pat_off[i], m, h_hashes[i], start, stop,
+                        k->b_local[i], k->b_cap[i], (int64_t)byte_lo, s,
+                        (uint64_t*)(k->d_bcnt + 4ull * i));
+  };
+  for (uint32_t i = 0; i < P; ++i)
+    if (int r = local_scan(i)) return r;
+  // 2. every rank's counters of every pattern -- {matches, hash_hits, collisions, the
+  //    rank's buffer size} -- in one all-gather and one host read.  A pattern with more
+  //    local offsets than its buffer held on some rank makes every rank take a second
+  //    round (the same decision everywhere, from the gathered sizes): that rank scans the
+  //    pattern again with room (later scans reused the per-tile scratch) and the buffer
+  //    keeps the size, so a steady workload pays this once.
+  for (uint32_t i = 0; i < P; ++i) k->h_ballcnt[i] = k->b_cap[i];
+  for (int round = 0;; ++round) {
+    RK_CUDA(cudaMemcpy2DAsync(k->d_bcnt + 3, 4 * sizeof(unsigned long long), k->h_ballcnt,
+                              sizeof(unsigned long long), sizeof(unsigned long long), P,
+                              cudaMemcpyHostToDevice, s));
+    RK_NCCL(api.AllGather(k->d_bcnt, k->d_ballcnt, 4ull * P, ncclUint64, k->comm, s));
+    RK_CUDA(cudaMemcpyAsync(k->h_ballcnt, k->d_ballcnt,
+                            4ull * P * k->nranks * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));
+    RK_CUDA(cudaStreamSynchronize(s));
+    bool again = false;
+    for (int r = 0; r < k->nranks; ++r)
+      for (uint32_t i = 0; i < P; ++i) {
+        const unsigned long long* cr = k->h_ballcnt + 4ull * P * r + 4ull * i;
+        again |= cr[0] > cr[3];
+      }
+    if (!again) break;
+    if (round > 0) return fail(RK_ECUDA, "sharded batch: local offsets overflowed twice");
+    std::vector<uint64_t> need(P);
+    for (uint32_t i = 0; i < P; ++i) need[i] = k->h_ballcnt[4ull * P * k->rank + 4ull * i];
+    for (uint32_t i = 0; i < P; ++i) {
+      if (need[i] <= k->b_cap[i]) continue;
+      if (int r = grow(&k->b_local[i], &k->b_cap[i], need[i], false, s)) return r;
+      if (int r = local_scan(i)) return r;
+    }
+    for (uint32_t i = 0; i < P; ++i) k->h_ballcnt[i] = k->b_cap[i];
+  }
+  // 3. allgather-v of every pattern's offsets, one NCCL group for all of them (every rank
+  //    takes part in every broadcast; a pattern whose list does not fit this rank's cap is
+  //    received into scratch and not written)
+  std::vector<uint64_t> total(P, 0);
+  uint64_t spill = 0;
+  for (uint32_t i = 0; i < P; ++i) {
+    uint64_t hits = 0, coll = 0;
+    for (int r = 0; r < k->nranks; ++r) {
+      const unsigned long long* cr = k->h_ballcnt + 4ull * P * r + 4ull * i;
+      total[i] += cr[0];
+      hits += cr[1];
+      coll += cr[2];
+    }
+    matches[i] = total[i];
+    hash_hits[i] = hits;
+    collisions[i] = coll;
+    if (total[i] > caps[i]) spill += total[i];
+  }
+  if (spill > k->gather_cap) {
+    RK_CUDA(cudaStreamSynchronize(s));
+    cudaFree(k->d_gather);
+    k->d_gather = nullptr;
+    k->gather_cap = 0;
+    RK_CUDA(cudaMalloc(&k->d_gather, spill * sizeof(int64_t)));
+    k->gather_cap = spill;
+  }
+  k->gathered = 0;
+  RK_NCCL(api.GroupStart());
+  uint64_t at = 0;
+  for (uint32_t i = 0; i < P; ++i) {
+    int64_t* recv = d_outs[i];
+    if (total[i] > caps[i]) {
+      recv = k->d_gather + at;
+      at += total[i];
+    }
+    uint64_t prefix = 0;
+    for (int r = 0; r < k->nranks; ++r) {
+      const uint64_t cnt = k->h_ballcnt[4ull * P * r + 4ull * i];
+      if (cnt) {
+        const bool me = r == k->rank;
+        ncclResult_t e = api.Broadcast(me ? (const void*)k->b_local[i] : (const void*)(recv + prefix),
+                                       recv + prefix, cnt, ncclInt64, r, k->comm, s);
+        if (e != ncclSuccess) {
+          api.GroupEnd();
+          return fail(RK_ENCCL, "ncclBroadcast failed: %s", api.GetErrorString(e));
+        }
+      }
+      prefix += cnt;
+    }
+  }
+  RK_NCCL(api.GroupEnd());
   return RK_OK;
 }
 

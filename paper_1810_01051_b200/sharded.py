@@ -272,6 +272,38 @@ class Communicator:
                 out = full
         return out[:k], k, int(co.value), int(hh.value)
 
+    def scan_batch(self, text, patterns, ranges, byte_lo: int, outs, stream=None):
+        """rk_scan_sharded_batch: every pattern over its global windows ``ranges[i] =
+        (win_lo, win_hi)`` of this rank's device shard (global bytes from byte_lo), the
+        global ordered offsets into ``outs[i]`` (CUDA int64 tensors; written only when the
+        list fits) -- one collective for all patterns.  Returns [(offsets view or None,
+        matches, collisions, hash_hits)] per pattern, totals over all ranks."""
+        import numpy as np
+
+        from . import _scan
+        from .rkhash import hash_full
+
+        L = _lib.lib()
+        pats = [_scan._host_bytes(_scan.as_u8(p)) for p in patterns]
+        P = len(pats)
+        flat = np.concatenate(pats)
+        lengths = np.array([p.size for p in pats], dtype=np.uint32)
+        hashes = np.array([hash_full(p.tobytes()) for p in pats], dtype=np.uint64)
+        lo = np.array([r[0] for r in ranges], dtype=np.uint64)
+        hi = np.array([r[1] for r in ranges], dtype=np.uint64)
+        ptrs = np.array([o.data_ptr() for o in outs], dtype=np.uint64)
+        caps = np.array([o.numel() for o in outs], dtype=np.uint64)
+        mt, co, hh = (np.zeros(P, dtype=np.uint64) for _ in range(3))
+        s = _scan._stream(self.device) if stream is None else stream
+        with self.ctx.lock:
+            _lib.check(L.rk_scan_sharded_batch(
+                self.handle, text.data_ptr() if text.numel() else 0, int(text.numel()), byte_lo,
+                flat.ctypes.data, lengths.ctypes.data, hashes.ctypes.data, P, lo.ctypes.data,
+                hi.ctypes.data, ptrs.ctypes.data, caps.ctypes.data, mt.ctypes.data,
+                co.ctypes.data, hh.ctypes.data, s))
+        return [(outs[i][: int(mt[i])] if mt[i] <= caps[i] else None, int(mt[i]), int(co[i]),
+                 int(hh[i])) for i in range(P)]
+
     def multi_scan(self, text, patterns, start_lo: int, start_hi: int, byte_lo: int,
                    n_total: int, *, cap: int = 1 << 16, stream=None):
         """rk_multi_scan_sharded: this rank's window starts [start_lo, start_hi) of the

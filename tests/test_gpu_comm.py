@@ -143,3 +143,33 @@ def test_sharded_multi_pattern(comm):
     for i in range(len(ps)):
         exp = [x for x in full[i].offsets if a <= x < b]
         assert off[idx == i].cpu().tolist() == exp, i
+
+
+def test_sharded_batch(comm):
+    """rk_scan_sharded_batch (one rank): nine patterns over one device shard in one
+    collective equal rk_scan_sharded per pattern, including a dense pattern that overflows
+    its first local buffer (second round) and an output cap below the total (not written,
+    totals still returned)."""
+    import torch
+
+    rng = np.random.default_rng(45)
+    n = 16 << 20
+    host = rng.integers(0, 4, n, dtype=np.uint8) + 65
+    host[(1 << 20): (1 << 20) + 200000] = 65  # an 'AAAA' run: a dense pattern
+    t = torch.from_numpy(host).cuda()
+    pats = [host[x:x + m].tobytes() for x, m in ((100, 4), (5000, 8), (70000, 16), (9 << 20, 32),
+                                                   (123, 64), (4567, 128), (99, 256))]
+    pats += [b"AAAA", b"ACGTACGTTT"]
+    ranges = [(1000, n - len(p) + 1 - 7) for p in pats]
+    outs = [torch.empty(1 << 20, dtype=torch.int64, device="cuda") for _ in pats]
+    outs[-1] = torch.empty(1, dtype=torch.int64, device="cuda")  # too small for its list
+    res = comm.scan_batch(t, pats, ranges, 0, outs)
+    for p, (lo, hi), (offs, k, coll, hits) in zip(pats, ranges, res):
+        e_offs, e_k, e_coll, e_hits = comm.scan(t, p, lo, hi, 0, cap=1 << 20)
+        assert (k, coll, hits) == (e_k, e_coll, e_hits)
+        if offs is not None:
+            assert torch.equal(offs, e_offs)
+    assert res[7][1] > 100000  # the dense one
+    # the second call reuses the grown buffers (a steady workload pays the second round once)
+    res2 = comm.scan_batch(t, pats, ranges, 0, outs)
+    assert [r[1:] for r in res2] == [r[1:] for r in res]
