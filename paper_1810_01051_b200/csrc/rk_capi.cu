@@ -272,6 +272,14 @@ int launch_one(rk_ctx* c, const uint8_t* d_text, uint64_t n, uint32_t m, uint64_
   a.tile_info = x ? x->tile_info : c->d_tile_info;
   a.masks = x ? x->masks : c->d_masks;
   a.pw = pw;
+  {
+    // is hx the pattern's own hash (the normal case)?  Then a window whose bytes equal the
+    // pattern is a hash hit and a match (dense runs settle from the bytes alone)
+    uint64_t h = 0;
+    for (uint32_t i = 0; i < m && i < 32; ++i)
+      h = (h << 1) + ((pw.w[i >> 2] >> (8 * (i & 3))) & 0xffu);
+    a.hx_is_pattern = m <= 8 && h == hx;
+  }
   // A scan with fewer tiles than the full grid has warps (e.g. C1, 1 MiB = 128 tiles
   // against 148 x 20 warps at m = 8) spreads them: every CTA slot gets ceil(tiles / slots)
   // warps, so a 1 MiB scan streams through ~128 SMs instead of 7 full CTAs.

@@ -31,6 +31,7 @@ struct ScanArgs {
   PatWords pw;
   uint32_t warps;                 // warps per CTA launched (<= scan_warps(m): small scans
                                   // spread one or a few warps over every SM)
+  uint32_t hx_is_pattern;         // hx == hash_full(pattern): equal bytes imply a hash hit
 };
 // Shape of the scan kernel per pattern length: m >= 15 (the running fold, the least work
 // per byte) streams 8 KiB stages -- one TMA copy and one ring hand-off per tile -- with 12

@@ -129,6 +129,24 @@ __global__ void __launch_bounds__(32 * scan_warps(M), scan_min_blocks(M))
     // per-lane inline settle of one chunk (dense chunks, edge tiles)
     const auto inline_settle = [&](const Vec32& v, const uint32_t (&lb)[8], int64_t J, int c) {
       uint32_t hm = 0, hits = 0;
+      if (dense && full && a.hx_is_pattern) {
+        // a dense run (C5's all-'a'): when every window of the chunk equals the pattern --
+        // bytes alone, since hx is the pattern's hash -- the chunk is 1024 matches
+        bool all = true;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int s0 = 33 + k - M;
+          all &= (w64(lb, v, s0) & K0) == P0;
+          if constexpr (M > 4) all &= (w64(lb, v, s0 + 4) & K1) == P1;
+        }
+        if (__all_sync(kFull, all)) {
+          my_hits += 32;
+          my_matches += 32;
+          tmask[c * 32 + lane] = 0xffffffffu;
+          hitflags |= 1u << c;
+          return;
+        }
+      }
       if (dense) {
         short_chunk<M, true>(a, v, lb, full, full ? 0xffffffffu : valid_mask(g, J), hm, hits);
       } else {
