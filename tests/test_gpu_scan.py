@@ -569,3 +569,20 @@ def test_search_parallel_device_shards_host_text(gpu):
         assert (st.hash_hits, st.collisions) == (st2.hash_hits, st2.collisions)
         pinned = torch.from_numpy(text).pin_memory()
         assert rk.search_parallel(pinned.numpy(), pat, cfg, 2, devices=[0, 0]) == r
+
+
+def test_search_each_many_patterns(gpu):
+    """More patterns than one rk_scan_host_batch call takes (64): split into batches, each
+    staging the text once; results and stats equal search_sequential's; no patterns: []."""
+    rng = np.random.default_rng(18)
+    text = rng.integers(0, 4, (5 << 20) + 3, dtype=np.uint8)
+    pats = [text[x:x + m].tobytes() for x, m in zip(rng.integers(0, text.size - 64, 70),
+                                                     rng.integers(1, 64, 70))]
+    st = rk.ScanStats()
+    got = rk.search_each(text.tobytes(), pats, stats=st)
+    st2 = rk.ScanStats()
+    assert got == [rk.search_sequential(text.tobytes(), p, stats=st2) for p in pats]
+    assert (st.windows, st.hash_hits, st.collisions) == (st2.windows, st2.hash_hits, st2.collisions)
+    assert rk.search_each(text.tobytes(), []) == []
+    with pytest.raises(ValueError):
+        rk.search_each(text.tobytes(), [b"ab", b""])
