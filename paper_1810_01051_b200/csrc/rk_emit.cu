@@ -4,15 +4,18 @@
 // The scan kernel never waits on other tiles: it leaves, per 8 KiB tile, its match
 // count and chunk bitmap (tile_info), the per-lane hit masks of the chunks that matched
 // (masks), and per-256-tile sums (block_sums).  This kernel turns that into the ordered
-// int64 offsets: block b adds up block_sums[0..b), scans its 256 tile counts, and each
-// warp expands the masks of its tiles with matches into window starts written at their
-// final positions -- ascending, deterministic, no sort, no text re-read.  For sparse
+// int64 offsets: each block adds up the counts before its span of tiles, scans its tile
+// counts, and each warp expands the masks of its tiles with matches into window starts
+// written at their final positions -- ascending, deterministic, no sort, no text re-read.  For sparse
 // matches this is a few microseconds per GiB.
 //
 // Dense outputs (every window matching, BASELINE config C5) are write-bound: a chunk's
 // offsets are staged in shared memory (padded so the lane-strided fill is nearly
-// conflict-free) and written back as contiguous, coalesced 16-byte stores; a chunk whose
-// 1024 windows all match is written directly as an arithmetic run.
+// conflict-free) and written back coalesced; a chunk whose 1024 windows all match is
+// written directly as an arithmetic run of 32-byte stores.  Tiles with >= kDeferMin
+// matches are not expanded by the block whose span holds them but queued, and expanded
+// by whichever warps are free once their own spans are done (dynamic balance: a static
+// split writes at the pace of the slowest SM).
 #include <algorithm>
 
 #include "rk_device.cuh"
@@ -21,18 +24,111 @@
 namespace rkb {
 
 constexpr int kEmitWarps = kEmitTiles / 32;
+#ifndef RK_EMIT_LD
+#define RK_EMIT_LD(p) (*(p))
+#endif
 constexpr int kPadded = kChunk + kChunk / 32;  // 1056 slots: +1 per 32
 
 __device__ __forceinline__ int padded(int i) { return i + (i >> 5); }
 
-__device__ __forceinline__ void st_global_v2(int64_t* p, int64_t a, int64_t b) {
-  asm volatile("st.global.v2.s64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+__device__ __forceinline__ void st_global_v4(int64_t* p, int64_t a) {
+  asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(a + 1),
+               "l"(a + 2), "l"(a + 3)
+               : "memory");
 }
 
-// Expands the hit masks of the tiles with matches among group g's 256 tiles (info = this
-// thread's tile_info, excl = its exclusive match prefix) into ordered offsets.
-__device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t g, uint32_t info,
-                                           uint64_t excl, int64_t* stage, int lane, int warp) {
+// Writes the arithmetic run v0, v0 + 1, ..., v0 + kChunk - 1 to o[0, kChunk) (o 8-byte
+// aligned): up to 3 scalar stores reach a 32-byte boundary, the body goes out as 32-byte
+// stores (STG.256, 1 KiB per warp instruction), then up to 3 scalar stores.  A run's start
+// is rarely aligned: C5's first chunk has 1021 matches, which shifts every later run.
+__device__ __forceinline__ void store_run(int64_t* o, int64_t v0, int lane) {
+  const int head = (int)(((32u - ((uint32_t)(uintptr_t)o & 31u)) & 31u) >> 3);
+  if (lane < head) o[lane] = v0 + lane;
+  int64_t* ob = o + head;
+  const int64_t vb = v0 + head;
+  const int body = (kChunk - head) & ~3;
+#pragma unroll 2
+  for (int i = 4 * lane; i < body; i += 128) st_global_v4(ob + i, vb + i);
+  if (lane < kChunk - head - body) ob[body + lane] = vb + body + lane;
+}
+
+// Loads the hit masks of tile tseq's flagged chunks (one round of independent loads).
+__device__ __forceinline__ void fetch_masks(const EmitArgs& e, uint64_t tseq, uint32_t flags,
+                                            int lane, uint32_t (&dst)[kTileChunks]) {
+  const uint32_t* tm = e.masks + tseq * (kTileChunks * 32);
+#pragma unroll
+  for (int c = 0; c < kTileChunks; ++c) dst[c] = ((flags >> c) & 1u) ? tm[c * 32 + lane] : 0u;
+}
+
+// Writes tile tseq's match offsets (hit masks hms of its flagged chunks) at out[run, ...).
+// The emit's code is kept small (rolled chunk loop): it runs beside the next scan's CTAs,
+// and a 3x larger emit (this expansion unrolled, inlined in both phases) cost that scan
+// 0.7% on the C2 sweep -- instruction-cache pressure, measured.
+__device__ __forceinline__ void expand_tile(const EmitArgs& e, uint64_t tseq, uint32_t flags,
+                                        uint64_t run, const uint32_t (&hms)[kTileChunks],
+                                        int64_t* stage, int lane) {
+  const int64_t tile_a = (int64_t)((e.tile0 + tseq) * (uint64_t)kTile);
+  uint32_t h[kTileChunks];
+#pragma unroll
+  for (int c = 0; c < kTileChunks; ++c) h[c] = hms[c];
+  // a rolled loop over the chunks (the masks rotate through h[0]: registers, not a local
+  // array) keeps the kernel's code small
+#pragma unroll 1
+  for (int c = 0; c < kTileChunks; ++c) {
+    uint32_t hm = h[0];
+#pragma unroll
+    for (int i = 0; i + 1 < kTileChunks; ++i) h[i] = h[i + 1];
+    if (!((flags >> c) & 1u)) continue;
+    const int64_t chunk0 = tile_a + c * kChunk + e.start_bias;  // value of window 0
+    if (__all_sync(kFull, hm == 0xffffffffu)) {
+      // all 1024 windows match: a contiguous arithmetic run
+      const uint64_t lim = e.cap > run ? e.cap - run : 0;
+      int64_t* o = e.out + run;
+      if (run + kChunk <= e.cap && ((uintptr_t)o & 7u) == 0) {
+        store_run(o, chunk0, lane);
+      } else {
+        for (int i = lane; i < kChunk; i += 32)
+          if ((uint64_t)i < lim) e.out[run + i] = chunk0 + i;
+      }
+      run += kChunk;
+      continue;
+    }
+    const uint32_t n = __popc(hm);
+    const uint32_t i2 = warp_incl_scan(n, lane);
+    const uint32_t tot = __shfl_sync(kFull, i2, 31);
+    // stage this chunk's offsets in order, then write them back coalesced
+    int r = (int)(i2 - n);
+    const int64_t v0 = chunk0 + lane * kR;
+    while (hm) {
+      const int k = __ffs(hm) - 1;
+      hm &= hm - 1;
+      stage[padded(r++)] = v0 + k;
+    }
+    __syncwarp();
+    const uint64_t lim = e.cap > run ? e.cap - run : 0;
+    for (int i = lane; i < (int)tot; i += 32)
+      if ((uint64_t)i < lim) e.out[run + i] = stage[padded(i)];
+    __syncwarp();
+    run += tot;
+  }
+}
+
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Expands the hit masks of the tiles with matches among the 256 tiles from sequence number
+// t0 (info = this thread's tile_info, excl = its exclusive match prefix) into ordered offsets.
+// With defer, tiles with at least kDeferMin matches are not expanded here but queued
+// (tile, excl) for the dynamically balanced second phase.
+__device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t t0, uint32_t info,
+                                           uint64_t excl, int64_t* stage, int lane, int warp,
+                                           bool defer) {
   const uint32_t cnt = info & 0xffffu;
   unsigned todo = __ballot_sync(kFull, cnt != 0);
   if (!todo) return;
@@ -41,7 +137,7 @@ __device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t g, uint32
     while (todo) {
       const int j = __ffs(todo) - 1;
       todo &= todo - 1;
-      const uint64_t tseq = g * kEmitTiles + warp * 32 + j;
+      const uint64_t tseq = t0 + warp * 32 + j;
       uint32_t flags = __shfl_sync(kFull, info, j) >> 16;
       const int64_t tile_a = (int64_t)((e.tile0 + tseq) * (uint64_t)kTile);
       const uint32_t* tm = e.masks + tseq * (kTileChunks * 32);
@@ -62,72 +158,79 @@ __device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t g, uint32
     }
     return;
   }
+  if (defer) {
+    const unsigned dense = __ballot_sync(kFull, cnt >= kDeferMin);
+    if (dense) {
+      unsigned long long at = 0;
+      if (lane == 0) at = atomicAdd(&e.work[1], (unsigned long long)__popc(dense));
+      at = __shfl_sync(kFull, at, 0);
+      if ((dense >> lane) & 1u) {
+        const uint64_t i = at + __popc(dense & ((1u << lane) - 1u));
+        e.dq_tile[i] = (uint32_t)(t0 + warp * 32 + lane);
+        st_release(&e.dq_excl[i], excl + 1);  // published after the tile index
+      }
+      todo &= ~dense;
+      if (!todo) return;
+    }
+  }
   // the hit masks of a tile come in one round of independent loads, issued while the
   // previous tile is being expanded (not one load latency per chunk)
   uint32_t hms[kTileChunks], nxt[kTileChunks];
-  auto fetch = [&](int j, uint32_t(&dst)[kTileChunks]) {
-    const uint64_t tseq = g * kEmitTiles + warp * 32 + j;
-    const uint32_t fl = __shfl_sync(kFull, info, j) >> 16;
-    const uint32_t* tm = e.masks + tseq * (kTileChunks * 32);
-#pragma unroll
-    for (int c = 0; c < kTileChunks; ++c) dst[c] = ((fl >> c) & 1u) ? tm[c * 32 + lane] : 0u;
-  };
   int jn = __ffs(todo) - 1;
-  fetch(jn, nxt);
+  fetch_masks(e, t0 + warp * 32 + jn, __shfl_sync(kFull, info, jn) >> 16, lane, nxt);
   while (todo) {
     const int j = jn;
     todo &= todo - 1;
 #pragma unroll
     for (int c = 0; c < kTileChunks; ++c) hms[c] = nxt[c];
     jn = todo ? __ffs(todo) - 1 : -1;
-    if (jn >= 0) fetch(jn, nxt);
-    const uint64_t tseq = g * kEmitTiles + warp * 32 + j;
-    uint32_t flags = __shfl_sync(kFull, info, j) >> 16;
-    uint64_t run = __shfl_sync(kFull, excl, j);
-    const int64_t tile_a = (int64_t)((e.tile0 + tseq) * (uint64_t)kTile);
-#pragma unroll
-    for (int c = 0; c < kTileChunks; ++c) {
-      if (!((flags >> c) & 1u)) continue;
-      uint32_t hm = hms[c];
-      const int64_t chunk0 = tile_a + c * kChunk + e.start_bias;  // value of window 0
-      if (__all_sync(kFull, hm == 0xffffffffu)) {
-        // all 1024 windows match: a contiguous arithmetic run
-        const uint64_t lim = e.cap > run ? e.cap - run : 0;
-        int64_t* o = e.out + run;
-        if (run + kChunk <= e.cap && ((uintptr_t)o & 15u) == 0) {  // 16-byte stores
-#pragma unroll 4
-          for (int i = 2 * lane; i < kChunk; i += 64) st_global_v2(o + i, chunk0 + i, chunk0 + i + 1);
-        } else {
-          for (int i = lane; i < kChunk; i += 32)
-            if ((uint64_t)i < lim) e.out[run + i] = chunk0 + i;
-        }
-        run += kChunk;
-        continue;
-      }
-      const uint32_t n = __popc(hm);
-      const uint32_t i2 = warp_incl_scan(n, lane);
-      const uint32_t tot = __shfl_sync(kFull, i2, 31);
-      // stage this chunk's offsets in order, then write them back coalesced
-      int r = (int)(i2 - n);
-      const int64_t v0 = chunk0 + lane * kR;
-      while (hm) {
-        const int k = __ffs(hm) - 1;
-        hm &= hm - 1;
-        stage[padded(r++)] = v0 + k;
-      }
-      __syncwarp();
-      const uint64_t lim = e.cap > run ? e.cap - run : 0;
-      for (int i = lane; i < (int)tot; i += 32)
-        if ((uint64_t)i < lim) e.out[run + i] = stage[padded(i)];
-      __syncwarp();
-      run += tot;
-    }
+    const uint32_t fl_next = __shfl_sync(kFull, info, jn < 0 ? 0 : jn) >> 16;
+    if (jn >= 0) fetch_masks(e, t0 + warp * 32 + jn, fl_next, lane, nxt);
+    const uint32_t flags = __shfl_sync(kFull, info, j) >> 16;
+    expand_tile(e, t0 + warp * 32 + j, flags, __shfl_sync(kFull, excl, j), hms, stage, lane);
   }
 }
 
-// Block b handles the groups (of kEmitTiles tiles) [b G, (b + 1) G), G = e.groups_per_block,
-// so that a sparse emit is one wave of blocks; the next group's tile_info is loaded while
-// the current one is scanned and expanded.
+// Second phase (scans with dense tiles only): once a block has finished its span, its
+// warps take queued dense tiles one at a time from a ticket counter until the queue is
+// drained and every block has finished its span.  Dense output is write-bound, and
+// statically assigned spans run at the pace of the slowest SM (measured: 6.2 TB/s for a
+// static split of a 2 GiB write against 7.3 for dynamic tickets, tools/write_fronts.cu).
+// Waiting for the other blocks needs them all resident: the grid is one wave of one CTA
+// per SM (launch_emit), and all of them have started before anything else may be
+// scheduled behind them (programmatic launch triggers once every CTA has run).  Entries
+// are zeroed after use and the last block out resets the counters.
+__device__ __forceinline__ void drain_queue(const EmitArgs& e, int64_t* stage, int lane) {
+  for (;;) {
+    unsigned long long t = 0, ex = 0;
+    if (lane == 0) {
+      t = atomicAdd(&e.work[0], 1ull);
+      for (uint32_t spins = 0;; ++spins) {
+        if (t < e.num_tiles) ex = ld_acquire(&e.dq_excl[t]);
+        if (ex) break;
+        if (ld_acquire(&e.work[2]) == gridDim.x && t >= ld_acquire(&e.work[1])) break;
+        if (spins > (1u << 25)) __trap();  // a lost producer: fail loudly, never hang
+        __nanosleep(100);
+      }
+    }
+    ex = __shfl_sync(kFull, ex, 0);
+    if (!ex) return;
+    t = __shfl_sync(kFull, t, 0);
+    const uint64_t tseq = e.dq_tile[t];
+    __syncwarp();
+    if (lane == 0) e.dq_excl[t] = 0ull;
+    const uint32_t flags = e.tile_info[tseq] >> 16;
+    uint32_t hms[kTileChunks];
+    fetch_masks(e, tseq, flags, lane, hms);
+    expand_tile(e, tseq, flags, ex - 1, hms, stage, lane);
+  }
+}
+
+// Block b handles the tiles [b S, (b + 1) S), S = e.tiles_per_block, 256 at a time (the
+// block's starting offset is block_sums over the groups before its
+// span plus the counts of the tiles of its first group that precede it).  The next 256
+// tile_info words are loaded while the current ones are scanned and expanded.  Sparse
+// tiles are expanded in place; dense ones are queued for the balanced second phase.
 __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the scan's writes are visible
   asm volatile("griddepcontrol.launch_dependents;");  // the next scan may be scheduled
@@ -136,18 +239,22 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
   __shared__ uint32_t wsum[kEmitWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int64_t* stage = stage_all + warp * kPadded;
-  const uint64_t G = e.groups_per_block;
-  const uint64_t g0 = (uint64_t)blockIdx.x * G;
-  const uint64_t groups = (e.num_tiles + kEmitTiles - 1) / kEmitTiles;
-  const uint64_t g_end = g0 + G < groups ? g0 + G : groups;
+  const uint64_t S = e.tiles_per_block;
+  const uint64_t t_begin = (uint64_t)blockIdx.x * S;
+  const uint64_t t_end = t_begin + S < e.num_tiles ? t_begin + S : e.num_tiles;
 
-  auto load_info = [&](uint64_t g) -> uint32_t {
-    const uint64_t seq = g * kEmitTiles + tid;
-    return (g < g_end && seq < e.num_tiles) ? e.tile_info[seq] : 0u;
+  auto load_info = [&](uint64_t t) -> uint32_t {
+    const uint64_t seq = t + tid;
+    return seq < t_end ? RK_EMIT_LD(&e.tile_info[seq]) : 0u;
   };
-  uint32_t info = load_info(g0);  // issued with the prefix loads below
+  uint32_t info = load_info(t_begin);  // issued with the prefix loads below
+  const uint64_t gb = t_begin / kEmitTiles;
   unsigned long long pre = 0;
-  for (uint64_t i = tid; i < g0; i += kEmitTiles) pre += e.block_sums[i];
+  for (uint64_t i = tid; i < gb; i += kEmitTiles) pre += RK_EMIT_LD(&e.block_sums[i]);
+  // the balanced phase runs when the scan saw a warp match a dense tile's worth
+  // (counters[3]; every block reads the same flag, so all agree)
+  const bool defer = e.defer_min && e.counters[3] != 0;
+  if (gb * kEmitTiles + tid < t_begin) pre += RK_EMIT_LD(&e.tile_info[gb * kEmitTiles + tid]) & 0xffffu;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(kFull, pre, o);
   if (lane == 0) red[warp] = pre;
@@ -158,12 +265,15 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
   unsigned long long base = 0;
 #pragma unroll
   for (int w = 0; w < kEmitWarps; ++w) base += red[w];
+#ifdef RK_EMIT_DEBUG
+  if (tid == 0) RK_EMIT_DEBUG[blockIdx.x] = base;
+#endif
 
-  for (uint64_t g = g0; g < g_end; ++g) {
-    const uint32_t next = load_info(g + 1);
+  for (uint64_t t = t_begin; t < t_end; t += kEmitTiles) {
+    const uint32_t next = load_info(t + kEmitTiles);
     const uint32_t cnt = info & 0xffffu;
     const uint32_t inc = warp_incl_scan(cnt, lane);
-    __syncthreads();  // wsum of the previous group has been read
+    __syncthreads();  // wsum of the previous round has been read
     if (lane == 31) wsum[warp] = inc;
     __syncthreads();
     uint32_t wpre = 0, gtot = 0;
@@ -173,8 +283,8 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
       gtot += wsum[w];
     }
     const uint64_t excl = base + wpre + inc - cnt;
-    const uint64_t seq = g * kEmitTiles + tid;
-    if (seq == e.num_tiles - 1) {
+    const uint64_t seq = t + tid;
+    if (seq == e.num_tiles - 1 && t_end == e.num_tiles) {  // (seq may run past a span)
       e.counters[0] = excl + cnt;
       if (e.counts_out) {
         e.counts_out[0] = excl + cnt;
@@ -182,9 +292,24 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
         e.counts_out[2] = e.counters[2];
       }
     }
-    emit_group(e, g, info, excl, stage, lane, warp);
+    emit_group(e, t, info, excl, stage, lane, warp, defer);
     base += gtot;
     info = next;
+  }
+  if (defer) {
+    __syncthreads();  // this block's queue entries are all published
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(&e.work[2], 1ull);
+    }
+    drain_queue(e, stage, lane);
+    __syncthreads();  // this block's warps are out of the queue
+    if (tid == 0 && atomicAdd(&e.work[3], 1ull) == gridDim.x - 1) {
+      e.work[0] = 0;  // the last block out: a clean queue for the next emit
+      e.work[1] = 0;
+      e.work[2] = 0;
+      e.work[3] = 0;
+    }
   }
 }
 
@@ -192,25 +317,37 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
 // placed as scan CTAs retire: with a small footprint several would pile onto the first SMs
 // to free up (a dense emit then ran on a third of the SMs, 2.4x slower).  Reserving more
 // than half an SM's shared memory keeps it to one CTA per SM.
+#ifndef RK_EMIT_CTAS
+#define RK_EMIT_CTAS 1  // emit CTAs per SM (the grid is a whole number of waves of these)
+#endif
 #ifndef RK_EMIT_MIN_SMEM_KB
-#define RK_EMIT_MIN_SMEM_KB 116
+#define RK_EMIT_MIN_SMEM_KB (228 / (RK_EMIT_CTAS + 1) + 1)
 #endif
 constexpr size_t kEmitMinSmem = RK_EMIT_MIN_SMEM_KB * 1024;
 #ifndef RK_EMIT_MAX_GROUPS
 #define RK_EMIT_MAX_GROUPS 4
 #endif
-constexpr uint64_t kEmitMaxGroups = RK_EMIT_MAX_GROUPS;  // groups of kEmitTiles per block
+constexpr uint64_t kEmitMaxGroups = RK_EMIT_MAX_GROUPS;  // x kEmitTiles: a block's largest span
 size_t emit_smem_bytes() {
   const size_t b = (size_t)kEmitWarps * kPadded * sizeof(int64_t);
   return b < kEmitMinSmem ? kEmitMinSmem : b;
 }
 
 cudaError_t launch_emit(EmitArgs e, int num_sms, cudaStream_t s) {
-  // one wave of blocks (one per SM, see below) when the scan is up to num_sms groups x G
-  const uint64_t groups = (e.num_tiles + kEmitTiles - 1) / kEmitTiles;
-  const uint64_t sms = num_sms > 0 ? (uint64_t)num_sms : 1;
-  e.groups_per_block = std::max<uint64_t>(1, std::min<uint64_t>(kEmitMaxGroups, (groups + sms - 1) / sms));
-  const uint64_t blocks = (groups + e.groups_per_block - 1) / e.groups_per_block;
+  const uint64_t sms = (num_sms > 0 ? (uint64_t)num_sms : 1) * RK_EMIT_CTAS;
+  const uint64_t tiles = e.num_tiles > 0 ? e.num_tiles : 1;
+  // the dense-tile queue (offsets mode, when the caller provides its buffers; used by the
+  // kernel only if the scan saw a dense tile) needs all blocks resident: one wave
+  e.defer_min = (kDeferMin > 0 && !e.bitmap && e.work && e.dq_excl && e.dq_tile) ? kDeferMin : 0;
+  // Whole waves of one block per SM, each block's span at most kEmitMaxGroups x 256 tiles
+  // and at least 32 (one warp's worth), equal spans: a scan of up to 148 x 4 groups (1.16
+  // GiB) is one wave, which the queue needs (measured against spans of whole groups with
+  // helper blocks for the queue: the same C5, 0.3% faster on the C2 sweep).
+  const uint64_t per_wave = sms * kEmitMaxGroups * kEmitTiles;
+  uint64_t blocks = std::min<uint64_t>(sms * ((tiles + per_wave - 1) / per_wave), (tiles + 31) / 32);
+  e.tiles_per_block = (tiles + blocks - 1) / blocks;
+  blocks = (tiles + e.tiles_per_block - 1) / e.tiles_per_block;
+  if (blocks > sms) e.defer_min = 0;  // the queue needs one wave
   static bool attr[kMaxDevices] = {};  // the smem opt-in is per device
   int dev = 0;
   cudaGetDevice(&dev);

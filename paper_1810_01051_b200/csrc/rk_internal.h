@@ -8,8 +8,10 @@
 //   RK_FOLD_FMA_BYTES    fold filter takes b0/b1 by dp4a instead of PRMT (0)
 //   RK_COOP_FROM         first m with the lane-flag + cooperative settle (5)
 //   RK_UNROLL_FROM       first m whose chunk loop is unrolled per stage (5)
-//   RK_EMIT_MIN_SMEM_KB  emit CTA shared-memory floor, one CTA per SM (116)
-//   RK_EMIT_MAX_GROUPS   groups of 256 tiles one emit block expands (4)
+//   RK_EMIT_MIN_SMEM_KB  emit CTA shared-memory floor, RK_EMIT_CTAS per SM (115)
+//   RK_EMIT_CTAS         emit CTAs per SM (1)
+//   RK_EMIT_MAX_GROUPS   groups of 256 tiles one emit block expands, static schedule (4)
+//   RK_EMIT_DEFER_MIN    matches from which a tile goes to the balanced phase (1024; 0 off)
 //   RK_MULTI_WARPS/STAGE, RK_MULTI_UNROLL   q-gram / tiny multi-pattern kernel shape
 #pragma once
 #include <cstdint>
@@ -92,6 +94,14 @@ int scan_blocks_per_sm(uint32_t m);
 cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t s);
 
 // ordered emission (rk_emit.cu)
+// A tile with at least this many matches is "dense": the emit queues such tiles for a
+// dynamically balanced phase when the scan flagged counters[3] (some warp matched this
+// many in all; rk_emit.cu; 0: off).
+#ifndef RK_EMIT_DEFER_MIN
+#define RK_EMIT_DEFER_MIN 1024
+#endif
+constexpr uint32_t kDeferMin = RK_EMIT_DEFER_MIN;
+
 struct EmitArgs {
   const uint32_t* tile_info;
   const uint32_t* masks;
@@ -107,7 +117,13 @@ struct EmitArgs {
   uint64_t clear_words;
   uint32_t* bitmap;                // bitmap mode: bit (end position + bit_bias) per match
   int64_t bit_bias;
-  uint64_t groups_per_block;       // set by launch_emit
+  uint64_t tiles_per_block;        // set by launch_emit
+  // queue of dense tiles for the balanced second phase (all zero between emits):
+  // work = {ticket, queued, blocks done, blocks out}; dq_excl[i] = excl + 1 of entry i
+  unsigned long long* work;
+  unsigned long long* dq_excl;
+  uint32_t* dq_tile;               // capacity >= num_tiles
+  uint32_t defer_min;              // set by launch_emit (0: no queue)
 };
 cudaError_t launch_emit(EmitArgs e, int num_sms, cudaStream_t s);
 

@@ -401,6 +401,8 @@ __device__ __forceinline__ void flush_totals(const ScanArgs& a, const WarpTotals
   if (lane == 0 && hits) {
     atomicAdd(&a.counters[1], (unsigned long long)hits);
     atomicAdd(&a.counters[2], (unsigned long long)(hits - tot.matches));
+    // counters[3]: some warp matched a dense tile's worth (the emit's balanced phase)
+    if (kDeferMin && tot.matches >= kDeferMin) a.counters[3] = 1ull;
   }
 }
 

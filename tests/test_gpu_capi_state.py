@@ -165,3 +165,36 @@ def test_concurrent_callers_get_their_own_contexts(gpu):
     for t in th:
         t.join()
     assert not errors, errors
+
+
+def test_dense_tiles_queued_with_caps(gpu):
+    """Dense stretches (all 'a') inside a sparse text: the emit queues the dense tiles for
+    its balanced phase and expands the sparse ones in place; the ordered list -- also cut
+    at caps inside dense and sparse tiles, and re-emitted by rk_scan_fetch -- equals the
+    oracle's."""
+    torch = _torch()
+    rng = np.random.default_rng(11)
+    host = rng.integers(0, 4, 24 << 20, dtype=np.uint8) + ord("a")
+    for x, ln in ((1 << 20, 3 << 20), (9 << 20, 1 << 20), ((20 << 20) + 77, 777_777)):
+        host[x:x + ln] = ord("a")
+    text = torch.from_numpy(host).cuda()
+    L = _lib.lib()
+    ctx = _lib.context(0)
+    s = _scan._stream(0)
+    for pat in (b"aa", b"aaaa", b"ab"):
+        p = np.frombuffer(pat, dtype=np.uint8)
+        exp, ecoll = oracle.c_scan(host, p)
+        for cap in (len(exp), len(exp) - 1, (1 << 20) + 5, 1000):
+            out = torch.full((cap,), -1, dtype=torch.int64, device="cuda")
+            mt, co, hh = _lib.u64ref(), _lib.u64ref(), _lib.u64ref()
+            with ctx.lock:
+                _lib.check(L.rk_scan(ctx.handle, text.data_ptr(), text.numel(), p.ctypes.data,
+                                     len(pat), rk.hash_full(pat), 0, text.numel() - len(pat) + 1,
+                                     out.data_ptr(), cap, ctypes.byref(mt), ctypes.byref(co),
+                                     ctypes.byref(hh), s))
+            assert int(mt.value) == len(exp) and int(co.value) == ecoll
+            assert np.array_equal(out.cpu().numpy(), exp[:cap])
+        with ctx.lock:
+            full = torch.empty(len(exp), dtype=torch.int64, device="cuda")
+            _lib.check(L.rk_scan_fetch(ctx.handle, full.data_ptr(), len(exp), s))
+        assert np.array_equal(full.cpu().numpy(), exp)
