@@ -219,8 +219,7 @@ int emit(rk_ctx* c, uint64_t tiles, uint64_t tile0, int64_t start_bias, int64_t*
   e.bitmap = nullptr;
   e.bit_bias = 0;
   e.work = nullptr;
-  e.dq_excl = nullptr;
-  e.dq_tile = nullptr;
+  e.queue = nullptr;
   e.defer_min = 0;
   if (!d_bitmap && d_out && cap) {
     // the dense-tile queue: zeroed once, left zeroed by every emit
@@ -228,11 +227,9 @@ int emit(rk_ctx* c, uint64_t tiles, uint64_t tile0, int64_t start_bias, int64_t*
     if (!c->d_emit_work) {
       if (int r = grow(&c->d_emit_work, &wcap, 4, true, s)) return r;
     }
-    if (int r = grow(&c->d_dq_excl, &c->dq_cap, tiles, true, s)) return r;
-    if (int r = grow(&c->d_dq_tile, &c->dq_tile_cap, tiles, false, s)) return r;
+    if (int r = grow(&c->d_queue, &c->queue_cap, tiles, true, s)) return r;
     e.work = c->d_emit_work;
-    e.dq_excl = c->d_dq_excl;
-    e.dq_tile = c->d_dq_tile;
+    e.queue = c->d_queue;
   }
   if (d_bitmap) {
     e.bitmap = d_bitmap;
@@ -944,8 +941,7 @@ int rk_ctx_destroy(rk_ctx_t* c) {
   cudaFreeHost(c->h_counters);
   cudaFree(c->d_tile_info);
   cudaFree(c->d_emit_work);
-  cudaFree(c->d_dq_excl);
-  cudaFree(c->d_dq_tile);
+  cudaFree(c->d_queue);
   cudaFree(c->d_masks);
   for (auto& sl : c->pat_cache) {
     cudaFree(sl.d);

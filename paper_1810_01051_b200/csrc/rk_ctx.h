@@ -90,9 +90,8 @@ struct rk_ctx {
   unsigned long long* d_mcount = nullptr;    // multi-pattern pair counter
   unsigned long long* h_counters = nullptr;  // pinned mirror
   unsigned long long* d_emit_work = nullptr;  // the emit's dense-tile queue (rk_emit.cu)
-  unsigned long long* d_dq_excl = nullptr;
-  uint32_t* d_dq_tile = nullptr;
-  uint64_t dq_cap = 0, dq_tile_cap = 0;
+  unsigned long long* d_queue = nullptr;
+  uint64_t queue_cap = 0;
   uint32_t* d_tile_info = nullptr;  // per tile: matches | chunk bitmap << 16
   uint64_t tile_info_cap = 0;
   uint32_t* d_masks = nullptr;      // per tile: kTileChunks x 32 lane hit masks

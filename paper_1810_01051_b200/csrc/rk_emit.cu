@@ -113,14 +113,20 @@ __device__ __forceinline__ void expand_tile(const EmitArgs& e, uint64_t tseq, ui
   }
 }
 
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+constexpr int kQueueTileBits = 22;
 
 // Expands the hit masks of the tiles with matches among the 256 tiles from sequence number
 // t0 (info = this thread's tile_info, excl = its exclusive match prefix) into ordered offsets.
@@ -166,8 +172,7 @@ __device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t t0, uint3
       at = __shfl_sync(kFull, at, 0);
       if ((dense >> lane) & 1u) {
         const uint64_t i = at + __popc(dense & ((1u << lane) - 1u));
-        e.dq_tile[i] = (uint32_t)(t0 + warp * 32 + lane);
-        st_release(&e.dq_excl[i], excl + 1);  // published after the tile index
+        st_relaxed(&e.queue[i], ((excl + 1) << kQueueTileBits) | (t0 + warp * 32 + lane));
       }
       todo &= ~dense;
       if (!todo) return;
@@ -200,29 +205,72 @@ __device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t t0, uint3
 // per SM (launch_emit), and all of them have started before anything else may be
 // scheduled behind them (programmatic launch triggers once every CTA has run).  Entries
 // are zeroed after use and the last block out resets the counters.
-__device__ __forceinline__ void drain_queue(const EmitArgs& e, int64_t* stage, int lane) {
-  for (;;) {
-    unsigned long long t = 0, ex = 0;
-    if (lane == 0) {
-      t = atomicAdd(&e.work[0], 1ull);
-      for (uint32_t spins = 0;; ++spins) {
-        if (t < e.num_tiles) ex = ld_acquire(&e.dq_excl[t]);
-        if (ex) break;
-        if (ld_acquire(&e.work[2]) == gridDim.x && t >= ld_acquire(&e.work[1])) break;
-        if (spins > (1u << 25)) __trap();  // a lost producer: fail loudly, never hang
-        __nanosleep(100);
-      }
+__device__ __forceinline__ unsigned long long claim_ticket(const EmitArgs& e, int lane) {
+  unsigned long long t = 0;
+  if (lane == 0) t = atomicAdd(&e.work[0], 1ull);
+  return __shfl_sync(kFull, t, 0);
+}
+
+// Entry t once published, or 0 when the queue is drained and every block has
+// finished its span (blocking: lane 0 spins on the entry and the done count).
+__device__ __forceinline__ unsigned long long wait_entry(const EmitArgs& e, unsigned long long t,
+                                                         int lane) {
+  unsigned long long ex = 0;
+  if (lane == 0) {
+    for (uint32_t spins = 0;; ++spins) {
+      if (t < e.num_tiles) ex = ld_relaxed(&e.queue[t]);
+      if (ex) break;
+      if (ld_acquire(&e.work[2]) == gridDim.x && t >= ld_acquire(&e.work[1])) break;
+      if (spins > (1u << 25)) __trap();  // a lost producer: fail loudly, never hang
+      __nanosleep(100);
     }
-    ex = __shfl_sync(kFull, ex, 0);
-    if (!ex) return;
-    t = __shfl_sync(kFull, t, 0);
-    const uint64_t tseq = e.dq_tile[t];
+  }
+  return __shfl_sync(kFull, ex, 0);
+}
+
+// Entry t if already published, else 0 (non-blocking probe).
+__device__ __forceinline__ unsigned long long probe_entry(const EmitArgs& e, unsigned long long t,
+                                                          int lane) {
+  unsigned long long ex = 0;
+  if (lane == 0 && t < e.num_tiles) ex = ld_relaxed(&e.queue[t]);
+  return __shfl_sync(kFull, ex, 0);
+}
+
+struct QueuedTile {
+  uint64_t tseq;
+  uint32_t flags;
+  uint32_t hms[kTileChunks];
+};
+
+__device__ __forceinline__ void load_entry(const EmitArgs& e, unsigned long long ex, int lane,
+                                           QueuedTile& q) {
+  q.tseq = ex & ((1ull << kQueueTileBits) - 1);
+  q.flags = e.tile_info[q.tseq] >> 16;
+  fetch_masks(e, q.tseq, q.flags, lane, q.hms);
+}
+
+__device__ __forceinline__ void drain_queue(const EmitArgs& e, int64_t* stage, int lane) {
+  // software-pipelined: the next ticket is claimed, and its entry loaded if already
+  // published, before the current tile is expanded (a tile's claim-and-load chain is a
+  // few microseconds of latency against ~10 of writing it)
+  unsigned long long t = claim_ticket(e, lane);
+  unsigned long long ex = wait_entry(e, t, lane);
+  QueuedTile cur, nxt;
+  if (ex) load_entry(e, ex, lane, cur);
+  while (ex) {
+    const unsigned long long t2 = claim_ticket(e, lane);
+    unsigned long long ex2 = probe_entry(e, t2, lane);
+    if (ex2) load_entry(e, ex2, lane, nxt);
     __syncwarp();
-    if (lane == 0) e.dq_excl[t] = 0ull;
-    const uint32_t flags = e.tile_info[tseq] >> 16;
-    uint32_t hms[kTileChunks];
-    fetch_masks(e, tseq, flags, lane, hms);
-    expand_tile(e, tseq, flags, ex - 1, hms, stage, lane);
+    if (lane == 0) e.queue[t] = 0ull;  // consumed: the queue is left zeroed
+    expand_tile(e, cur.tseq, cur.flags, (ex >> kQueueTileBits) - 1, cur.hms, stage, lane);
+    if (!ex2) {
+      ex2 = wait_entry(e, t2, lane);
+      if (ex2) load_entry(e, ex2, lane, nxt);
+    }
+    t = t2;
+    ex = ex2;
+    cur = nxt;
   }
 }
 
@@ -338,7 +386,7 @@ cudaError_t launch_emit(EmitArgs e, int num_sms, cudaStream_t s) {
   const uint64_t tiles = e.num_tiles > 0 ? e.num_tiles : 1;
   // the dense-tile queue (offsets mode, when the caller provides its buffers; used by the
   // kernel only if the scan saw a dense tile) needs all blocks resident: one wave
-  e.defer_min = (kDeferMin > 0 && !e.bitmap && e.work && e.dq_excl && e.dq_tile) ? kDeferMin : 0;
+  e.defer_min = (kDeferMin > 0 && !e.bitmap && e.work && e.queue) ? kDeferMin : 0;
   // Whole waves of one block per SM, each block's span at most kEmitMaxGroups x 256 tiles
   // and at least 32 (one warp's worth), equal spans: a scan of up to 148 x 4 groups (1.16
   // GiB) is one wave, which the queue needs (measured against spans of whole groups with
@@ -347,7 +395,7 @@ cudaError_t launch_emit(EmitArgs e, int num_sms, cudaStream_t s) {
   uint64_t blocks = std::min<uint64_t>(sms * ((tiles + per_wave - 1) / per_wave), (tiles + 31) / 32);
   e.tiles_per_block = (tiles + blocks - 1) / blocks;
   blocks = (tiles + e.tiles_per_block - 1) / e.tiles_per_block;
-  if (blocks > sms) e.defer_min = 0;  // the queue needs one wave
+  if (blocks > sms || tiles >= (1ull << kQueueTileBits)) e.defer_min = 0;  // one wave
   static bool attr[kMaxDevices] = {};  // the smem opt-in is per device
   int dev = 0;
   cudaGetDevice(&dev);

@@ -119,10 +119,11 @@ struct EmitArgs {
   int64_t bit_bias;
   uint64_t tiles_per_block;        // set by launch_emit
   // queue of dense tiles for the balanced second phase (all zero between emits):
-  // work = {ticket, queued, blocks done, blocks out}; dq_excl[i] = excl + 1 of entry i
+  // work = {ticket, queued, blocks done, blocks out}; queue[i] = (excl + 1) << 22 | tile
+  // (one word: read with a relaxed load, no acquire -- whose L1 invalidation per entry
+  // stalled the stores); capacity >= num_tiles (< 2^22 whenever the queue is used)
   unsigned long long* work;
-  unsigned long long* dq_excl;
-  uint32_t* dq_tile;               // capacity >= num_tiles
+  unsigned long long* queue;
   uint32_t defer_min;              // set by launch_emit (0: no queue)
 };
 cudaError_t launch_emit(EmitArgs e, int num_sms, cudaStream_t s);

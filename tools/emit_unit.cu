@@ -37,10 +37,8 @@ int main() {
     cudaMalloc(&d_bs, bs.size() * 8);
     cudaMalloc(&d_cnt, 32);
     unsigned long long *d_work, *d_dq;
-    uint32_t* d_dqt;
     cudaMalloc(&d_work, 32);
     cudaMalloc(&d_dq, tiles * 8);
-    cudaMalloc(&d_dqt, tiles * 4);
     cudaMemset(d_work, 0, 32);
     cudaMemset(d_dq, 0, tiles * 8);
     int64_t* d_out;
@@ -63,8 +61,7 @@ int main() {
         e.out = d_out;
         e.cap = 8;
         e.work = d_work;
-        e.dq_excl = d_dq;
-        e.dq_tile = d_dqt;
+        e.queue = d_dq;
       }
       cudaError_t err = launch_emit(e, sms, 0);
       if (err == cudaSuccess) err = cudaDeviceSynchronize();
@@ -103,7 +100,7 @@ int main() {
       }
     }
     cudaFree(d_info); cudaFree(d_masks); cudaFree(d_bs); cudaFree(d_cnt);
-    cudaFree(d_work); cudaFree(d_dq); cudaFree(d_dqt); cudaFree(d_out);
+    cudaFree(d_work); cudaFree(d_dq); cudaFree(d_out);
   }
   printf("emit_unit bad=%d\n", bad);
   return bad != 0;

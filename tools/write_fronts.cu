@@ -68,6 +68,48 @@ __global__ void tickets(int64_t* o, uint64_t n, int64_t v) {
     for (int k = 0; k < UKB * 128 / ((int)blockDim.x * 4); ++k) st4(p + k * blockDim.x * 4, v);
   }
 }
+// warp-level tickets: a warp claims a U KiB unit and writes it 8 KiB (1024 values) at a
+// time, STG.256 (the emit's balanced phase)
+__device__ unsigned long long g_wticket;
+template <int UKB>
+__global__ void warp_tickets(int64_t* o, uint64_t n, int64_t v) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nu = n / (UKB * 128);
+  for (;;) {
+    unsigned long long u = 0;
+    if (lane == 0) u = atomicAdd(&g_wticket, 1ull);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= nu) break;
+    int64_t* p = o + u * (UKB * 128);
+    for (int c = 0; c < UKB * 128; c += 1024)
+#pragma unroll 2
+      for (int i = 4 * lane; i < 1024; i += 128) st4(p + c + i, v + c + i);
+  }
+}
+// the same with every 8 KiB run starting 3 values past a 32-byte boundary: up to 3
+// scalar stores, the 32-byte body, then the tail (the emit's store_run on C5's offsets)
+template <int UKB>
+__global__ void warp_tickets_mis(int64_t* o, uint64_t n, int64_t v) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nu = n / (UKB * 128) - 1;
+  for (;;) {
+    unsigned long long u = 0;
+    if (lane == 0) u = atomicAdd(&g_wticket, 1ull);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= nu) break;
+    int64_t* p = o + 3 + u * (UKB * 128);
+    for (int c = 0; c < UKB * 128; c += 1024) {
+      int64_t* q = p + c;
+      const int head = (int)(((32u - ((uint32_t)(uintptr_t)q & 31u)) & 31u) >> 3);
+      if (lane < head) q[lane] = v + lane;
+      int64_t* ob = q + head;
+      const int body = (1024 - head) & ~3;
+#pragma unroll 2
+      for (int i = 4 * lane; i < body; i += 128) st4(ob + i, v + i);
+      if (lane < 1024 - head - body) ob[body + lane] = v + body + lane;
+    }
+  }
+}
 // the same pattern, grid-stride over 8 KiB blocks with a persistent grid
 __global__ void torch_like_persist(int64_t* o, uint64_t nb, int64_t v) {
   for (uint64_t b = blockIdx.x; b < nb; b += gridDim.x) {
@@ -146,6 +188,14 @@ int main() {
   run10("tickets 512KiB 256thr 148x1", [&] { zt(); tickets<512><<<148, 256>>>(o, n, 7); });
   run10("tickets 2MiB 256thr 148x1", [&] { zt(); tickets<2048><<<148, 256>>>(o, n, 7); });
   run10("tickets 64KiB 1024thr 148x2", [&] { zt(); tickets<64><<<148 * 2, 1024>>>(o, n, 7); });
+  auto zw = [&] { unsigned long long z = 0; cudaMemcpyToSymbolAsync(g_wticket, &z, 8); };
+  run10("warp tickets 64KiB 148x256", [&] { zw(); warp_tickets<64><<<148, 256>>>(o, n, 7); });
+  run10("warp tickets mis 64KiB 148x256", [&] { zw(); warp_tickets_mis<64><<<148, 256>>>(o, n, 7); });
+  run10("warp tickets 64KiB 148x512", [&] { zw(); warp_tickets<64><<<148, 512>>>(o, n, 7); });
+  run10("warp tickets 64KiB 148x1024", [&] { zw(); warp_tickets<64><<<148, 1024>>>(o, n, 7); });
+  run10("warp tickets 64KiB 296x1024", [&] { zw(); warp_tickets<64><<<296, 1024>>>(o, n, 7); });
+  run10("warp tickets 8KiB 148x256", [&] { zw(); warp_tickets<8><<<148, 256>>>(o, n, 7); });
+  run10("warp tickets 512KiB 148x256", [&] { zw(); warp_tickets<512><<<148, 256>>>(o, n, 7); });
   run10("torch-like permuted", [&] { torch_like_perm<<<n / 1024, 128>>>(o, 18, 7); });
   run10("blocks 64KiB x256thr", [&] { big_blocks<64><<<n / (64 * 128), 256>>>(o, 7); });
   run10("blocks 64KiB x1024thr", [&] { big_blocks<64><<<n / (64 * 128), 1024>>>(o, 7); });
