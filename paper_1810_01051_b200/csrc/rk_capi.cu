@@ -631,8 +631,7 @@ int rkb::multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_leng
     const uint32_t fbits = short_filter_bits(sw.sq);
     const auto set_bits = [&](uint32_t x) {
       const uint32_t h = short_filter_hash(x);
-      filt[short_filter_word(h)] |= (1u << (h & 31)) | (1u << ((h >> 5) & 31)) |
-                                    (fbits == 3 ? 1u << ((h >> 10) & 31) : 0u);
+      filt[short_filter_word(h)] |= short_filter_bit_set(h, fbits);
     };
     for (const Entry& e : es) {
       if (sw.sq) {
@@ -645,6 +644,7 @@ int rkb::multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_leng
           memcpy(&gram, pb + j, sw.sq);
           set_bits(gram);
         }
+        if (RK_SHORT_KEY_REFINE && sw.sq == 3) set_bits(e.lo ^ kShortKeySalt);  // 4-byte prefix
       } else {
         set_bits(tiny_key_hash(e.lo, short_tag(0u, e.len), th));
       }

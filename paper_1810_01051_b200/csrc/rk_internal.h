@@ -196,6 +196,12 @@ constexpr uint32_t kGramMul = 0x9E3779B1u;
 // match the patterns' for real ~1/400 anchors, so more bits only cost instructions; 1024 x
 // m = 4: 2.72 -> 2.62 ms), 3 otherwise (1024 x m = 5: 1.92 -> 1.79 ms)
 __host__ __device__ constexpr uint32_t short_filter_bits(uint32_t q) { return q == 3 ? 2u : 3u; }
+// 3-gram sweeps also hold every pattern's first 4 bytes ^ this salt in their filter: a
+// passing anchor's windows are tested on their prefixes before the settle
+#ifndef RK_SHORT_KEY_REFINE
+#define RK_SHORT_KEY_REFINE 1
+#endif
+constexpr uint32_t kShortKeySalt = 0x5BD1E995u;
 __host__ __device__ __forceinline__ uint32_t short_filter_hash(uint32_t x) {
   // both halves of the 64-bit product: every bit depends on every input bit
   const uint64_t p = (uint64_t)x * kGramMul;
@@ -203,6 +209,11 @@ __host__ __device__ __forceinline__ uint32_t short_filter_hash(uint32_t x) {
 }
 __host__ __device__ __forceinline__ uint32_t short_filter_word(uint32_t h) {
   return h >> (32 - RK_SHORT_FILTER_LOG2_WORDS);
+}
+// The bits an entry with hash h sets in its filter word: h, h >> 5 (and h >> 10), mod 32.
+inline uint32_t short_filter_bit_set(uint32_t h, uint32_t bits) {
+  const auto rot = [](uint32_t b) { return 1u << (b & 31); };
+  return rot(h) | rot(h >> 5) | (bits == 3 ? rot(h >> 10) : 0u);
 }
 // anchored sweeps: anchors every 2 bytes, q-gram length q = 3 when the sweep has length 4
 // (q + 2 - 1 <= m), else 4; an occurrence at y holds the q-gram ending at the first anchor
