@@ -644,7 +644,7 @@ int rkb::multi_plan(rk_ctx* c, const uint8_t* h_patterns, const uint32_t* h_leng
           memcpy(&gram, pb + j, sw.sq);
           set_bits(gram);
         }
-        if (RK_SHORT_KEY_REFINE && sw.sq == 3) set_bits(e.lo ^ kShortKeySalt);  // 4-byte prefix
+        if (short_refined(sw.sq)) set_bits(e.lo ^ kShortKeySalt);  // the 4-byte prefix
       } else {
         set_bits(tiny_key_hash(e.lo, short_tag(0u, e.len), th));
       }

@@ -195,13 +195,23 @@ constexpr uint32_t kGramMul = 0x9E3779B1u;
 // bits per entry: 2 for 3-gram sweeps (q = 3, i.e. a set with length 4: its text 3-grams
 // match the patterns' for real ~1/400 anchors, so more bits only cost instructions; 1024 x
 // m = 4: 2.72 -> 2.62 ms), 3 otherwise (1024 x m = 5: 1.92 -> 1.79 ms)
-__host__ __device__ constexpr uint32_t short_filter_bits(uint32_t q) { return q == 3 ? 2u : 3u; }
 // 3-gram sweeps also hold every pattern's first 4 bytes ^ this salt in their filter: a
 // passing anchor's windows are tested on their prefixes before the settle
 #ifndef RK_SHORT_KEY_REFINE
 #define RK_SHORT_KEY_REFINE 1
 #endif
 constexpr uint32_t kShortKeySalt = 0x5BD1E995u;
+#ifndef RK_SHORT_Q4_BITS
+#define RK_SHORT_Q4_BITS 3
+#endif
+__host__ __device__ constexpr uint32_t short_filter_bits(uint32_t q) {
+  return q == 3 ? 2u : (q == 4 ? (uint32_t)RK_SHORT_Q4_BITS : 3u);
+}
+// anchored sweeps whose passing anchors are refined on the windows' 4-byte prefixes
+__host__ __device__ constexpr bool short_refined(uint32_t q) {
+  return RK_SHORT_KEY_REFINE && (q == 3 || (q == 4 && RK_SHORT_Q4_BITS == 2));
+}
+
 __host__ __device__ __forceinline__ uint32_t short_filter_hash(uint32_t x) {
   // both halves of the 64-bit product: every bit depends on every input bit
   const uint64_t p = (uint64_t)x * kGramMul;

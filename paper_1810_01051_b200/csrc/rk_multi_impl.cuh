@@ -401,13 +401,12 @@ __device__ __forceinline__ uint32_t short_anchor_pass(uint32_t filt, const Vec32
     const int k = 2 * t + 1;
     pass = pass * 2u + short_filter_test<Q>(filt, w64(lb, v, 33 + k - Q) & QK);
   }
-#if RK_SHORT_KEY_REFINE
-  if constexpr (Q == 3) {
+  if constexpr (short_refined(Q)) {
     // 3-gram sweeps: the text's 3-grams equal the patterns' for real at ~1/400 anchors, so
     // a passing anchor's two windows are first tested on their 4-byte prefixes (the same
     // filter also holds every pattern's first 4 bytes, salted): ~1/1000 of them go on to
-    // the warp-round settle.  The prefix of window y0 (j = 0) of the last anchor ends one
-    // byte past this lane's 32: the next lane's first byte (lane 31: kept untested).
+    // the warp-round settle.  For q = 3 the prefix of window y0 of the last anchor ends
+    // one byte past this lane's 32: the next lane's first byte (lane 31: kept untested).
     if (__any_sync(kFull, pass != 0)) {
       const uint32_t nxt = __shfl_down_sync(kFull, v.w[0], 1);
       const int lane = threadIdx.x & 31;
@@ -416,11 +415,11 @@ __device__ __forceinline__ uint32_t short_anchor_pass(uint32_t filt, const Vec32
       for (int t = 0; t < 16; ++t) {
         if (!((pass >> t) & 1u)) continue;
         const int k = 2 * t + 1;
-        const uint32_t k1 = w64(lb, v, 29 + k);  // window y0 - 1: bytes 29 + k .. 32 + k
-        uint32_t ok = short_filter_test<Q>(filt, k1 ^ kShortKeySalt);
-        if (t < 15) {
-          ok |= short_filter_test<Q>(filt, w64(lb, v, 30 + k) ^ kShortKeySalt);
-        } else {
+        // window y0 - 1 starts at byte 32 + k - Q of (lb, v), window y0 one byte later
+        uint32_t ok = short_filter_test<Q>(filt, w64(lb, v, 32 + k - Q) ^ kShortKeySalt);
+        if (36 + k - Q <= 63) {
+          ok |= short_filter_test<Q>(filt, w64(lb, v, 33 + k - Q) ^ kShortKeySalt);
+        } else {  // Q = 3, the last anchor: bytes 61..63 and the next lane's first
           ok |= lane == 31 ? 1u
                            : short_filter_test<Q>(filt, __funnelshift_r(v.w[7], nxt, 8) ^ kShortKeySalt);
         }
@@ -429,7 +428,6 @@ __device__ __forceinline__ uint32_t short_anchor_pass(uint32_t filt, const Vec32
       pass = keep;
     }
   }
-#endif
   return pass;
 }
 
