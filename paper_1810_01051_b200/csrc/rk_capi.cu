@@ -818,72 +818,34 @@ int multi_enqueue(rk_ctx* c, const uint8_t* d_text, uint64_t n, uint64_t start_l
   return RK_OK;
 }
 
-// Orders the k pairs of d_off / d_idx by (caller index, offset) -- the reference's
-// per-pattern ascending lists: on the host when they fit one round trip (the count and a
-// prefix come back together), else by the device radix sort.  Offsets < n, indices < P.
-// *total receives the pair count (which may exceed cap: only cap were written).
-// Orders k pairs of d_off / d_idx by (caller index, offset) -- the reference's per-pattern
-// ascending lists -- given the first min(k, kMultiPrefix) of them already in
-// c->h_mresult (offsets at +1, indices at +1+kMultiPrefix): on the host when they all
-// are, else by the device radix sort.  Offsets < n, indices < P.
+// Orders k pairs of d_off / d_idx (k known on the host) by (caller index, offset) -- the
+// reference's per-pattern ascending lists: one block in shared memory up to kSmallSort
+// pairs, else the device radix sort.  Offsets < n, indices < P.
 int order_pairs(rk_ctx* c, int64_t* d_off, uint32_t* d_idx, uint64_t k, uint64_t n, uint32_t P,
                 cudaStream_t s) {
-  if (k > kMultiPrefix) {  // too many for a host round trip: radix-sort the pairs on the device
+  if (k > kSmallSort) {
     const size_t need = sort_pairs_scratch(k);
     if (int r = grow(&c->d_sort, &c->sort_cap, (uint64_t)need, false, s)) return r;
     RK_CUDA(sort_pairs(d_off, d_idx, k, n, P, c->d_sort, c->sort_cap, s));
   } else if (k > 1) {
-    std::vector<int64_t> off(k);
-    std::vector<uint32_t> idx(k);
-    memcpy(off.data(), c->h_mresult + 1, k * sizeof(int64_t));
-    memcpy(idx.data(), c->h_mresult + 1 + kMultiPrefix, k * sizeof(uint32_t));
-    std::vector<uint64_t> perm(k);
-    for (uint64_t i = 0; i < k; ++i) perm[i] = i;
-    std::sort(perm.begin(), perm.end(), [&](uint64_t x, uint64_t y) {
-      return idx[x] != idx[y] ? idx[x] < idx[y] : off[x] < off[y];
-    });
-    bool sorted = true;
-    for (uint64_t i = 0; i < k && sorted; ++i) sorted = perm[i] == i;
-    if (!sorted) {
-      std::vector<int64_t> off2(k);
-      std::vector<uint32_t> idx2(k);
-      for (uint64_t i = 0; i < k; ++i) {
-        off2[i] = off[perm[i]];
-        idx2[i] = idx[perm[i]];
-      }
-      // pageable sources: each call returns once its bytes are staged
-      RK_CUDA(cudaMemcpyAsync(d_off, off2.data(), k * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-      RK_CUDA(cudaMemcpyAsync(d_idx, idx2.data(), k * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-    }
+    RK_CUDA(small_sort_pairs(d_off, d_idx, nullptr, k, k, n, nullptr, s));
   }
   return RK_OK;
 }
 
-// Copies the first min(k, kMultiPrefix) pairs into c->h_mresult (synchronising s).
-int fetch_pair_prefix(rk_ctx* c, const int64_t* d_off, const uint32_t* d_idx, uint64_t k,
-                      cudaStream_t s) {
-  const uint64_t pre = std::min<uint64_t>(k, kMultiPrefix);
-  if (pre) {
-    RK_CUDA(cudaMemcpyAsync(c->h_mresult + 1, d_off, pre * sizeof(int64_t),
-                            cudaMemcpyDeviceToHost, s));
-    RK_CUDA(cudaMemcpyAsync(c->h_mresult + 1 + kMultiPrefix, d_idx, pre * sizeof(uint32_t),
-                            cudaMemcpyDeviceToHost, s));
-  }
-  RK_CUDA(cudaStreamSynchronize(s));
-  return RK_OK;
-}
-
-// The pair count (from d_count) and a prefix of the pairs come back in one round trip;
-// then the first min(count, cap) pairs are ordered (order_pairs).  *total_out receives the
-// count, which may exceed cap: only cap pairs were written.
+// The same for pairs whose count is on the device (d_count): the one-block sort reads it
+// there and writes it to the pinned result word (mapped, no copy); the host waits once,
+// and only a set above kSmallSort pairs needs the radix sort after that.  *total_out
+// receives the pair count (which may exceed cap: only cap were written).
 int multi_order(rk_ctx* c, int64_t* d_off, uint32_t* d_idx, uint64_t cap, uint64_t n, uint32_t P,
                 const unsigned long long* d_count, uint64_t* total_out, cudaStream_t s) {
-  RK_CUDA(cudaMemcpyAsync(c->h_mresult, d_count, sizeof(unsigned long long),
-                          cudaMemcpyDeviceToHost, s));
-  if (int r = fetch_pair_prefix(c, d_off, d_idx, cap, s)) return r;
-  const uint64_t total = c->h_mresult[0];
+  c->h_mresult[0] = 0;
+  RK_CUDA(small_sort_pairs(d_off, d_idx, d_count, 0, cap, n, c->h_mresult, s));
+  RK_CUDA(cudaStreamSynchronize(s));
+  const uint64_t total = *(volatile unsigned long long*)c->h_mresult;
   *total_out = total;
-  return order_pairs(c, d_off, d_idx, std::min(total, cap), n, P, s);
+  const uint64_t k = std::min(total, cap);
+  return k > kSmallSort ? order_pairs(c, d_off, d_idx, k, n, P, s) : RK_OK;
 }
 
 }  // namespace rkb
@@ -921,8 +883,7 @@ int rk_ctx_create(int device, rk_ctx_t** out) {
   c->num_sms = prop.multiProcessorCount;
   RK_CUDA(cudaMalloc(&c->d_mcount, sizeof(unsigned long long)));
   RK_CUDA(cudaMallocHost(&c->h_counters, 4 * sizeof(unsigned long long)));
-  RK_CUDA(cudaMallocHost(&c->h_mresult, (1 + kMultiPrefix) * sizeof(unsigned long long) +
-                                            kMultiPrefix * sizeof(uint32_t)));
+  RK_CUDA(cudaMallocHost(&c->h_mresult, 4 * sizeof(unsigned long long)));
   RK_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
   RK_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
   for (auto& e : c->ev_copied) RK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

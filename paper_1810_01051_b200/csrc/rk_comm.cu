@@ -594,7 +594,6 @@ int rk_multi_scan_sharded(rk_comm_t* k, const uint8_t* d_text, uint64_t len, uin
   }
   RK_NCCL(api.GroupEnd());
   // 3. (pattern index, offset) order over all ranks -- the reference's per-pattern lists
-  if (int r = fetch_pair_prefix(c, goff, gidx, total, s)) return r;
   if (int r = order_pairs(c, goff, gidx, total, n_total, P, s)) return r;
   if (goff != d_off && cap) {
     RK_CUDA(cudaMemcpyAsync(d_off, goff, cap * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));

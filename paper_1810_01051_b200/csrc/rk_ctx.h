@@ -72,10 +72,8 @@ struct MultiPlan {
   std::vector<Group> groups;
   std::vector<Sweep> sweeps;
 };
-constexpr uint64_t kMultiPrefix = 4096;  // pairs fetched with the count in one round trip
 }  // namespace rkb
 using rkb::MultiPlan;
-using rkb::kMultiPrefix;
 
 struct rk_ctx {
   int device = 0;
@@ -128,7 +126,7 @@ struct rk_ctx {
   uint64_t mblob_cap = 0;
   uint8_t* h_mstage = nullptr;  // pinned staging of the blob
   uint64_t h_mstage_cap = 0;
-  unsigned long long* h_mresult = nullptr;  // pinned: count, kMultiPrefix offsets, indices
+  unsigned long long* h_mresult = nullptr;  // pinned (mapped): a multi scan's pair count
   MultiPlan mplan;              // the last pattern set's plan (cache key + layout)
   // The scratch above is ordered on the stream of the call that used it.  When a call
   // arrives on another stream, that stream first waits for everything queued so far on
@@ -201,8 +199,6 @@ int multi_enqueue(rk_ctx* c, const uint8_t* d_text, uint64_t n, uint64_t start_l
                   uint64_t cap, cudaStream_t s);
 int multi_order(rk_ctx* c, int64_t* d_off, uint32_t* d_idx, uint64_t cap, uint64_t n, uint32_t P,
                 const unsigned long long* d_count, uint64_t* total_out, cudaStream_t s);
-int fetch_pair_prefix(rk_ctx* c, const int64_t* d_off, const uint32_t* d_idx, uint64_t k,
-                      cudaStream_t s);
 int order_pairs(rk_ctx* c, int64_t* d_off, uint32_t* d_idx, uint64_t k, uint64_t n, uint32_t P,
                 cudaStream_t s);
 

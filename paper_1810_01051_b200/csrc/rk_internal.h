@@ -280,6 +280,10 @@ cudaError_t launch_multi(const MultiArgs& a, int grid, cudaStream_t s);
 
 // device ordering of (pattern index, offset) pairs (rk_pairs.cu)
 size_t sort_pairs_scratch(uint64_t k);
+constexpr uint64_t kSmallSort = 4096;  // pairs ordered by one block (rk_pairs.cu)
+cudaError_t small_sort_pairs(int64_t* d_off, uint32_t* d_idx, const unsigned long long* d_count,
+                             uint64_t k_host, uint64_t cap, uint64_t n,
+                             unsigned long long* count_out, cudaStream_t s);
 cudaError_t sort_pairs(int64_t* d_off, uint32_t* d_idx, uint64_t k, uint64_t n, uint32_t P,
                        void* scratch, size_t scratch_bytes, cudaStream_t s);
 

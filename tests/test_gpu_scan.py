@@ -404,8 +404,30 @@ def test_multi_mixed_lengths_longer_than_text(gpu):
             assert r == rk.search_naive(text, ps[i]), (n, i, len(ps[i]))
 
 
+def test_multi_pair_counts_at_the_small_sort_limit(gpu):
+    """Pair counts around the one-block sort's limit (4096 pairs: kSmallSort) and the
+    radix sort above it: planted copies of two patterns in random order, every list exact
+    and ascending, for 2, 4095, 4096, 4097 and 9000 pairs."""
+    rng = np.random.default_rng(84)
+    n = 1 << 20
+    for total in (2, 4095, 4096, 4097, 9000):
+        text = rng.integers(ord("a"), ord("z") + 1, n, dtype=np.uint8)
+        starts = np.sort(rng.choice(n // 16 - 1, total, replace=False)) * 16
+        for j, x in enumerate(starts):
+            text[x:x + 8] = np.frombuffer(b"QRSTUVWX" if j % 3 else b"QRSTUVWY", np.uint8)
+        pats = [b"QRSTUVWX", b"QRSTUVWY", b"ZZZZZZZZZ"]
+        out = rk.search_multi(text.tobytes(), pats)
+        ps, _, _ = oracle.pattern_set(pats)
+        got = 0
+        for i, r in out:
+            exp = rk.search_naive(text.tobytes(), ps[i])
+            assert r == exp, (total, i)
+            got += len(r.offsets)
+        assert got == total
+
+
 def test_multi_many_pairs_device_sorted(gpu):
-    """More pairs than the host round trip takes (4096): ordered on the device."""
+    """More pairs than one block sorts (4096): ordered by the device radix sort."""
     rng = np.random.default_rng(83)
     text = rng.integers(0, 2, 300000, dtype=np.uint8).tobytes()
     pats = [bytes(rng.integers(0, 2, m, dtype=np.uint8)) for m in (3, 5, 8, 8, 9, 12, 20)]
