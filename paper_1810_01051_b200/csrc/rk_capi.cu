@@ -808,6 +808,7 @@ int multi_enqueue(rk_ctx* c, const uint8_t* d_text, uint64_t n, uint64_t start_l
     p.out_idx = d_idx;
     p.cap = cap;
     p.counters = c->d_mcount;
+    multi_set_append(p);
     const uint64_t grid = std::max<uint64_t>(
         1, std::min<uint64_t>((uint64_t)c->num_sms * multi_blocks_per_sm(p),
                               (gg.num_tiles + kMultiWarps - 1) / kMultiWarps));

@@ -271,10 +271,18 @@ struct MultiArgs {
   const uint8_t* stab;
   TinyHash th;
   uint32_t sq;
+  // pairs each warp buffers in shared memory before one atomic reserves their slots (the
+  // shared memory the kernel leaves over; 0: one atomic per warp per round)
+  uint32_t append_cap;
   MultiGroup grp[kMultiMaxGroups];
 };
-size_t multi_smem_bytes();
-size_t multi_short_smem_bytes(uint32_t slots);
+constexpr size_t kMultiSmemMax = 227 * 1024;  // the sm_100 opt-in per block
+__host__ __device__ constexpr uint32_t multi_append_stride(uint32_t cap) {
+  return cap ? 16u + 12u * cap : 0u;  // per warp: count (16 B), offsets, indices
+}
+size_t multi_smem_bytes(uint32_t append_cap);
+size_t multi_short_smem_bytes(uint32_t slots, uint32_t append_cap);
+void multi_set_append(MultiArgs& a);  // a.append_cap from the kernel's other shared memory
 int multi_blocks_per_sm(const MultiArgs& a);
 cudaError_t launch_multi(const MultiArgs& a, int grid, cudaStream_t s);
 

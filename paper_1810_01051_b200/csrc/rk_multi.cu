@@ -1,5 +1,7 @@
 // rk_multi.cu -- dispatch of the multi-pattern scan kernels (the short-length variants
 // instantiated in rk_multi_g0.cu; kernels in rk_multi_impl.cuh).
+#include <algorithm>
+
 #include "rk_multi_impl.cuh"
 
 namespace rkb {
@@ -8,12 +10,14 @@ namespace rkb {
 __global__ void __launch_bounds__(kMultiBlock) rk_multi_qgram_kernel(const __grid_constant__ MultiArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   MultiRing* rings = reinterpret_cast<MultiRing*>(smem);
-  uint32_t* sfilter = reinterpret_cast<uint32_t*>(smem + sizeof(MultiRing) * kMultiWarps);
+  uint32_t* sfilter = reinterpret_cast<uint32_t*>(smem + sizeof(MultiRing) * kMultiWarps +
+                                                  kMultiWarps * multi_append_stride(a.append_cap));
   for (int i = threadIdx.x; i < kQFilterWords; i += blockDim.x) sfilter[i] = a.qfilter[i];
-  __syncthreads();
-
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  multi_append_init(a, lane);
+  __syncthreads();
+
   MultiRing* R = rings + warp;
   ring_init(R, lane);
   const uint64_t W = (uint64_t)gridDim.x * kMultiWarps;
@@ -35,6 +39,7 @@ __global__ void __launch_bounds__(kMultiBlock) rk_multi_qgram_kernel(const __gri
       default: qgram_tile<4, 1, true>(a, R, S, t, lane, sfilter); break;
     }
   }
+  multi_flush(a, lane);
 }
 
 template <int Q>
@@ -42,12 +47,31 @@ cudaError_t launch_multi_short(const MultiArgs& a, int grid, cudaStream_t s);
 template <int Q>
 int multi_short_occupancy(size_t smem);
 
-size_t multi_smem_bytes() {
-  return sizeof(MultiRing) * kMultiWarps + kQFilterWords * sizeof(uint32_t);
+// rings, the append buffers, the shared filter
+size_t multi_smem_bytes(uint32_t append_cap) {
+  return sizeof(MultiRing) * kMultiWarps + kMultiWarps * multi_append_stride(append_cap) +
+         kQFilterWords * sizeof(uint32_t);
 }
 
-size_t multi_short_smem_bytes(uint32_t slots) {  // rings + the sweep's cuckoo table + filter
-  return sizeof(MultiRing) * kMultiWarps + slots * 8u + kShortFilterWords * 4u;
+// rings, the append buffers, the sweep's cuckoo table + filter
+size_t multi_short_smem_bytes(uint32_t slots, uint32_t append_cap) {
+  return sizeof(MultiRing) * kMultiWarps + kMultiWarps * multi_append_stride(append_cap) +
+         slots * 8u + kShortFilterWords * 4u;
+}
+
+#ifndef RK_MULTI_APPEND_MAX
+#define RK_MULTI_APPEND_MAX 256  // pairs per warp buffer (0: no buffering)
+#endif
+void multi_set_append(MultiArgs& a) {
+  if (a.qmode) {  // the q-gram sweep appends directly (lengths >= 7 are rarely dense)
+    a.append_cap = 0;
+    return;
+  }
+  const size_t base = a.qmode ? multi_smem_bytes(0) : multi_short_smem_bytes(a.th.size, 0);
+  const size_t room = base < kMultiSmemMax ? (kMultiSmemMax - base) / kMultiWarps : 0;
+  uint32_t cap = room > 16 ? (uint32_t)((room - 16) / 12) & ~3u : 0u;
+  cap = std::min<uint32_t>(cap, RK_MULTI_APPEND_MAX);
+  a.append_cap = cap >= 32 ? cap : 0u;  // a buffer under one warp's worth is not worth it
 }
 
 int multi_blocks_per_sm(const MultiArgs& a) {
@@ -55,14 +79,16 @@ int multi_blocks_per_sm(const MultiArgs& a) {
     static int occ[kTinySlotsMax * 2] = {};  // per table size (a power of two)
     const uint32_t k = a.th.size;
     if (!occ[k]) {
-      const size_t smem = multi_short_smem_bytes(k);
+      MultiArgs t = a;
+      multi_set_append(t);
+      const size_t smem = multi_short_smem_bytes(k, t.append_cap);
       occ[k] = a.sq == 3 ? multi_short_occupancy<3>(smem)
                : a.sq == 4 ? multi_short_occupancy<4>(smem) : multi_short_occupancy<0>(smem);
     }
     return occ[k];
   }
   static int occ = 0;  // same on every B200
-  if (!occ) occ = multi_occupancy(rk_multi_qgram_kernel, multi_smem_bytes());
+  if (!occ) occ = multi_occupancy(rk_multi_qgram_kernel, multi_smem_bytes(a.append_cap));
   return occ;
 }
 
@@ -72,7 +98,7 @@ cudaError_t launch_multi(const MultiArgs& a, int grid, cudaStream_t s) {
            : a.sq == 4 ? launch_multi_short<4>(a, grid, s) : launch_multi_short<0>(a, grid, s);
   }
   return multi_launch_kernel<struct QgramAttr>(rk_multi_qgram_kernel, a, grid,
-                                               multi_smem_bytes(), s);
+                                               multi_smem_bytes(a.append_cap), s);
 }
 
 }  // namespace rkb

@@ -16,11 +16,12 @@ cudaError_t launch_multi_short(const MultiArgs& a, int grid, cudaStream_t s) {
   if (dev >= kMaxDevices || !attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(rk_multi_short_kernel<Q>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)multi_short_smem_bytes(kTinySlotsMax));
+                                         (int)kMultiSmemMax);
     if (e != cudaSuccess) return e;
     if (dev < kMaxDevices) attr[dev] = true;
   }
-  rk_multi_short_kernel<Q><<<grid, kMultiBlock, multi_short_smem_bytes(a.th.size), s>>>(a);
+  rk_multi_short_kernel<Q><<<grid, kMultiBlock, multi_short_smem_bytes(a.th.size, a.append_cap),
+                             s>>>(a);
   return cudaGetLastError();
 }
 
@@ -28,7 +29,7 @@ template <int Q>
 int multi_short_occupancy(size_t smem) {
   // (the opt-in stays at the largest table's size; only the query uses this one's)
   cudaFuncSetAttribute(rk_multi_short_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)multi_short_smem_bytes(kTinySlotsMax));
+                       (int)kMultiSmemMax);
   int b = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rk_multi_short_kernel<Q>, kMultiBlock, smem);
   return b > 0 ? b : 1;

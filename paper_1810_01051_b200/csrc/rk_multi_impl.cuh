@@ -145,18 +145,84 @@ __device__ __forceinline__ int group_resolve(const MultiGroup& G, const uint8_t*
 }
 
 // Appends (window start, pattern) for the lanes with idx >= 0: one atomic per warp.
+// This warp's append buffer (after the kernel's rings): a count, then append_cap offsets
+// and append_cap indices.
+__device__ __forceinline__ uint8_t* append_buf(const MultiArgs& a) {
+  extern __shared__ __align__(16) uint8_t smem_dyn[];
+  return smem_dyn + sizeof(MultiRing) * kMultiWarps +
+         (threadIdx.x >> 5) * multi_append_stride(a.append_cap);
+}
+
+__device__ __forceinline__ void multi_append_init(const MultiArgs& a, int lane) {
+  if (a.append_cap && lane == 0) *reinterpret_cast<uint32_t*>(append_buf(a)) = 0u;
+  __syncwarp();
+}
+
+// Writes the warp's buffered pairs out: one atomic reserves their slots, then coalesced
+// stores (warp-uniform call).
+__device__ __forceinline__ void multi_flush(const MultiArgs& a, int lane) {
+  if (!a.append_cap) return;
+  uint8_t* b = append_buf(a);
+  __syncwarp();
+  const uint32_t n = *reinterpret_cast<volatile uint32_t*>(b);
+  if (!n) return;
+  const int64_t* boff = reinterpret_cast<const int64_t*>(b + 16);
+  const uint32_t* bidx = reinterpret_cast<const uint32_t*>(b + 16 + 8u * a.append_cap);
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(&a.counters[0], (unsigned long long)n);
+  base = __shfl_sync(kFull, base, 0);
+  for (uint32_t i = lane; i < n; i += 32) {
+    const uint64_t pos = base + i;
+    if (pos < a.cap) {
+      a.out_off[pos] = boff[i] + a.out_bias;
+      a.out_idx[pos] = bidx[i];
+    }
+  }
+  __syncwarp();
+  if (lane == 0) *reinterpret_cast<uint32_t*>(b) = 0u;
+  __syncwarp();
+}
+
+// Appends the lanes' pairs (idx >= 0) -- warp-uniform call -- with one atomic per warp per
+// round, or (Buffered) into the warp's shared-memory buffer, flushed with one atomic per
+// append_cap pairs: dense output (all 'a' against {aaaa, aaaaa, aaaaaa}) made one atomic
+// per round serialise on one address.  The buffered path is out of line: inlined into the
+// fast pass it cost registers (spills) in the sparse common case.
+static __device__ __noinline__ void multi_append_buffered(const MultiArgs& a, int idx, int64_t y,
+                                                   int lane, unsigned hit) {
+  const uint32_t k = __popc(hit);
+  const uint32_t rank = __popc(hit & ((1u << lane) - 1u));
+  uint8_t* b = append_buf(a);
+  uint32_t n = *reinterpret_cast<volatile uint32_t*>(b);
+  if (n + k > a.append_cap) {
+    multi_flush(a, lane);
+    n = 0;
+  }
+  if (idx >= 0) {
+    reinterpret_cast<int64_t*>(b + 16)[n + rank] = y;
+    reinterpret_cast<uint32_t*>(b + 16 + 8u * a.append_cap)[n + rank] = (uint32_t)idx;
+  }
+  __syncwarp();
+  if (lane == 0) *reinterpret_cast<uint32_t*>(b) = n + k;
+  __syncwarp();
+}
+
+template <bool Buffered = false>
 __device__ __forceinline__ void multi_append(const MultiArgs& a, int idx, int64_t y, int lane) {
   const unsigned hit = __ballot_sync(kFull, idx >= 0);
-  if (hit) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(&a.counters[0], (unsigned long long)__popc(hit));
-    base = __shfl_sync(kFull, base, 0);
-    if (idx >= 0) {
-      const uint64_t pos = base + __popc(hit & ((1u << lane) - 1u));
-      if (pos < a.cap) {
-        a.out_off[pos] = y + a.out_bias;
-        a.out_idx[pos] = (uint32_t)idx;
-      }
+  if (!hit) return;
+  if (Buffered && a.append_cap) {
+    multi_append_buffered(a, idx, y, lane, hit);
+    return;
+  }
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(&a.counters[0], (unsigned long long)__popc(hit));
+  base = __shfl_sync(kFull, base, 0);
+  if (idx >= 0) {
+    const uint64_t pos = base + __popc(hit & ((1u << lane) - 1u));
+    if (pos < a.cap) {
+      a.out_off[pos] = y + a.out_bias;
+      a.out_idx[pos] = (uint32_t)idx;
     }
   }
 }
@@ -475,7 +541,7 @@ __device__ __forceinline__ void short_anchor_candidates(const MultiArgs& a, cons
             const uint32_t lo = j ? lo1 : lo0, hw = j ? hi1 : hi0;
             idx = short_probe(a, slots, lo & SL.klo[gi], hw & SL.khi[gi], SL.L[gi]);
           }
-          multi_append(a, idx, y0 - j - (int64_t)a.g.amis, lane);
+          multi_append<true>(a, idx, y0 - j - (int64_t)a.g.amis, lane);
         }
       }
     } else {
@@ -486,7 +552,7 @@ __device__ __forceinline__ void short_anchor_candidates(const MultiArgs& a, cons
           const int idx = t >= 0 ? short_lookup(a, slots, cur, c0, stage_bytes, ya,
                                                 a.grp[gi].m, a.grp[gi].ys_hi)
                                  : -1;
-          multi_append(a, idx, ya - (int64_t)a.g.amis, lane);
+          multi_append<true>(a, idx, ya - (int64_t)a.g.amis, lane);
         }
       }
     }
@@ -526,7 +592,7 @@ __device__ __forceinline__ void short_chunk_multi(const MultiArgs& a, const Shor
         const int64_t ya = J + k - (int64_t)L + 1;
         const int idx =
             k >= 0 ? short_lookup(a, slots, cur, c0, stage_bytes, ya, L, a.grp[gi].ys_hi) : -1;
-        multi_append(a, idx, ya - (int64_t)a.g.amis, lane);
+        multi_append<true>(a, idx, ya - (int64_t)a.g.amis, lane);
         act = __ballot_sync(kFull, pass != 0);
       }
     }
@@ -538,16 +604,17 @@ template <int Q>
 __global__ void __launch_bounds__(kMultiBlock) rk_multi_short_kernel(const __grid_constant__ MultiArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   MultiRing* rings = reinterpret_cast<MultiRing*>(smem);
-  uint8_t* tab = smem + sizeof(MultiRing) * kMultiWarps;
+  uint8_t* tab = smem + sizeof(MultiRing) * kMultiWarps + kMultiWarps * multi_append_stride(a.append_cap);
   const uint32_t n16 = (a.th.size * 8u + kShortFilterWords * 4u) / 16u;  // slots, then filter
   const uint4* src = reinterpret_cast<const uint4*>(a.stab);
   for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) reinterpret_cast<uint4*>(tab)[i] = src[i];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  multi_append_init(a, lane);
   __syncthreads();
   const uint32_t slots = smem_u32(tab);
   const uint32_t filt = slots + a.th.size * 8u;
 
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
   MultiRing* R = rings + warp;
   ring_init(R, lane);
   const uint64_t W = (uint64_t)gridDim.x * kMultiWarps;
@@ -568,6 +635,7 @@ __global__ void __launch_bounds__(kMultiBlock) rk_multi_short_kernel(const __gri
                             short_chunk_multi<Q>(a, SL, v, lb, J, S.cur, lane, slots, filt, sb);
                           });
   }
+  multi_flush(a, lane);
 }
 
 template <class K>
