@@ -1,3 +1,7 @@
+#ifdef RK_HOST_PROFILE
+#include <map>
+#include <string>
+#endif
 // rk_capi.cu -- the C ABI (include/rkb200.h): contexts, argument checking, launch
 // planning for the ordered single-pattern scan, the host-text staging pipeline, the
 // multi-pattern table build, and error reporting.
@@ -34,6 +38,27 @@ int rkb::fail(int code, const char* fmt, ...) {
   return code;
 }
 
+#ifdef RK_HOST_PROFILE
+static std::map<std::string, std::pair<double, long>>& hprof_map() {
+  static std::map<std::string, std::pair<double, long>> m;
+  static bool reg = false;
+  if (!reg) {
+    reg = true;
+    atexit([] {
+      for (auto& kv : hprof_map())
+        fprintf(stderr, "hprof %-24s %8.2f us avg over %ld\n", kv.first.c_str(),
+                kv.second.first / kv.second.second, kv.second.second);
+    });
+  }
+  return m;
+}
+HostProf::~HostProf() {
+  const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  auto& e = hprof_map()[name];
+  e.first += us;
+  e.second += 1;
+}
+#endif
 namespace rkb {
 
 // Persistent host threads for the pageable -> pinned staging copy (CPU-bound: one
@@ -235,7 +260,10 @@ int emit(rk_ctx* c, uint64_t tiles, uint64_t tile0, int64_t start_bias, int64_t*
     e.bitmap = d_bitmap;
     e.bit_bias = bit_bias;
   }
-  RK_CUDA(launch_emit(e, c->num_sms, s));
+  {
+    RK_HPROF("launch_emit");
+    RK_CUDA(launch_emit(e, c->num_sms, s));
+  }
   ++c->launches;
   return RK_OK;
 }
@@ -300,6 +328,7 @@ int launch_one(rk_ctx* c, const uint8_t* d_text, uint64_t n, uint32_t m, uint64_
   uint64_t warps = (uint64_t)scan_warps(m);
   if (g.num_tiles < slots * warps) warps = std::max<uint64_t>(1, (g.num_tiles + slots - 1) / slots);
   a.warps = (uint32_t)warps;
+  RK_HPROF("launch_scan");
   RK_CUDA(launch_scan(a, grid_for(g.num_tiles, c->num_sms, scan_blocks_per_sm(m), (int)warps),
                       s));
   ++c->launches;
@@ -362,11 +391,21 @@ int enqueue_scan(rk_ctx* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_
                  uint64_t cap, int64_t bias, cudaStream_t s, uint64_t* d_counts) {
   c->last_scan.valid = false;
   if (stop <= start || hash_unreachable(m, hx)) return zero_result(c, d_counts, s);
-  if (int r = upload_pattern(c, h_pattern, m, s)) return r;
+  {
+    RK_HPROF("upload_pattern");
+    if (int r = upload_pattern(c, h_pattern, m, s)) return r;
+  }
   const Geometry g = geometry(d_text, m, start, stop);
-  if (int r = begin_scan(c, g.num_tiles, s)) return r;
-  if (int r = launch_one(c, d_text, n, m, hx, start, stop, 0, pack_pattern(h_pattern, m), s))
-    return r;
+  {
+    RK_HPROF("begin_scan");
+    if (int r = begin_scan(c, g.num_tiles, s)) return r;
+  }
+  {
+    RK_HPROF("launch_one");
+    if (int r = launch_one(c, d_text, n, m, hx, start, stop, 0, pack_pattern(h_pattern, m), s))
+      return r;
+  }
+  RK_HPROF("emit");
   c->last_scan.valid = true;
   c->last_scan.host = false;
   c->last_scan.tiles = g.num_tiles;
@@ -936,6 +975,7 @@ uint64_t rk_launch_count(rk_ctx_t* c) { return c ? c->launches : 0; }
 int rk_scan_async(rk_ctx_t* c, const uint8_t* d_text, uint64_t n, const uint8_t* h_pattern,
                   uint32_t m, uint64_t hx, uint64_t start, uint64_t stop, int64_t* d_out,
                   uint64_t cap, int64_t out_bias, uint64_t* d_counts, void* stream) {
+  RK_HPROF("rk_scan_async total");
   if (!c) return fail(RK_EINVAL, "context is NULL");
   if (int r = check_scan_args(d_text, n, h_pattern, m, start, stop, d_out, cap)) return r;
   std::lock_guard<std::mutex> lk(c->mu);

@@ -2,6 +2,10 @@
 // helpers shared by the C-ABI translation units (rk_capi.cu: scans, staging, multi-pattern;
 // rk_comm.cu: NCCL communicators and the sharded scan).
 #pragma once
+#ifdef RK_HOST_PROFILE
+#include <chrono>
+#include <cstdio>
+#endif
 #include <cstdint>
 #include <map>
 #include <mutex>
@@ -23,12 +27,24 @@ int fail(int code, const char* fmt, ...);
                          __FILE__, __LINE__);                                           \
   } while (0)
 
-struct DeviceGuard {
+#ifdef RK_HOST_PROFILE
+struct HostProf {
+  const char* name;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit HostProf(const char* n) : name(n) {}
+  ~HostProf();
+};
+#define RK_HPROF(n) HostProf _hp_##__LINE__(n)
+#else
+#define RK_HPROF(n)
+#endif
+struct DeviceGuard {  // (no cudaSetDevice when the caller is already on the device)
   int prev = -1;
   bool ok = false;
   explicit DeviceGuard(int dev) {
     if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    ok = cudaSetDevice(dev) == cudaSuccess;
+    ok = prev == dev || cudaSetDevice(dev) == cudaSuccess;
+    if (prev == dev) prev = -1;
   }
   ~DeviceGuard() {
     if (prev >= 0) cudaSetDevice(prev);

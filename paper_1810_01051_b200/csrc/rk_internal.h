@@ -13,6 +13,9 @@
 //   RK_EMIT_MAX_GROUPS   groups of 256 tiles one emit block expands, static schedule (4)
 //   RK_EMIT_DEFER_MIN    matches from which a tile goes to the balanced phase (1024; 0 off)
 //   RK_MULTI_WARPS/STAGE, RK_MULTI_UNROLL   q-gram / tiny multi-pattern kernel shape
+//   RK_MULTI_APPEND_MAX  pairs a short-sweep warp buffers before one atomic (256; 0 off)
+//   RK_SHORT_KEY_REFINE  3-gram anchors refined on 4-byte prefixes (1)
+//   RK_HOST_PROFILE      per-call host time of the enqueue steps, printed at exit (off)
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
