@@ -198,3 +198,46 @@ def test_dense_tiles_queued_with_caps(gpu):
             full = torch.empty(len(exp), dtype=torch.int64, device="cuda")
             _lib.check(L.rk_scan_fetch(ctx.handle, full.data_ptr(), len(exp), s))
         assert np.array_equal(full.cpu().numpy(), exp)
+
+
+def test_emit_queue_fuzz(gpu):
+    """Randomised texts of dense stretches (one letter, or two letters alternating) inside
+    sparse random text, m = 1..12, scanned through the C ABI with random caps and then
+    re-emitted in full (rk_scan_fetch): the dense tiles go through the emit's queue, the
+    rest is expanded in place, and every list, cut and count equals the oracle's."""
+    torch = _torch()
+    rng = np.random.default_rng(4242)
+    L = _lib.lib()
+    ctx = _lib.context(0)
+    s = _scan._stream(0)
+    for case in range(40):
+        n = int(rng.integers(1 << 16, 6 << 20))
+        host = rng.integers(ord("a"), ord("e"), n, dtype=np.uint8)
+        for _ in range(int(rng.integers(1, 6))):
+            ln = int(rng.integers(1, 1 << 20))
+            x = int(rng.integers(0, n))
+            seg = host[x:x + ln]
+            if rng.random() < 0.5:
+                seg[:] = ord("a")
+            else:
+                seg[0::2] = ord("a")
+                seg[1::2] = ord("b")
+        m = int(rng.integers(1, 13))
+        pat = (b"a" * m) if rng.random() < 0.5 else bytes((b"ab" * 8)[:m])
+        p = np.frombuffer(pat, dtype=np.uint8)
+        exp, ecoll = oracle.c_scan(host, p, workers=8)
+        text = torch.from_numpy(host).cuda()
+        cap = int(rng.integers(0, len(exp) + 2)) if len(exp) else 0
+        out = torch.full((max(cap, 1),), -1, dtype=torch.int64, device="cuda")
+        mt, co, hh = _lib.u64ref(), _lib.u64ref(), _lib.u64ref()
+        with ctx.lock:
+            _lib.check(L.rk_scan(ctx.handle, text.data_ptr(), n, p.ctypes.data, m,
+                                 rk.hash_full(pat), 0, n - m + 1, out.data_ptr(), cap,
+                                 ctypes.byref(mt), ctypes.byref(co), ctypes.byref(hh), s))
+            k = int(mt.value)
+            assert k == len(exp) and int(co.value) == ecoll and int(hh.value) == k + ecoll, case
+            full = torch.empty(max(k, 1), dtype=torch.int64, device="cuda")
+            if k:
+                _lib.check(L.rk_scan_fetch(ctx.handle, full.data_ptr(), k, s))
+        assert np.array_equal(out[:min(cap, k)].cpu().numpy(), exp[:cap]), (case, n, m, cap)
+        assert np.array_equal(full[:k].cpu().numpy(), exp), (case, n, m)
