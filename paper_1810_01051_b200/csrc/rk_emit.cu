@@ -127,6 +127,16 @@ __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long 
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 constexpr int kQueueTileBits = 22;
+#ifdef RK_DEBUG_CHECKS
+#define RK_DCHECK(c) \
+  do {               \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define RK_DCHECK(c) \
+  do {               \
+  } while (0)
+#endif
 
 // Expands the hit masks of the tiles with matches among the 256 tiles from sequence number
 // t0 (info = this thread's tile_info, excl = its exclusive match prefix) into ordered offsets.
@@ -172,6 +182,7 @@ __device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t t0, uint3
       at = __shfl_sync(kFull, at, 0);
       if ((dense >> lane) & 1u) {
         const uint64_t i = at + __popc(dense & ((1u << lane) - 1u));
+        RK_DCHECK(i < e.num_tiles && t0 + warp * 32 + lane < e.num_tiles);
         st_relaxed(&e.queue[i], ((excl + 1) << kQueueTileBits) | (t0 + warp * 32 + lane));
       }
       todo &= ~dense;
@@ -245,6 +256,7 @@ struct QueuedTile {
 __device__ __forceinline__ void load_entry(const EmitArgs& e, unsigned long long ex, int lane,
                                            QueuedTile& q) {
   q.tseq = ex & ((1ull << kQueueTileBits) - 1);
+  RK_DCHECK(q.tseq < e.num_tiles);
   q.flags = e.tile_info[q.tseq] >> 16;
   fetch_masks(e, q.tseq, q.flags, lane, q.hms);
 }

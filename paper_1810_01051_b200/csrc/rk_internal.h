@@ -16,6 +16,7 @@
 //   RK_MULTI_APPEND_MAX  pairs a short-sweep warp buffers before one atomic (256; 0 off)
 //   RK_SHORT_KEY_REFINE  3-gram anchors refined on 4-byte prefixes (1)
 //   RK_HOST_PROFILE      per-call host time of the enqueue steps, printed at exit (off)
+//   RK_DEBUG_CHECKS      device-side bounds checks (trap) in the emit queue (off)
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
