@@ -6,8 +6,8 @@
 // (masks), and per-256-tile sums (block_sums).  This kernel turns that into the ordered
 // int64 offsets: each block adds up the counts before its span of tiles, scans its tile
 // counts, and each warp expands the masks of its tiles with matches into window starts
-// written at their final positions -- ascending, deterministic, no sort, no text re-read.  For sparse
-// matches this is a few microseconds per GiB.
+// written at their final positions -- ascending, deterministic, no sort, no text
+// re-read.  For sparse matches this is a few microseconds per GiB.
 //
 // Dense outputs (every window matching, BASELINE config C5) are write-bound: a chunk's
 // offsets are staged in shared memory (padded so the lane-strided fill is nearly
@@ -24,6 +24,10 @@
 namespace rkb {
 
 constexpr int kEmitWarps = kEmitTiles / 32;
+#ifndef RK_EMIT_MAX_GROUPS
+#define RK_EMIT_MAX_GROUPS 4
+#endif
+constexpr uint64_t kEmitMaxGroups = RK_EMIT_MAX_GROUPS;  // x kEmitTiles: a block's largest span
 #ifndef RK_EMIT_LD
 #define RK_EMIT_LD(p) (*(p))
 #endif
@@ -138,13 +142,13 @@ constexpr int kQueueTileBits = 22;
   } while (0)
 #endif
 
-// Expands the hit masks of the tiles with matches among the 256 tiles from sequence number
-// t0 (info = this thread's tile_info, excl = its exclusive match prefix) into ordered offsets.
+// Expands the hit masks of the warp's tiles with matches -- lane j's tile is tw + j ts,
+// info its tile_info, excl its exclusive match prefix -- into ordered offsets.
 // With defer, tiles with at least kDeferMin matches are not expanded here but queued
 // (tile, excl) for the dynamically balanced second phase.
-__device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t t0, uint32_t info,
-                                           uint64_t excl, int64_t* stage, int lane, int warp,
-                                           bool defer) {
+__device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t tw, uint32_t ts,
+                                           uint32_t info, uint64_t excl, int64_t* stage,
+                                           int lane, bool defer) {
   const uint32_t cnt = info & 0xffffu;
   unsigned todo = __ballot_sync(kFull, cnt != 0);
   if (!todo) return;
@@ -153,7 +157,7 @@ __device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t t0, uint3
     while (todo) {
       const int j = __ffs(todo) - 1;
       todo &= todo - 1;
-      const uint64_t tseq = t0 + warp * 32 + j;
+      const uint64_t tseq = tw + (uint64_t)j * ts;
       uint32_t flags = __shfl_sync(kFull, info, j) >> 16;
       const int64_t tile_a = (int64_t)((e.tile0 + tseq) * (uint64_t)kTile);
       const uint32_t* tm = e.masks + tseq * (kTileChunks * 32);
@@ -182,8 +186,8 @@ __device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t t0, uint3
       at = __shfl_sync(kFull, at, 0);
       if ((dense >> lane) & 1u) {
         const uint64_t i = at + __popc(dense & ((1u << lane) - 1u));
-        RK_DCHECK(i < e.num_tiles && t0 + warp * 32 + lane < e.num_tiles);
-        st_relaxed(&e.queue[i], ((excl + 1) << kQueueTileBits) | (t0 + warp * 32 + lane));
+        RK_DCHECK(i < e.num_tiles && tw + (uint64_t)lane * ts < e.num_tiles);
+        st_relaxed(&e.queue[i], ((excl + 1) << kQueueTileBits) | (tw + (uint64_t)lane * ts));
       }
       todo &= ~dense;
       if (!todo) return;
@@ -193,7 +197,7 @@ __device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t t0, uint3
   // previous tile is being expanded (not one load latency per chunk)
   uint32_t hms[kTileChunks], nxt[kTileChunks];
   int jn = __ffs(todo) - 1;
-  fetch_masks(e, t0 + warp * 32 + jn, __shfl_sync(kFull, info, jn) >> 16, lane, nxt);
+  fetch_masks(e, tw + (uint64_t)jn * ts, __shfl_sync(kFull, info, jn) >> 16, lane, nxt);
   while (todo) {
     const int j = jn;
     todo &= todo - 1;
@@ -201,9 +205,9 @@ __device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t t0, uint3
     for (int c = 0; c < kTileChunks; ++c) hms[c] = nxt[c];
     jn = todo ? __ffs(todo) - 1 : -1;
     const uint32_t fl_next = __shfl_sync(kFull, info, jn < 0 ? 0 : jn) >> 16;
-    if (jn >= 0) fetch_masks(e, t0 + warp * 32 + jn, fl_next, lane, nxt);
+    if (jn >= 0) fetch_masks(e, tw + (uint64_t)jn * ts, fl_next, lane, nxt);
     const uint32_t flags = __shfl_sync(kFull, info, j) >> 16;
-    expand_tile(e, t0 + warp * 32 + j, flags, __shfl_sync(kFull, excl, j), hms, stage, lane);
+    expand_tile(e, tw + (uint64_t)j * ts, flags, __shfl_sync(kFull, excl, j), hms, stage, lane);
   }
 }
 
@@ -286,11 +290,11 @@ __device__ __forceinline__ void drain_queue(const EmitArgs& e, int64_t* stage, i
   }
 }
 
-// Block b handles the tiles [b S, (b + 1) S), S = e.tiles_per_block, 256 at a time (the
-// block's starting offset is block_sums over the groups before its
-// span plus the counts of the tiles of its first group that precede it).  The next 256
-// tile_info words are loaded while the current ones are scanned and expanded.  Sparse
-// tiles are expanded in place; dense ones are queued for the balanced second phase.
+// Block b handles the tiles [b S, (b + 1) S), S = e.tiles_per_block <= 1024, each thread
+// 4 consecutive ones (the block's starting offset is block_sums over the groups before
+// its span plus the counts of the tiles of its first group that precede it; one block-wide
+// scan orders the rest).  Sparse tiles are expanded in place; dense ones are queued for
+// the balanced second phase.
 __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the scan's writes are visible
   asm volatile("griddepcontrol.launch_dependents;");  // the next scan may be scheduled
@@ -303,11 +307,20 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
   const uint64_t t_begin = (uint64_t)blockIdx.x * S;
   const uint64_t t_end = t_begin + S < e.num_tiles ? t_begin + S : e.num_tiles;
 
-  auto load_info = [&](uint64_t t) -> uint32_t {
-    const uint64_t seq = t + tid;
-    return seq < t_end ? RK_EMIT_LD(&e.tile_info[seq]) : 0u;
-  };
-  uint32_t info = load_info(t_begin);  // issued with the prefix loads below
+  // Thread tid owns the Q consecutive tiles from tq (a span is at most Q x 256 tiles):
+  // all tile_info loads are issued at once and one block-wide scan orders them -- one
+  // barrier per emit instead of two per 256 tiles (the emit sits on the critical path
+  // between two scans of a sweep: C2 1.487 -> 1.480 ms per step)
+  constexpr int Q = (int)kEmitMaxGroups;
+  const uint64_t tq = t_begin + (uint64_t)tid * Q;
+  uint32_t inf[Q];
+  uint32_t tsum = 0;
+#pragma unroll
+  for (int k = 0; k < Q; ++k) {
+    const uint64_t seq = tq + k;
+    inf[k] = seq < t_end ? RK_EMIT_LD(&e.tile_info[seq]) : 0u;
+    tsum += inf[k] & 0xffffu;
+  }
   const uint64_t gb = t_begin / kEmitTiles;
   unsigned long long pre = 0;
   for (uint64_t i = tid; i < gb; i += kEmitTiles) pre += RK_EMIT_LD(&e.block_sums[i]);
@@ -317,44 +330,71 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
   if (gb * kEmitTiles + tid < t_begin) pre += RK_EMIT_LD(&e.tile_info[gb * kEmitTiles + tid]) & 0xffffu;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(kFull, pre, o);
+  const uint32_t inc = warp_incl_scan(tsum, lane);
   if (lane == 0) red[warp] = pre;
+  if (lane == 31) wsum[warp] = inc;
   for (uint64_t i = (uint64_t)blockIdx.x * kEmitTiles + tid; i < e.clear_words;
        i += (uint64_t)gridDim.x * kEmitTiles)
     e.clear[i] = 0ull;
   __syncthreads();
   unsigned long long base = 0;
+  uint32_t wpre = 0;
 #pragma unroll
-  for (int w = 0; w < kEmitWarps; ++w) base += red[w];
+  for (int w = 0; w < kEmitWarps; ++w) {
+    base += red[w];
+    if (w < warp) wpre += wsum[w];
+  }
 #ifdef RK_EMIT_DEBUG
   if (tid == 0) RK_EMIT_DEBUG[blockIdx.x] = base;
 #endif
-
-  for (uint64_t t = t_begin; t < t_end; t += kEmitTiles) {
-    const uint32_t next = load_info(t + kEmitTiles);
-    const uint32_t cnt = info & 0xffffu;
-    const uint32_t inc = warp_incl_scan(cnt, lane);
-    __syncthreads();  // wsum of the previous round has been read
-    if (lane == 31) wsum[warp] = inc;
-    __syncthreads();
-    uint32_t wpre = 0, gtot = 0;
+  uint64_t ex[Q];
+  ex[0] = base + wpre + inc - tsum;
 #pragma unroll
-    for (int w = 0; w < kEmitWarps; ++w) {
-      if (w < warp) wpre += wsum[w];
-      gtot += wsum[w];
-    }
-    const uint64_t excl = base + wpre + inc - cnt;
-    const uint64_t seq = t + tid;
-    if (seq == e.num_tiles - 1 && t_end == e.num_tiles) {  // (seq may run past a span)
-      e.counters[0] = excl + cnt;
-      if (e.counts_out) {
-        e.counts_out[0] = excl + cnt;
-        e.counts_out[1] = e.counters[1];
-        e.counts_out[2] = e.counters[2];
+  for (int k = 1; k < Q; ++k) ex[k] = ex[k - 1] + (inf[k - 1] & 0xffffu);
+  if (defer) {
+    // dense tiles to the queue, in tile order (lane-major, then k: ascending tiles), so
+    // consecutive tickets write neighbouring output
+    uint32_t dm = 0;
+#pragma unroll
+    for (int k = 0; k < Q; ++k) dm |= ((inf[k] & 0xffffu) >= kDeferMin ? 1u : 0u) << k;
+    const uint32_t d = __popc(dm);
+    const uint32_t dinc = warp_incl_scan(d, lane);
+    const uint32_t dtot = __shfl_sync(kFull, dinc, 31);
+    if (dtot) {
+      unsigned long long at = 0;
+      if (lane == 0) at = atomicAdd(&e.work[1], (unsigned long long)dtot);
+      at = __shfl_sync(kFull, at, 0) + dinc - d;
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        if ((dm >> k) & 1u) {
+          RK_DCHECK(at < e.num_tiles && tq + k < e.num_tiles);
+          st_relaxed(&e.queue[at], ((ex[k] + 1) << kQueueTileBits) | (tq + k));
+          ++at;
+          inf[k] = 0u;  // not expanded here
+        }
       }
     }
-    emit_group(e, t, info, excl, stage, lane, warp, defer);
-    base += gtot;
-    info = next;
+  }
+  if (t_end == e.num_tiles && tq <= e.num_tiles - 1 && e.num_tiles - 1 < tq + Q) {
+    // the last tile's thread: the totals
+    const uint64_t total = ex[0] + tsum;
+    e.counters[0] = total;
+    if (e.counts_out) {
+      e.counts_out[0] = total;
+      e.counts_out[1] = e.counters[1];
+      e.counts_out[2] = e.counters[2];
+    }
+  }
+  // (a rolled loop -- the tiles' words rotate through inf[0] / ex[0] -- keeps the emit's
+  // code small: it runs beside the next scan's CTAs)
+#pragma unroll 1
+  for (int k = 0; k < Q; ++k) {
+    emit_group(e, t_begin + (uint64_t)warp * 32 * Q + k, Q, inf[0], ex[0], stage, lane, false);
+#pragma unroll
+    for (int j = 0; j + 1 < Q; ++j) {
+      inf[j] = inf[j + 1];
+      ex[j] = ex[j + 1];
+    }
   }
   if (defer) {
     __syncthreads();  // this block's queue entries are all published
@@ -384,10 +424,6 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
 #define RK_EMIT_MIN_SMEM_KB (228 / (RK_EMIT_CTAS + 1) + 1)
 #endif
 constexpr size_t kEmitMinSmem = RK_EMIT_MIN_SMEM_KB * 1024;
-#ifndef RK_EMIT_MAX_GROUPS
-#define RK_EMIT_MAX_GROUPS 4
-#endif
-constexpr uint64_t kEmitMaxGroups = RK_EMIT_MAX_GROUPS;  // x kEmitTiles: a block's largest span
 size_t emit_smem_bytes() {
   const size_t b = (size_t)kEmitWarps * kPadded * sizeof(int64_t);
   return b < kEmitMinSmem ? kEmitMinSmem : b;
