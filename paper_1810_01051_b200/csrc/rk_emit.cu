@@ -144,11 +144,9 @@ constexpr int kQueueTileBits = 22;
 
 // Expands the hit masks of the warp's tiles with matches -- lane j's tile is tw + j ts,
 // info its tile_info, excl its exclusive match prefix -- into ordered offsets.
-// With defer, tiles with at least kDeferMin matches are not expanded here but queued
-// (tile, excl) for the dynamically balanced second phase.
 __device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t tw, uint32_t ts,
                                            uint32_t info, uint64_t excl, int64_t* stage,
-                                           int lane, bool defer) {
+                                           int lane) {
   const uint32_t cnt = info & 0xffffu;
   unsigned todo = __ballot_sync(kFull, cnt != 0);
   if (!todo) return;
@@ -177,21 +175,6 @@ __device__ __forceinline__ void emit_group(const EmitArgs& e, uint64_t tw, uint3
       }
     }
     return;
-  }
-  if (defer) {
-    const unsigned dense = __ballot_sync(kFull, cnt >= kDeferMin);
-    if (dense) {
-      unsigned long long at = 0;
-      if (lane == 0) at = atomicAdd(&e.work[1], (unsigned long long)__popc(dense));
-      at = __shfl_sync(kFull, at, 0);
-      if ((dense >> lane) & 1u) {
-        const uint64_t i = at + __popc(dense & ((1u << lane) - 1u));
-        RK_DCHECK(i < e.num_tiles && tw + (uint64_t)lane * ts < e.num_tiles);
-        st_relaxed(&e.queue[i], ((excl + 1) << kQueueTileBits) | (tw + (uint64_t)lane * ts));
-      }
-      todo &= ~dense;
-      if (!todo) return;
-    }
   }
   // the hit masks of a tile come in one round of independent loads, issued while the
   // previous tile is being expanded (not one load latency per chunk)
@@ -389,7 +372,7 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
   // code small: it runs beside the next scan's CTAs)
 #pragma unroll 1
   for (int k = 0; k < Q; ++k) {
-    emit_group(e, t_begin + (uint64_t)warp * 32 * Q + k, Q, inf[0], ex[0], stage, lane, false);
+    emit_group(e, t_begin + (uint64_t)warp * 32 * Q + k, Q, inf[0], ex[0], stage, lane);
 #pragma unroll
     for (int j = 0; j + 1 < Q; ++j) {
       inf[j] = inf[j + 1];
