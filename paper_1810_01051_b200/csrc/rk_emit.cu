@@ -240,10 +240,18 @@ struct QueuedTile {
   uint32_t hms[kTileChunks];
 };
 
+constexpr unsigned long long kQueueFull = 1ull << 63;  // every window of the tile matches
+
 __device__ __forceinline__ void load_entry(const EmitArgs& e, unsigned long long ex, int lane,
                                            QueuedTile& q) {
   q.tseq = ex & ((1ull << kQueueTileBits) - 1);
   RK_DCHECK(q.tseq < e.num_tiles);
+  if (ex & kQueueFull) {  // known from the entry: no tile_info or mask loads
+    q.flags = (1u << kTileChunks) - 1u;
+#pragma unroll
+    for (int c = 0; c < kTileChunks; ++c) q.hms[c] = ~0u;
+    return;
+  }
   q.flags = e.tile_info[q.tseq] >> 16;
   fetch_masks(e, q.tseq, q.flags, lane, q.hms);
 }
@@ -262,7 +270,8 @@ __device__ __forceinline__ void drain_queue(const EmitArgs& e, int64_t* stage, i
     if (ex2) load_entry(e, ex2, lane, nxt);
     __syncwarp();
     if (lane == 0) e.queue[t] = 0ull;  // consumed: the queue is left zeroed
-    expand_tile(e, cur.tseq, cur.flags, (ex >> kQueueTileBits) - 1, cur.hms, stage, lane);
+    expand_tile(e, cur.tseq, cur.flags, ((ex & ~kQueueFull) >> kQueueTileBits) - 1, cur.hms, stage,
+                lane);
     if (!ex2) {
       ex2 = wait_entry(e, t2, lane);
       if (ex2) load_entry(e, ex2, lane, nxt);
@@ -351,7 +360,9 @@ __global__ void __launch_bounds__(kEmitTiles) rk_emit_kernel(const EmitArgs e) {
       for (int k = 0; k < Q; ++k) {
         if ((dm >> k) & 1u) {
           RK_DCHECK(at < e.num_tiles && tq + k < e.num_tiles);
-          st_relaxed(&e.queue[at], ((ex[k] + 1) << kQueueTileBits) | (tq + k));
+          const bool full = inf[k] == ((uint32_t)kTile | (((1u << kTileChunks) - 1u) << 16));
+          st_relaxed(&e.queue[at], ((ex[k] + 1) << kQueueTileBits) | (tq + k) |
+                                       (full ? kQueueFull : 0ull));
           ++at;
           inf[k] = 0u;  // not expanded here
         }
