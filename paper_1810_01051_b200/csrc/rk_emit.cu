@@ -215,11 +215,19 @@ __device__ __forceinline__ unsigned long long wait_entry(const EmitArgs& e, unsi
                                                          int lane) {
   unsigned long long ex = 0;
   if (lane == 0) {
+    unsigned long long t0 = 0;
     for (uint32_t spins = 0;; ++spins) {
       if (t < e.num_tiles) ex = ld_relaxed(&e.queue[t]);
       if (ex) break;
       if (ld_acquire(&e.work[2]) == gridDim.x && t >= ld_acquire(&e.work[1])) break;
-      if (spins > (1u << 25)) __trap();  // a lost producer: fail loudly, never hang
+      if ((spins & 1023u) == 0) {
+        // a producer missing for 60 s (other work can hold SMs for a while, never that
+        // long): fail loudly instead of hanging
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (!t0) t0 = now;
+        if (now - t0 > 60ull * 1000000000ull) __trap();
+      }
       __nanosleep(100);
     }
   }
