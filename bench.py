@@ -55,6 +55,10 @@ def parse():
                          "16 GiB DNA, strong scaling)")
     ap.add_argument("--c4-bytes", type=int, default=16 * GiB)
     ap.add_argument("--sustained-steps", type=int, default=200)
+    ap.add_argument("--force-comm", action="store_true",
+                    help="run the N > 1 exchange path (C-ABI communicator) even at one rank (tests)")
+    ap.add_argument("--slab", type=int, default=4096,
+                    help="N > 1: offsets per pattern and rank exchanged without a host round trip")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-seconds", type=float, default=150.0,
@@ -327,7 +331,8 @@ def run_ours(args):
     # N > 1: the exchange through the C ABI (NCCL); --dist-backend gloo (the plumbing test of
     # this multi-rank path on one GPU: ranks never wait on each other's kernels) exchanges
     # through torch.distributed on the host instead
-    comm = sharded.Communicator(device=dev) if world > 1 and args.dist_backend == "nccl" else None
+    comm = (sharded.Communicator(device=dev)
+            if (world > 1 and args.dist_backend == "nccl") or args.force_comm else None)
     gloo = world > 1 and comm is None
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
@@ -338,6 +343,8 @@ def run_ours(args):
     glob = {}
     pat_bufs = {m: np.frombuffer(pats[m], dtype=np.uint8) for m in sweep}
     n_local = int(text.numel())
+    acounts = torch.zeros((len(sweep), 4), dtype=torch.int64, device=f"cuda:{dev}")
+    batch_async = [comm is not None]  # N > 1 over NCCL: the asynchronous batch
 
     def step(ev_pairs=None):
         for i, m in enumerate(sweep):
@@ -365,22 +372,43 @@ def run_ours(args):
             if ev_pairs is not None:
                 ev_pairs[i][1].record(stream)
         if comm is not None and ev_pairs is None:
-            # the C ABI's batched sharded scan: the nine local scans back to back, then one
-            # all-gather of every rank's counters, one host read and one NCCL group of
-            # broadcasts putting every rank's ordered positions into every rank's outputs
-            res = comm.scan_batch(text, [pats[m] for m in sweep],
-                                  [(plans[m][0] + byte_lo, plans[m][1] + byte_lo) for m in sweep],
-                                  byte_lo, [outs[m] for m in sweep], stream=sptr)
-            for m, r in zip(sweep, res):
-                glob[m] = r
+            if batch_async[0]:
+                # the C ABI's asynchronous batched sharded scan: the nine local scans back to
+                # back, each into a fixed slab, then ONE NCCL group all-gathering every rank's
+                # counters and slabs, and a device kernel ordering every rank's positions
+                # into every rank's outputs -- no host round trip inside the step
+                comm.scan_batch_async(text, [pats[m] for m in sweep],
+                                      [(plans[m][0] + byte_lo, plans[m][1] + byte_lo)
+                                       for m in sweep],
+                                      byte_lo, [outs[m] for m in sweep], acounts,
+                                      slab=args.slab, stream=sptr)
+            else:
+                # (a rank found more than a slab: the synchronous batch, which sizes the
+                # exchange from the gathered counts)
+                res = comm.scan_batch(text, [pats[m] for m in sweep],
+                                      [(plans[m][0] + byte_lo, plans[m][1] + byte_lo)
+                                       for m in sweep],
+                                      byte_lo, [outs[m] for m in sweep], stream=sptr)
+                for m, r in zip(sweep, res):
+                    glob[m] = r
         return counts
 
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
+    if comm is not None and batch_async[0]:
+        ac = acounts.cpu().numpy()
+        if ac[:, 3].any():
+            batch_async[0] = False  # some list is over a slab: the synchronous batch
+            for _ in range(max(args.warmup, 3)):
+                step()
+            torch.cuda.synchronize()
+        else:
+            for i, m in enumerate(sweep):
+                glob[m] = (outs[m][: int(ac[i, 0])], int(ac[i, 0]), int(ac[i, 2]), int(ac[i, 1]))
     # correctness gate: counts add up; at N > 1 every rank holds the same global ascending
     # list, and its total is the sum over ranks
-    if world == 1:
+    if comm is None and not gloo:
         host_counts = counts.cpu().numpy()
     else:
         host_counts = np.array([[glob[m][1], glob[m][3], glob[m][2]] for m in sweep], dtype=np.int64)
@@ -426,7 +454,7 @@ def run_ours(args):
 
     # roofline of the scan kernel: algorithmic bytes = n + 8*matches per launch (local)
     peak, peak_kind = load_peaks()
-    local_counts = counts.cpu().numpy() if world == 1 else None
+    local_counts = counts.cpu().numpy() if comm is None and not gloo else None
     alg = [(plans[m][1] - plans[m][0] + m - 1) +
            8 * int((local_counts if local_counts is not None else host_counts)[i, 0])
            for i, m in enumerate(sweep)]
@@ -509,11 +537,11 @@ def run_ours(args):
                         "pinned host text + the 9 patterns in, per-pattern counters and ordered "
                         "offsets out in host memory; the text crosses PCIe once per step in 64 "
                         "MiB chunks, every pattern scanning each chunk as it lands",
-                        local_k if world == 1 else None)
+                        local_k if local_counts is not None else None)
         e2e_call = timed_e2e(e2e_call_step, 1,
                              "rk_scan_host per pattern (search_sequential on a host text: the "
                              "text crosses PCIe for every pattern, chunked DMA overlapped with "
-                             "the scan)", local_k if world == 1 else None)
+                             "the scan)", local_k if local_counts is not None else None)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -560,8 +588,13 @@ def run_ours(args):
             "gpu_launches": launches,
         }
         if comm is not None:
-            line["exchange"] = {"api": "rk_scan_sharded (C ABI, NCCL allgather-v)",
-                                "nccl": comm.info()}
+            line["exchange"] = {
+                "api": ("rk_scan_sharded_batch_async (C ABI: one NCCL group all-gathering every "
+                        "rank's counters and %d-offset slabs per pattern, ordered on the device; "
+                        "no host round trip per step)" % args.slab) if batch_async[0] else
+                       "rk_scan_sharded_batch (C ABI, NCCL allgather-v sized from the gathered "
+                       "counts: a list was over the slab)",
+                "nccl": comm.info()}
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()

@@ -233,6 +233,24 @@ int rk_scan_sharded_batch(rk_comm_t* comm, const uint8_t* d_text, uint64_t len, 
                           void* stream);
 
 /*
+ * rk_scan_sharded_batch_async -- rk_scan_sharded_batch with no host round trip: each
+ * pattern's local ordered offsets go into a fixed slab of `slab` offsets, ONE NCCL group
+ * all-gathers every rank's counters and slabs, and a device kernel writes the global
+ * ordered lists to d_outs[i] (up to caps[i]) and, per pattern, {matches, hash_hits,
+ * collisions, overflow} to d_counts[4 i .. 4 i + 3] (device memory, the totals over all
+ * ranks).  Everything is stream-ordered on `stream`; the call returns at once.  overflow
+ * = 1: some rank found more than `slab` matches, the list is incomplete -- run
+ * rk_scan_sharded_batch (or again with a larger slab).  The reference's ordered merge
+ * of range results (parallel.py:168-172) without a host synchronisation per step.
+ */
+int rk_scan_sharded_batch_async(rk_comm_t* comm, const uint8_t* d_text, uint64_t len,
+                                uint64_t byte_lo, const uint8_t* h_patterns,
+                                const uint32_t* h_lengths, const uint64_t* h_hashes, uint32_t P,
+                                const uint64_t* win_lo, const uint64_t* win_hi,
+                                int64_t* const* d_outs, const uint64_t* caps, uint64_t slab,
+                                uint64_t* d_counts, void* stream);
+
+/*
  * rk_multi_scan_sharded -- search_multi (matcher.py:125-157) over a text sharded across the
  * communicator's ranks (collective).  Each rank passes the bytes it holds, d_text = global
  * bytes [byte_lo, byte_lo + len) in device memory, and the window starts it owns,

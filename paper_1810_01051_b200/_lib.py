@@ -28,6 +28,7 @@ EXPORTS = (
     "rk_multi_scan", "rk_multi_scan_mixed", "rk_window_hashes", "rk_generate", "rk_launch_count",
     "rk_comm_get_unique_id", "rk_comm_init", "rk_comm_destroy", "rk_comm_info", "rk_shard_range",
     "rk_scan_sharded", "rk_comm_fetch", "rk_multi_scan_sharded", "rk_scan_sharded_batch",
+    "rk_scan_sharded_batch_async",
 )
 
 _lib = None
@@ -93,6 +94,9 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.rk_scan_sharded_batch.restype = ci
     lib.rk_scan_sharded_batch.argtypes = [vp, u8p, u64, u64, u8p, vp, vp, u32, vp, vp, vp, vp, vp,
                                           vp, vp, vp]
+    lib.rk_scan_sharded_batch_async.restype = ci
+    lib.rk_scan_sharded_batch_async.argtypes = [vp, u8p, u64, u64, u8p, vp, vp, u32, vp, vp, vp,
+                                                vp, u64, vp, vp]
     lib.rk_multi_scan_sharded.restype = ci
     lib.rk_multi_scan_sharded.argtypes = [vp, u8p, u64, u64, u64, u8p, vp, u32, vp, u64, u64, vp,
                                           vp, u64, pu64, vp]

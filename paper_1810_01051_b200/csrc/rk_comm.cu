@@ -121,7 +121,53 @@ struct rk_comm {
   unsigned long long* d_bcnt = nullptr;     // 4 x RK_BATCH_MAX_PATTERNS, this rank's
   unsigned long long* d_ballcnt = nullptr;  // every rank's, rank-major
   unsigned long long* h_ballcnt = nullptr;  // pinned mirror
+  // asynchronous batches: this rank's slabs (P x slab ordered offsets), every rank's,
+  // and the counters (P x 4, every rank's rank-major)
+  int64_t* a_local = nullptr;
+  int64_t* a_all = nullptr;
+  uint64_t a_local_cap = 0, a_all_cap = 0;
+  unsigned long long* a_cnt = nullptr;
+  unsigned long long* a_allcnt = nullptr;
 };
+
+namespace {
+struct SlabOuts {  // the kernel parameter: every pattern's output and its capacity
+  int64_t* out[RK_BATCH_MAX_PATTERNS];
+  uint64_t cap[RK_BATCH_MAX_PATTERNS];
+};
+
+// Block (pattern i, rank r): rank r's ordered offsets of pattern i (its slab) to their
+// place in the global list, after every earlier rank's; block (i, 0) also writes pattern
+// i's totals {matches, hash_hits, collisions, overflow} to counts.
+__global__ void slab_compact_kernel(const int64_t* __restrict__ all,
+                                    const unsigned long long* __restrict__ allcnt, uint32_t P,
+                                    uint64_t slab, int nranks, SlabOuts o,
+                                    unsigned long long* counts) {
+  const uint32_t i = blockIdx.x;
+  const int r = (int)blockIdx.y;
+  uint64_t prefix = 0, total = 0, hits = 0, coll = 0;
+  bool over = false;
+  for (int q = 0; q < nranks; ++q) {
+    const unsigned long long* c = allcnt + 4ull * ((uint64_t)q * P + i);
+    if (q < r) prefix += c[0];
+    total += c[0];
+    hits += c[1];
+    coll += c[2];
+    over |= c[0] > slab;
+  }
+  const uint64_t cnt = allcnt[4ull * ((uint64_t)r * P + i)];
+  const uint64_t n = cnt < slab ? cnt : slab;
+  const int64_t* src = all + ((uint64_t)r * P + i) * slab;
+  for (uint64_t j = threadIdx.x; j < n; j += blockDim.x)
+    if (prefix + j < o.cap[i]) o.out[i][prefix + j] = src[j];
+  if (r == 0 && threadIdx.x == 0) {
+    counts[4ull * i + 0] = total;
+    counts[4ull * i + 1] = hits;
+    counts[4ull * i + 2] = coll;
+    counts[4ull * i + 3] = over ? 1ull : 0ull;
+  }
+}
+}  // namespace
 
 extern "C" {
 
@@ -190,6 +236,10 @@ int rk_comm_destroy(rk_comm_t* k) {
   for (int64_t* p : k->b_local) cudaFree(p);
   cudaFree(k->d_bcnt);
   cudaFree(k->d_ballcnt);
+  cudaFree(k->a_local);
+  cudaFree(k->a_all);
+  cudaFree(k->a_cnt);
+  cudaFree(k->a_allcnt);
   cudaFreeHost(k->h_ballcnt);
   cudaFree(k->d_moff);
   cudaFree(k->d_midx);
@@ -474,6 +524,81 @@ int rk_scan_sharded_batch(rk_comm_t* k, const uint8_t* d_text, uint64_t len, uin
     }
   }
   RK_NCCL(api.GroupEnd());
+  return RK_OK;
+}
+
+int rk_scan_sharded_batch_async(rk_comm_t* k, const uint8_t* d_text, uint64_t len,
+                                uint64_t byte_lo, const uint8_t* h_patterns,
+                                const uint32_t* h_lengths, const uint64_t* h_hashes, uint32_t P,
+                                const uint64_t* win_lo, const uint64_t* win_hi,
+                                int64_t* const* d_outs, const uint64_t* caps, uint64_t slab,
+                                uint64_t* d_counts, void* stream) {
+  if (!k) return fail(RK_EINVAL, "communicator is NULL");
+  if (P < 1 || P > RK_BATCH_MAX_PATTERNS)
+    return fail(RK_EINVAL, "pattern count %u outside [1, %d]", P, RK_BATCH_MAX_PATTERNS);
+  if (!h_patterns || !h_lengths || !h_hashes || !win_lo || !win_hi || !d_outs || !caps ||
+      !d_counts)
+    return fail(RK_EINVAL, "NULL argument array");
+  if (slab < 1) return fail(RK_EINVAL, "slab must hold at least one offset");
+  uint64_t off = 0;
+  std::vector<uint64_t> pat_off(P);
+  SlabOuts o{};
+  for (uint32_t i = 0; i < P; ++i) {
+    const uint32_t m = h_lengths[i];
+    if (m < 1) return fail(RK_EINVAL, "pattern %u is empty", i);
+    pat_off[i] = off;
+    off += m;
+    if (win_hi[i] > win_lo[i]) {
+      if (win_lo[i] < byte_lo || win_hi[i] - byte_lo + m - 1 > len)
+        return fail(RK_EINVAL, "pattern %u: windows [%llu, %llu) need bytes the shard does not "
+                    "hold", i, (unsigned long long)win_lo[i], (unsigned long long)win_hi[i]);
+      if (!d_text) return fail(RK_EINVAL, "text pointer is NULL");
+    }
+    if (caps[i] && !d_outs[i]) return fail(RK_EINVAL, "pattern %u: NULL output", i);
+    o.out[i] = d_outs[i];
+    o.cap[i] = caps[i];
+  }
+  rk_ctx* c = k->ctx;
+  NcclApi& api = nccl();
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d_text && len && !is_device_pointer(d_text, c->device))
+    return fail(RK_EINVAL, "rk_scan_sharded_batch_async takes device texts of the context's device");
+  if (int r = enter(c, s)) return r;
+  if (!k->a_cnt) {
+    RK_CUDA(cudaMalloc(&k->a_cnt, 4ull * RK_BATCH_MAX_PATTERNS * sizeof(unsigned long long)));
+    RK_CUDA(cudaMalloc(&k->a_allcnt,
+                       4ull * RK_BATCH_MAX_PATTERNS * k->nranks * sizeof(unsigned long long)));
+  }
+  if (int r = grow(&k->a_local, &k->a_local_cap, (uint64_t)P * slab, false, s)) return r;
+  if (int r = grow(&k->a_all, &k->a_all_cap, (uint64_t)P * slab * k->nranks, false, s)) return r;
+  // 1. the local scans, each emitting its ordered offsets into its slab
+  for (uint32_t i = 0; i < P; ++i) {
+    const uint32_t m = h_lengths[i];
+    const uint64_t start = win_hi[i] > win_lo[i] ? win_lo[i] - byte_lo : 0;
+    const uint64_t stop = win_hi[i] > win_lo[i] ? win_hi[i] - byte_lo : 0;
+    if (int r = enqueue_scan(c, d_text, len, h_patterns + pat_off[i], m, h_hashes[i], start, stop,
+                             k->a_local + (uint64_t)i * slab, slab, (int64_t)byte_lo, s,
+                             (uint64_t*)(k->a_cnt + 4ull * i)))
+      return r;
+  }
+  // 2. one NCCL group: every rank's counters and slabs to every rank (fixed sizes, so no
+  //    host read between the scans and the exchange)
+  RK_NCCL(api.GroupStart());
+  ncclResult_t e = api.AllGather(k->a_cnt, k->a_allcnt, 4ull * P, ncclUint64, k->comm, s);
+  if (e == ncclSuccess)
+    e = api.AllGather(k->a_local, k->a_all, (uint64_t)P * slab, ncclInt64, k->comm, s);
+  if (e != ncclSuccess) {
+    api.GroupEnd();
+    return fail(RK_ENCCL, "ncclAllGather failed: %s", api.GetErrorString(e));
+  }
+  RK_NCCL(api.GroupEnd());
+  // 3. the global ordered lists, and the totals, on the device
+  slab_compact_kernel<<<dim3(P, (unsigned)k->nranks), 256, 0, s>>>(
+      k->a_all, k->a_allcnt, P, slab, k->nranks, o, (unsigned long long*)d_counts);
+  RK_CUDA(cudaGetLastError());
+  ++c->launches;
   return RK_OK;
 }
 

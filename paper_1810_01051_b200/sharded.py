@@ -217,6 +217,7 @@ class Communicator:
         # a context of its own: the sharded scans' scratch never interleaves with other
         # callers' scans on the device's shared context
         self.ctx = _lib.Context(self.device)
+        self._batch_key, self._batch_args = None, None
         h = ctypes.c_void_p()
         _lib.check(L.rk_comm_init(self.ctx.handle, uid, self.world, self.rank, ctypes.byref(h)))
         self.handle = h
@@ -281,14 +282,10 @@ class Communicator:
         import numpy as np
 
         from . import _scan
-        from .rkhash import hash_full
 
         L = _lib.lib()
-        pats = [_scan._host_bytes(_scan.as_u8(p)) for p in patterns]
-        P = len(pats)
-        flat = np.concatenate(pats)
-        lengths = np.array([p.size for p in pats], dtype=np.uint32)
-        hashes = np.array([hash_full(p.tobytes()) for p in pats], dtype=np.uint64)
+        flat, lengths, hashes = self._batch_arrays(patterns)
+        P = int(lengths.size)
         lo = np.array([r[0] for r in ranges], dtype=np.uint64)
         hi = np.array([r[1] for r in ranges], dtype=np.uint64)
         ptrs = np.array([o.data_ptr() for o in outs], dtype=np.uint64)
@@ -303,6 +300,54 @@ class Communicator:
                 co.ctypes.data, hh.ctypes.data, s))
         return [(outs[i][: int(mt[i])] if mt[i] <= caps[i] else None, int(mt[i]), int(co[i]),
                  int(hh[i])) for i in range(P)]
+
+    def _batch_arrays(self, patterns):
+        """(flat bytes, lengths, hashes) of a pattern list, kept for the next call with the
+        same patterns (hash_full of a 1 KiB pattern in Python costs ~0.1 ms)."""
+        import numpy as np
+
+        from . import _scan
+        from .rkhash import hash_full
+
+        key = tuple(bytes(p) if isinstance(p, (bytes, bytearray, memoryview)) else None
+                    for p in patterns)
+        if None not in key and key == self._batch_key:
+            return self._batch_args
+        pats = [_scan._host_bytes(_scan.as_u8(p)) for p in patterns]
+        args = (np.concatenate(pats), np.array([p.size for p in pats], dtype=np.uint32),
+                np.array([hash_full(p.tobytes()) for p in pats], dtype=np.uint64))
+        if None not in key:
+            self._batch_key, self._batch_args = key, args
+        return args
+
+    def scan_batch_async(self, text, patterns, ranges, byte_lo: int, outs, counts, *,
+                         slab: int = 4096, stream=None) -> None:
+        """rk_scan_sharded_batch_async: as scan_batch, with no host round trip -- every
+        rank's first ``slab`` ordered offsets per pattern are all-gathered in one NCCL
+        group and ordered into ``outs[i]`` on the device; row i of ``counts`` (a CUDA int64
+        tensor of P x 4) receives [matches, hash_hits, collisions, overflow], the totals
+        over all ranks, stream-ordered; overflow = 1 when some rank found more than
+        ``slab`` (the list is then incomplete: use scan_batch)."""
+        import numpy as np
+
+        from . import _scan
+
+        L = _lib.lib()
+        flat, lengths, hashes = self._batch_arrays(patterns)
+        P = int(lengths.size)
+        if counts.numel() < 4 * P or not counts.is_cuda:
+            raise ValueError("counts must be a CUDA tensor of at least 4 x P int64")
+        lo = np.array([r[0] for r in ranges], dtype=np.uint64)
+        hi = np.array([r[1] for r in ranges], dtype=np.uint64)
+        ptrs = np.array([o.data_ptr() for o in outs], dtype=np.uint64)
+        caps = np.array([o.numel() for o in outs], dtype=np.uint64)
+        s = _scan._stream(self.device) if stream is None else stream
+        with self.ctx.lock:
+            _lib.check(L.rk_scan_sharded_batch_async(
+                self.handle, text.data_ptr() if text.numel() else 0, int(text.numel()), byte_lo,
+                flat.ctypes.data, lengths.ctypes.data, hashes.ctypes.data, P, lo.ctypes.data,
+                hi.ctypes.data, ptrs.ctypes.data, caps.ctypes.data, int(slab),
+                counts.data_ptr(), s))
 
     def multi_scan(self, text, patterns, start_lo: int, start_hi: int, byte_lo: int,
                    n_total: int, *, cap: int = 1 << 16, stream=None):

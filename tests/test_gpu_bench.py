@@ -50,3 +50,19 @@ def test_bench_two_rank_plumbing(gpu):
     assert len(lines) == 1  # rank 0 alone prints
     line = lines[0]
     assert line["n_gpus"] == 2 and line["scaling"] == "weak" and line["value"] > 0
+
+
+def test_bench_exchange_path_one_rank(gpu):
+    """The N > 1 step's exchange (rk_scan_sharded_batch_async through the C-ABI NCCL
+    communicator, no host round trip per step) run at one rank: the line reports it, the
+    counts it gathered match the plain path's, and a slab too small for a list falls back
+    to the synchronous batch."""
+    (plain,) = _run([sys.executable, "bench.py", *SMALL])
+    (line,) = _run([sys.executable, "bench.py", "--force-comm", *SMALL])
+    assert line["exchange"]["api"].startswith("rk_scan_sharded_batch_async")
+    assert line["matches_per_m"] == plain["matches_per_m"] and line["value"] > 0
+    (small,) = _run([sys.executable, "bench.py", "--force-comm", "--slab", "1", *SMALL])
+    over = max(plain["matches_per_m"].values()) > 1
+    assert small["exchange"]["api"].startswith(
+        "rk_scan_sharded_batch (" if over else "rk_scan_sharded_batch_async")
+    assert small["matches_per_m"] == plain["matches_per_m"]

@@ -173,3 +173,37 @@ def test_sharded_batch(comm):
     # the second call reuses the grown buffers (a steady workload pays the second round once)
     res2 = comm.scan_batch(t, pats, ranges, 0, outs)
     assert [r[1:] for r in res2] == [r[1:] for r in res]
+
+
+def test_sharded_batch_async(comm):
+    """rk_scan_sharded_batch_async (one rank): the same lists and totals as the synchronous
+    batch, with no host round trip; a pattern over its slab reports overflow, an output
+    cap below the total keeps only its prefix; back-to-back calls stay exact."""
+    import torch
+
+    rng = np.random.default_rng(46)
+    n = 16 << 20
+    host = rng.integers(0, 4, n, dtype=np.uint8) + 65
+    host[(2 << 20): (2 << 20) + 50000] = 65
+    t = torch.from_numpy(host).cuda()
+    pats = [host[x:x + m].tobytes() for x, m in ((100, 4), (5000, 8), (70000, 16), (9 << 20, 32),
+                                                   (123, 64), (4567, 128))]
+    pats += [b"AAAA", b"ACGTACGTTT"]
+    ranges = [(1000, n - len(p) + 1 - 7) for p in pats]
+    ref_outs = [torch.empty(1 << 20, dtype=torch.int64, device="cuda") for _ in pats]
+    ref = comm.scan_batch(t, pats, ranges, 0, ref_outs)
+    outs = [torch.full((1 << 20,), -1, dtype=torch.int64, device="cuda") for _ in pats]
+    outs[1] = torch.full((3,), -1, dtype=torch.int64, device="cuda")  # a cap below the total
+    counts = torch.zeros((len(pats), 4), dtype=torch.int64, device="cuda")
+    slab = 8192
+    for _ in range(3):
+        comm.scan_batch_async(t, pats, ranges, 0, outs, counts, slab=slab)
+    torch.cuda.synchronize()
+    c = counts.cpu().numpy()
+    for i, (offs, k, coll, hits) in enumerate(ref):
+        assert (int(c[i, 0]), int(c[i, 1]), int(c[i, 2])) == (k, hits, coll), i
+        assert int(c[i, 3]) == (1 if k > slab else 0), i
+        if k <= slab:
+            w = min(k, outs[i].numel())
+            assert torch.equal(outs[i][:w], offs[:w]), i
+    assert int(c[6, 3]) == 1  # the 'AAAA' run is over the slab
