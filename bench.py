@@ -11,7 +11,8 @@ from the corpus as rkmatch.bench._make_pattern does).  One step = the whole swee
 
 N > 1 runs under torchrun, one rank per GPU: weak scaling, each rank owns 1 GiB of the
 global N GiB corpus plus an (m-1)-byte halo, scans it, and the global ordered position
-list is returned to every rank by the C ABI's rk_scan_sharded (NCCL allgather-v).
+lists are returned to every rank by the C ABI's rk_scan_sharded_batch_async (one NCCL
+group per step, no host round trip).
 `--workload C4` runs BASELINE configs[3] instead: 16 GiB DNA, m = 32, strong scaling.  `--impl reference` times the reference
 algorithm (the C restatement in oracle/ of rkmatch._scan_range + search_parallel's range
 partition) on the host cores on a bounded sample of the same workload.
@@ -634,15 +635,32 @@ def run_c4(args, world, rank, dev):
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
     out = torch.empty(1 << 20, dtype=torch.int64, device=f"cuda:{dev}")
+    acounts = torch.zeros((1, 4), dtype=torch.int64, device=f"cuda:{dev}")
     res = {}
+    use_async = [True]
 
     def step(_ev=None):
-        res["r"] = comm.scan(text, pat, a, b, blo, cap=out.numel(), out=out, stream=sptr)
+        if use_async[0]:
+            # the exchange with no host round trip (one NCCL group: counters + a fixed slab
+            # per rank, ordered on the device) -- a strong-scaling step is ~0.3 ms at N = 8
+            comm.scan_batch_async(text, [pat], [(a, b)], blo, [out], acounts, slab=args.slab,
+                                  stream=sptr)
+        else:
+            res["r"] = comm.scan(text, pat, a, b, blo, cap=out.numel(), out=out, stream=sptr)
 
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
-    offs, k, coll, hits = res["r"]
+    ac = acounts.cpu().numpy()[0]
+    if ac[3]:  # a rank's list is over the slab: the synchronous exchange
+        use_async[0] = False
+        for _ in range(max(args.warmup, 3)):
+            step()
+        torch.cuda.synchronize()
+        offs, k, coll, hits = res["r"]
+    else:
+        k, hits, coll = int(ac[0]), int(ac[1]), int(ac[2])
+        offs = out[:k]
     got = set(offs.cpu().tolist())
     assert set(plants) <= got and hits == k + coll
     l0 = comm.ctx.launches
@@ -698,7 +716,10 @@ def run_c4(args, world, rank, dev):
                          "kernel": "rk_scan_kernel<32> (+ emit + exchange)",
                          "algorithmic_bytes": "shard bytes + 8*matches per step"},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
-            "exchange": {"api": "rk_scan_sharded (C ABI, NCCL allgather-v)", "nccl": comm.info()},
+            "exchange": {"api": ("rk_scan_sharded_batch_async (C ABI: one NCCL group, counters + "
+                                 "a %d-offset slab per rank, ordered on the device)" % args.slab)
+                                if use_async[0] else "rk_scan_sharded (C ABI, NCCL allgather-v)",
+                         "nccl": comm.info()},
         }
         line["roofline"]["frac"] = line["roofline"]["achieved"] / peak
         print(json.dumps(line), flush=True)
