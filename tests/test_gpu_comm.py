@@ -207,3 +207,32 @@ def test_sharded_batch_async(comm):
             w = min(k, outs[i].numel())
             assert torch.equal(outs[i][:w], offs[:w]), i
     assert int(c[6, 3]) == 1  # the 'AAAA' run is over the slab
+
+
+def test_sharded_batch_async_edges(comm):
+    """The asynchronous batch at its limits: 64 patterns (RK_BATCH_MAX_PATTERNS), some with
+    no windows (win_hi <= win_lo) or no output (cap 0), a slab of one offset; every total
+    equals the synchronous batch's and the overflow flags say which lists are complete."""
+    import torch
+
+    rng = np.random.default_rng(47)
+    n = 4 << 20
+    host = rng.integers(0, 4, n, dtype=np.uint8) + 65
+    t = torch.from_numpy(host).cuda()
+    pats = [host[x:x + m].tobytes() for x, m in zip(rng.integers(0, n - 64, 64), rng.integers(3, 40, 64))]
+    ranges = [(100, n - len(p) + 1) if i % 7 else (500, 500) for i, p in enumerate(pats)]
+    ref_outs = [torch.empty(1 << 16, dtype=torch.int64, device="cuda") for _ in pats]
+    ref = comm.scan_batch(t, pats, ranges, 0, ref_outs)
+    outs = [torch.full((1 << 16,) if i % 5 else (0,), -1, dtype=torch.int64, device="cuda")
+            for i in range(len(pats))]
+    counts = torch.zeros((len(pats), 4), dtype=torch.int64, device="cuda")
+    comm.scan_batch_async(t, pats, ranges, 0, outs, counts, slab=1)
+    torch.cuda.synchronize()
+    c = counts.cpu().numpy()
+    for i, (offs, k, coll, hits) in enumerate(ref):
+        assert (int(c[i, 0]), int(c[i, 1]), int(c[i, 2])) == (k, hits, coll), i
+        assert int(c[i, 3]) == (1 if k > 1 else 0), i
+        if k == 1 and outs[i].numel():
+            assert torch.equal(outs[i][:1], offs[:1]), i
+        if i % 7 == 0:
+            assert k == 0
